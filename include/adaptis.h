@@ -1,0 +1,218 @@
+/*
+ * adaptis.h — C ABI of libadaptis.so: batched evaluation of the AdaPtis
+ * Pipeline Performance Model (arXiv 2509.23722, Alg. 1) over an enumerated
+ * space of (model partition, model placement, workload schedule) candidates,
+ * reduced to the best plan that satisfies the memory constraint (Eq. 1-2).
+ *
+ * Citation convention: "P:n" = line n of the paper text, with the
+ * section / algorithm / equation it falls in; "R<k>" = reading k in DESIGN.md
+ * (where the paper is silent or ambiguous).
+ *
+ * Conventions for every call
+ *  - All integers are host-endian. Inputs are structure-of-arrays.
+ *  - Ownership: every pointer is owned by the caller. Inputs are only read
+ *    during the call (and copied to the device); the caller may free them on
+ *    return. Outputs are caller-allocated (host memory, or device memory when
+ *    `out_on_device` is non-zero).
+ *  - Errors: every call returns an adaptis_status. No C++ exception crosses
+ *    the ABI. After a failure on a call that takes a context,
+ *    adaptis_last_error(ctx) names the offending field, e.g.
+ *    "layers.t_f[3] < 1". Calls without a context write the message to a
+ *    thread-local buffer readable through adaptis_last_error(NULL).
+ *  - Threads: one context per thread at a time; distinct contexts may be used
+ *    concurrently.
+ *  - Determinism: results are pure functions of the inputs (integer ticks and
+ *    bytes, total-order argmin key), identical for any number of GPUs.
+ */
+#ifndef ADAPTIS_H
+#define ADAPTIS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADAPTIS_MAX_P 32      /* pipeline devices per candidate (lanes of one warp)   */
+#define ADAPTIS_MAX_V 4       /* virtual stages per device                            */
+#define ADAPTIS_MAX_S 64      /* stages S = p*v                                       */
+#define ADAPTIS_MAX_GROUPS 4  /* v-groups per search space                            */
+
+typedef enum {
+  ADAPTIS_OK = 0,
+  ADAPTIS_EINVAL = 1,      /* invalid argument; adaptis_last_error names the field            */
+  ADAPTIS_EINFEASIBLE = 2, /* search: no candidate satisfies Eq. 2                */
+  ADAPTIS_EOVERFLOW = 3,   /* makespan bound and index do not fit the 63-bit argmin key       */
+  ADAPTIS_ECUDA = 4,       /* CUDA runtime error (message in adaptis_last_error)              */
+  ADAPTIS_ECOLL = 5        /* the cross-GPU allreduce callback failed                         */
+} adaptis_status;
+
+/* Model placement families (§2.3): SEQ = S-1F1B sequential (v = 1),
+ * INTERLEAVED = I-1F1B virtual stages (stage s -> device s mod p),
+ * WAVE = Hanayo wave (stage c*p+j -> device j for even c, p-1-j for odd c). */
+enum { ADAPTIS_SEQ = 0, ADAPTIS_INTERLEAVED = 1, ADAPTIS_WAVE = 2 };
+
+/* Workload-scheduling policies (§2.4, §4.3, readings R9-R14):
+ * GPIPE and ONEF1B run B and W fused; ZB and GREEDY split them. */
+enum { ADAPTIS_GPIPE = 0, ADAPTIS_ONEF1B = 1, ADAPTIS_ZB = 2, ADAPTIS_GREEDY = 3 };
+
+/* Partition spaces (R19): FULL = every contiguous S-way split of the L rows;
+ * BALL = cut vectors within L1 distance `radius` of a seed partition. */
+enum { ADAPTIS_PART_FULL = 0, ADAPTIS_PART_BALL = 1 };
+
+/* Per-candidate status codes (adaptis_results_soa.status, adaptis_result.status). */
+enum {
+  ADAPTIS_CAND_OK = 0,
+  ADAPTIS_CAND_INVALID = 1,  /* BALL decode whose cuts are not strictly increasing in [1, L-1] */
+  ADAPTIS_CAND_OVER_CAP = 2, /* some M_d > M_d^capacity (Eq. 2)                    */
+  ADAPTIS_CAND_STUCK = 3     /* the schedule cannot complete (cyclic wait / memory gate)        */
+};
+
+/* Fixed combo table (R12). Bit k of adaptis_group.combo_mask enables combo k.
+ *   v == 1 : 0 SEQ x GPIPE, 1 SEQ x ONEF1B, 2 SEQ x ZB, 3 SEQ x GREEDY
+ *   v >= 2 : 0 INT x GPIPE, 1 INT x ONEF1B, 2 INT x ZB, 3 INT x GREEDY,
+ *            4 WAVE x GPIPE, 5 WAVE x GREEDY                                       */
+
+/* Profiled data per layer row: ProfiledCompCost(l) and ProfiledMemCost(l) of
+ * Alg. 1 Step 1, split by computation type F / B / W (P:152-153,
+ * P:181). Row 0 is the embedding, row L-1 the LM head (R24). Each pointer is a
+ * host array of L int64 values. */
+typedef struct {
+  int32_t L;                 /* rows, 2 <= L <= 32767                                        */
+  const int64_t* t_f;        /* forward ticks per micro-batch, >= 1 (R17)                    */
+  const int64_t* t_b;        /* input-gradient ticks, >= 1                                   */
+  const int64_t* t_w;        /* parameter-gradient ticks, >= 1                               */
+  const int64_t* act_bytes;  /* held from F start to B end, per micro-batch, >= 0 (R16)      */
+  const int64_t* stash_bytes;/* held from F start to W end (B end when fused), >= 0          */
+  const int64_t* weight_bytes;/* static from t = 0, >= 0                                     */
+  const int64_t* grad_bytes; /* static from t = 0, >= 0                                      */
+  const int64_t* comm_ticks; /* p2p latency of the boundary after row l, >= 0 (R3-R5);
+                                entry L-1 is ignored                                         */
+} adaptis_layers;
+
+typedef struct {
+  adaptis_layers layers;
+  int32_t p;                  /* pipeline devices P, 1 <= p <= 32                            */
+  int32_t m;                  /* micro-batches nmb, 1 <= m <= 65535                          */
+  int64_t mem_cap_bytes;      /* M_d^capacity (uniform); INT64_MAX = unconstrained           */
+  double  tick_seconds;       /* seconds per tick, throughput only (R22)                     */
+  int64_t tokens_per_microbatch; /* throughput only (TS)                              */
+} adaptis_problem;
+
+typedef struct {              /* one group of the space per virtual-stage count v            */
+  int32_t v;                  /* 1..4; S = p*v <= min(64, L); v > 1 requires m % p == 0 (R10)*/
+  int32_t part_mode;          /* ADAPTIS_PART_FULL or ADAPTIS_PART_BALL                       */
+  int32_t radius;             /* BALL only: L1 radius R >= 0                                  */
+  const int16_t* seed_cuts;   /* BALL only: S-1 interior cuts, or NULL = min-max seed (R20)   */
+  uint32_t combo_mask;        /* non-empty subset of the combo table above                    */
+} adaptis_group;
+
+typedef struct {
+  int32_t n_groups;           /* 1..4; index order follows group order (R19)                  */
+  adaptis_group group[ADAPTIS_MAX_GROUPS];
+} adaptis_space;
+
+/* A decoded candidate: stage s owns rows [cuts[s], cuts[s+1]), cuts[0] = 0,
+ * cuts[S] = L ("consecutive layers"; Layers(s) of Table `tab: notations`). */
+typedef struct {
+  int32_t v, placement, policy, S;
+  int16_t cuts[ADAPTIS_MAX_S + 1];
+} adaptis_plan;
+
+/* Per-candidate outputs, structure of arrays, `count` entries each. Any
+ * pointer may be NULL to skip that output. */
+typedef struct {
+  int64_t* makespan;         /* max_d T_d (Eq. 1) in ticks; INT64_MAX unless status == 0    */
+  int64_t* peak_mem_bytes;   /* max_d M_d (Alg. 1 Step 3); 0 for status 1 and 3            */
+  float*   bubble_ratio;     /* 1 - sum_d busy_d / (p * makespan) (R7); 0 unless status 0   */
+  uint8_t* status;           /* ADAPTIS_CAND_*                                              */
+} adaptis_results_soa;
+
+typedef struct {             /* host-side result of one candidate                            */
+  int64_t makespan, peak_mem_bytes;
+  float   bubble_ratio;
+  double  throughput;        /* tokens/s = m * tokens_per_microbatch / (makespan * tick_s)   */
+  uint8_t status;
+} adaptis_result;
+
+typedef struct {             /* output of adaptis_search                                     */
+  uint64_t index;            /* global index of the winner (lowest index among ties, R18)    */
+  adaptis_plan plan;
+  adaptis_result result;
+  int32_t p;
+  int64_t T_d[ADAPTIS_MAX_P];    /* per-device completion time (Alg. 1 Step 3 output)        */
+  int64_t busy_d[ADAPTIS_MAX_P]; /* per-device compute ticks                                  */
+  int64_t M_d[ADAPTIS_MAX_P];    /* per-device peak memory, static + dynamic (Eq. 2)          */
+  uint64_t n_candidates;     /* |space| (all ranks)                                          */
+  uint64_t n_evaluated;      /* candidates this rank evaluated                               */
+  uint64_t n_invalid;        /* of those, invalid decodes (status 1)                         */
+  float    kernel_ms;        /* device time of this rank's evaluation kernels                */
+} adaptis_best;
+
+typedef struct adaptis_ctx adaptis_ctx;
+typedef struct adaptis_prepared adaptis_prepared;
+
+/* Cross-GPU reduction hook for world > 1: must replace *dev_key (one int64 in
+ * device memory of this rank's GPU) by its minimum over all ranks, ordered
+ * after the work already queued on `cuda_stream`, and return 0 on success.
+ * The Python binding installs torch.distributed.all_reduce(MIN) over an NCCL
+ * process group (one 8-byte allreduce per search). */
+typedef int (*adaptis_allreduce_min_fn)(int64_t* dev_key, void* cuda_stream, void* user);
+
+/* Create a context bound to `cuda_device`. rank/world describe the candidate
+ * sharding (block-cyclic chunks of 65536 indices, chunk k -> rank k mod world).
+ * EINVAL if world < 1 or rank not in [0, world); ECUDA if the device is
+ * unusable. */
+adaptis_status adaptis_ctx_create(int cuda_device, int rank, int world, adaptis_ctx** out);
+void           adaptis_ctx_destroy(adaptis_ctx* ctx);
+adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_allreduce_min_fn fn, void* user);
+/* The CUDA stream (cudaStream_t) every kernel of this context is queued on. */
+void*          adaptis_ctx_stream(adaptis_ctx* ctx);
+/* Number of kernel launches this context has issued since creation. */
+uint64_t       adaptis_ctx_launch_count(const adaptis_ctx* ctx);
+
+/* |space| for this problem (the candidate space). EINVAL on an
+ * invalid problem/space; EOVERFLOW if the count does not fit in 63 bits. */
+adaptis_status adaptis_space_size(const adaptis_problem* problem, const adaptis_space* space,
+                                  uint64_t* n_out);
+
+/* Decode a global index into its (v, placement, policy, cuts) candidate, in the
+ * canonical order of R19. EINVAL if index >= |space|. An invalid BALL decode
+ * is still returned (its cuts are not strictly increasing). */
+adaptis_status adaptis_decode(const adaptis_problem* problem, const adaptis_space* space,
+                              uint64_t index, adaptis_plan* out);
+
+/* Validate, derive host tables (prefix sums, seeds, counts) and upload them to
+ * the device once, so repeated evaluations start with inputs resident in HBM. */
+adaptis_status adaptis_prepare(adaptis_ctx* ctx, const adaptis_problem* problem,
+                               const adaptis_space* space, adaptis_prepared** out);
+void           adaptis_prepared_free(adaptis_prepared* prep);
+
+/* Evaluate candidates [first, first+count) of the space (Alg. 1 Steps 1-3 per
+ * candidate) and write per-candidate results. Unlike search this is not
+ * sharded: the context's GPU evaluates the whole range. */
+adaptis_status adaptis_eval_batch(adaptis_ctx* ctx, const adaptis_problem* problem,
+                                  const adaptis_space* space, uint64_t first, uint64_t count,
+                                  const adaptis_results_soa* out, int out_on_device);
+adaptis_status adaptis_eval_prepared(adaptis_ctx* ctx, adaptis_prepared* prep,
+                                     uint64_t first, uint64_t count,
+                                     const adaptis_results_soa* out, int out_on_device);
+
+/* Search the whole space for min (makespan, index) over candidates with
+ * status 0 (Eq. 1-2, ties to the lowest index, R18). With world > 1 every
+ * rank evaluates its shard and the allreduce hook combines the packed keys;
+ * every rank returns the same `out`. EINFEASIBLE if no candidate is feasible
+ * (out->index = UINT64_MAX). */
+adaptis_status adaptis_search(adaptis_ctx* ctx, const adaptis_problem* problem,
+                              const adaptis_space* space, adaptis_best* out);
+adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* prep,
+                                       adaptis_best* out);
+
+/* Message of the last failure on `ctx` (or of the calling thread when ctx is NULL). */
+const char*    adaptis_last_error(const adaptis_ctx* ctx);
+const char*    adaptis_status_str(adaptis_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADAPTIS_H */

@@ -1,0 +1,300 @@
+"""ctypes wrapper of the C oracle (oracle.c). TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+--impl reference legs may import this module. It never imports the CUDA
+package; inputs arrive as plain numpy arrays (workloads.Problem/Space objects
+are duck-typed: only their attributes are read).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "liboracle.so")
+SRC = os.path.join(HERE, "oracle.c")
+HDR = os.path.join(HERE, "oracle.h")
+MAXS, MAXP = 64, 32
+INT64_MAX = (1 << 63) - 1
+UINT64_MAX = (1 << 64) - 1
+
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain C11 + pthreads)."""
+    stale = (not os.path.exists(LIB) or
+             max(os.path.getmtime(SRC), os.path.getmtime(HDR)) > os.path.getmtime(LIB))
+    if force or stale:
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-fPIC", "-shared", "-pthread",
+                               SRC, "-o", LIB])
+    return LIB
+
+
+class _Problem(C.Structure):
+    _fields_ = [("L", C.c_int)] + [(n, C.POINTER(C.c_int64)) for n in
+                                   ("t_f", "t_b", "t_w", "act", "stash", "weight", "grad", "comm")] + \
+               [("p", C.c_int), ("m", C.c_int), ("cap", C.c_int64)]
+
+
+class _Plan(C.Structure):
+    _fields_ = [("v", C.c_int), ("placement", C.c_int), ("policy", C.c_int), ("S", C.c_int),
+                ("cuts", C.c_int * (MAXS + 1))]
+
+
+class _Result(C.Structure):
+    _fields_ = [("status", C.c_int), ("makespan", C.c_int64), ("peak_mem", C.c_int64),
+                ("bubble", C.c_double)] + [(n, C.c_int64 * MAXP) for n in
+                                           ("T_d", "busy_d", "M_d", "static_d")]
+
+
+class _Trace(C.Structure):
+    _fields_ = [("cap_per_dev", C.c_int), ("n", C.c_int * MAXP),
+                ("kind", C.POINTER(C.c_int)), ("stage", C.POINTER(C.c_int)),
+                ("mb", C.POINTER(C.c_int)), ("start", C.POINTER(C.c_int64))]
+
+
+class _Group(C.Structure):
+    _fields_ = [("v", C.c_int), ("part_mode", C.c_int), ("radius", C.c_int),
+                ("seed_cuts", C.POINTER(C.c_int)), ("combo_mask", C.c_uint)]
+
+
+class _Space(C.Structure):
+    _fields_ = [("n_groups", C.c_int), ("group", _Group * 4)]
+
+
+class _Best(C.Structure):
+    _fields_ = [("index", C.c_uint64), ("makespan", C.c_int64), ("plan", _Plan),
+                ("n_total", C.c_uint64), ("n_invalid", C.c_uint64), ("n_simulated", C.c_uint64),
+                ("n_feasible", C.c_uint64)]
+
+
+CB = C.CFUNCTYPE(None, C.c_uint64, C.POINTER(_Plan), C.c_void_p)
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(LIB)
+            L.orc_simulate.argtypes = [C.POINTER(_Problem), C.POINTER(_Plan), C.POINTER(_Result),
+                                       C.POINTER(_Trace)]
+            L.orc_longest_path.argtypes = [C.POINTER(_Problem), C.POINTER(_Plan), C.c_int,
+                                           C.POINTER(_Trace), C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+            L.orc_fixed_order.argtypes = [C.POINTER(_Problem), C.POINTER(_Plan), C.c_int,
+                                          C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                          C.POINTER(C.c_int), C.c_int]
+            L.orc_seed_minmax.restype = C.c_int64
+            L.orc_seed_minmax.argtypes = [C.c_int, C.POINTER(C.c_int64), C.c_int, C.POINTER(C.c_int)]
+            L.orc_device_of_stage.argtypes = [C.c_int] * 4
+            L.orc_combo.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+            L.orc_space_size.restype = C.c_uint64
+            L.orc_space_size.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.POINTER(C.c_int)]
+            L.orc_enumerate.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), CB, C.c_void_p]
+            L.orc_decode.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.c_uint64,
+                                     C.POINTER(_Plan)]
+            L.orc_eval_indices.argtypes = [C.POINTER(_Problem), C.POINTER(_Space),
+                                           C.POINTER(C.c_uint64), C.c_uint64, C.c_int,
+                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_double), C.POINTER(C.c_uint8)]
+            L.orc_search.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.c_int, C.c_int,
+                                     C.POINTER(_Best)]
+            _lib = L
+    return _lib
+
+
+def _i64p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+class _Ctx:
+    """Keeps numpy arrays alive while C structs point into them."""
+
+    def __init__(self, pr, sp=None):
+        self.keep = []
+        cols = {}
+        for n in ("t_f", "t_b", "t_w", "act", "stash", "weight", "grad", "comm"):
+            a = np.ascontiguousarray(np.asarray(getattr(pr, n), dtype=np.int64))
+            self.keep.append(a)
+            cols[n] = _i64p(a)
+        self.pr = _Problem(L=len(pr.t_f), p=pr.p, m=pr.m, cap=int(pr.cap), **cols)
+        self.sp = None
+        if sp is not None:
+            s = _Space()
+            s.n_groups = len(sp.groups)
+            for i, g in enumerate(sp.groups):
+                seed = None
+                if g.seed_cuts is not None:
+                    arr = (C.c_int * len(g.seed_cuts))(*g.seed_cuts)
+                    self.keep.append(arr)
+                    seed = C.cast(arr, C.POINTER(C.c_int))
+                s.group[i] = _Group(v=g.v, part_mode=g.part_mode, radius=g.radius,
+                                    seed_cuts=seed, combo_mask=g.combo_mask)
+            self.sp = s
+
+
+def make_plan(v, placement, policy, cuts, L=None):
+    """cuts: interior cuts (S-1 values) or the full list [0, ..., L]."""
+    cuts = list(cuts)
+    if L is not None and (not cuts or cuts[0] != 0 or cuts[-1] != L):
+        cuts = [0] + cuts + [L]
+    pl = _Plan(v=v, placement=placement, policy=policy, S=len(cuts) - 1)
+    for i, c in enumerate(cuts):
+        pl.cuts[i] = c
+    return pl
+
+
+def plan_dict(pl):
+    return {"v": pl.v, "placement": pl.placement, "policy": pl.policy, "S": pl.S,
+            "cuts": [pl.cuts[i] for i in range(pl.S + 1)]}
+
+
+def simulate(pr, v, placement, policy, cuts, trace=False):
+    """Alg. 1 for one candidate. cuts = interior cuts. Returns a dict."""
+    ctx = _Ctx(pr)
+    pl = make_plan(v, placement, policy, cuts, L=len(pr.t_f))
+    res = _Result()
+    tr_p = None
+    if trace:
+        capd = 3 * pl.S * pr.m
+        arrs = [np.zeros(capd * pr.p, np.int32) for _ in range(3)] + [np.zeros(capd * pr.p, np.int64)]
+        tr = _Trace(cap_per_dev=capd, kind=arrs[0].ctypes.data_as(C.POINTER(C.c_int)),
+                    stage=arrs[1].ctypes.data_as(C.POINTER(C.c_int)),
+                    mb=arrs[2].ctypes.data_as(C.POINTER(C.c_int)), start=_i64p(arrs[3]))
+        tr_p = C.pointer(tr)
+    rc = lib().orc_simulate(C.byref(ctx.pr), C.byref(pl), C.byref(res), tr_p)
+    if rc != 0:
+        raise RuntimeError("oracle internal inconsistency")
+    p = pr.p
+    out = {"status": res.status, "makespan": res.makespan, "peak_mem": res.peak_mem,
+           "bubble": res.bubble, "T_d": list(res.T_d[:p]), "busy_d": list(res.busy_d[:p]),
+           "M_d": list(res.M_d[:p]), "static_d": list(res.static_d[:p])}
+    if trace:
+        lists = []
+        for d in range(p):
+            n = tr.n[d]
+            o = d * capd
+            lists.append([(int(arrs[0][o + i]), int(arrs[1][o + i]), int(arrs[2][o + i]),
+                           int(arrs[3][o + i])) for i in range(n)])
+        out["trace"] = lists
+    return out
+
+
+def longest_path(pr, v, placement, cuts, fused, lists):
+    """Independent longest-path checker over explicit per-device lists of
+    (kind, stage, mb). Returns (makespan, T_d, starts) or None on a cycle."""
+    ctx = _Ctx(pr)
+    pl = make_plan(v, placement, 0, cuts, L=len(pr.t_f))
+    capd = max(1, max(len(x) for x in lists))
+    p = pr.p
+    kind = np.zeros(capd * p, np.int32)
+    stage = np.zeros(capd * p, np.int32)
+    mb = np.zeros(capd * p, np.int32)
+    start = np.zeros(capd * p, np.int64)
+    tr = _Trace(cap_per_dev=capd, kind=kind.ctypes.data_as(C.POINTER(C.c_int)),
+                stage=stage.ctypes.data_as(C.POINTER(C.c_int)),
+                mb=mb.ctypes.data_as(C.POINTER(C.c_int)), start=_i64p(start))
+    for d, lst in enumerate(lists):
+        tr.n[d] = len(lst)
+        for i, t in enumerate(lst):
+            kind[d * capd + i], stage[d * capd + i], mb[d * capd + i] = t[0], t[1], t[2]
+    st = np.zeros(capd * p, np.int64)
+    mk = C.c_int64()
+    Td = (C.c_int64 * MAXP)()
+    cyc = lib().orc_longest_path(C.byref(ctx.pr), C.byref(pl), int(fused), C.byref(tr), _i64p(st),
+                                 C.byref(mk), Td)
+    if cyc:
+        return None
+    starts = [[int(st[d * capd + i]) for i in range(len(lists[d]))] for d in range(p)]
+    return mk.value, list(Td[:p]), starts
+
+
+def fixed_order(pr, v, placement, policy, cuts, d):
+    ctx = _Ctx(pr)
+    pl = make_plan(v, placement, policy, cuts, L=len(pr.t_f))
+    cap = 2 * pr.m * v
+    k = (C.c_int * cap)(); s = (C.c_int * cap)(); j = (C.c_int * cap)()
+    n = lib().orc_fixed_order(C.byref(ctx.pr), C.byref(pl), d, k, s, j, cap)
+    return [(k[i], s[i], j[i]) for i in range(n)]
+
+
+def seed_minmax(w, S):
+    w = np.ascontiguousarray(np.asarray(w, dtype=np.int64))
+    cuts = (C.c_int * max(1, S))()
+    val = lib().orc_seed_minmax(len(w), _i64p(w), S, cuts)
+    return val, [cuts[i] for i in range(S - 1)]
+
+
+def device_of_stage(placement, p, v, s):
+    return lib().orc_device_of_stage(placement, p, v, s)
+
+
+def combo(v, k):
+    a, b = C.c_int(), C.c_int()
+    ok = lib().orc_combo(v, k, C.byref(a), C.byref(b))
+    return (a.value, b.value) if ok else None
+
+
+def space_size(pr, sp):
+    ctx = _Ctx(pr, sp)
+    of = C.c_int()
+    n = lib().orc_space_size(C.byref(ctx.pr), C.byref(ctx.sp), C.byref(of))
+    if of.value:
+        raise OverflowError("space size does not fit in 63 bits")
+    return int(n)
+
+
+def enumerate_space(pr, sp, limit=10_000_000):
+    """Every candidate in canonical order (small spaces only)."""
+    ctx = _Ctx(pr, sp)
+    out = []
+
+    def cb(idx, plp, _):
+        if len(out) < limit:
+            out.append((int(idx), plan_dict(plp.contents)))
+    f = CB(cb)
+    lib().orc_enumerate(C.byref(ctx.pr), C.byref(ctx.sp), f, None)
+    return out
+
+
+def decode(pr, sp, index):
+    ctx = _Ctx(pr, sp)
+    pl = _Plan()
+    if lib().orc_decode(C.byref(ctx.pr), C.byref(ctx.sp), index, C.byref(pl)) != 0:
+        raise IndexError(index)
+    return plan_dict(pl)
+
+
+def eval_indices(pr, sp, indices, nthreads=None):
+    ctx = _Ctx(pr, sp)
+    idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
+    n = idx.shape[0]
+    ms = np.zeros(n, np.int64); pk = np.zeros(n, np.int64)
+    bub = np.zeros(n, np.float64); st = np.zeros(n, np.uint8)
+    nth = nthreads or os.cpu_count() or 1
+    rc = lib().orc_eval_indices(C.byref(ctx.pr), C.byref(ctx.sp),
+                                idx.ctypes.data_as(C.POINTER(C.c_uint64)), n, nth, _i64p(ms),
+                                _i64p(pk), bub.ctypes.data_as(C.POINTER(C.c_double)),
+                                st.ctypes.data_as(C.POINTER(C.c_uint8)))
+    if rc != 0:
+        raise RuntimeError("oracle internal inconsistency")
+    return {"makespan": ms, "peak_mem": pk, "bubble": bub, "status": st}
+
+
+def search(pr, sp, prune=True, nthreads=None):
+    ctx = _Ctx(pr, sp)
+    b = _Best()
+    nth = nthreads or os.cpu_count() or 1
+    rc = lib().orc_search(C.byref(ctx.pr), C.byref(ctx.sp), int(prune), nth, C.byref(b))
+    if rc != 0:
+        raise RuntimeError("oracle internal inconsistency")
+    return {"index": int(b.index), "makespan": int(b.makespan), "plan": plan_dict(b.plan),
+            "n_total": int(b.n_total), "n_invalid": int(b.n_invalid),
+            "n_simulated": int(b.n_simulated), "n_feasible": int(b.n_feasible)}

@@ -1,0 +1,342 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix
+(closed forms, SPEC/paper worked examples, brute force on tiny inputs).
+
+None of these re-types the oracle's formulas: each expected value comes from a
+closed form, a cited worked example (tests/golden/), or an exhaustive
+brute force written here in plain Python.
+"""
+import itertools
+import json
+import math
+import os
+from fractions import Fraction
+
+import pytest
+
+from oracle import oracle as O
+from paper_2509_23722_b200 import workloads as W
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SPEC = json.load(open(os.path.join(GOLD, "spec_examples.json")))
+CFG1 = json.load(open(os.path.join(GOLD, "cfg1_unit.json")))
+
+
+def homo(L, p, m, tf, tb, tw, comm=0, act=0, stash=0, weight=0, cap=W.INT64_MAX):
+    return W.Problem(t_f=[tf] * L, t_b=[tb] * L, t_w=[tw] * L, act=[act] * L, stash=[stash] * L,
+                     weight=[weight] * L, grad=[0] * L, comm=[comm] * L, p=p, m=m, cap=cap)
+
+
+def seq_cuts(S):
+    return list(range(1, S))
+
+
+# ---------------------------------------------------------------- Alg. 1 Step 1
+def test_stage_sums_whole_model_equals_column_sums():
+    """with S = 1 the stage cost is the column sum; busy = m * sum (Alg.1 Step 1-2)."""
+    pr = W.random_problem(W.SplitMix64(7), 9, 1, 3)
+    for pol in range(4):
+        r = O.simulate(pr, 1, W.SEQ, pol, [])
+        total = sum(int(pr.t_f[i] + pr.t_b[i] + pr.t_w[i]) for i in range(9))
+        assert r["busy_d"] == [3 * total]
+        assert r["makespan"] == 3 * total  # serial device: no bubbles
+        assert r["static_d"] == [int(pr.weight.sum() + pr.grad.sum())]
+
+
+def test_stage_sum_pair_spec_example():
+    ex = SPEC["stage_sum_pair"]
+    pr = W.Problem(t_f=ex["t_f"] + [1], t_b=[1] * 3, t_w=[1] * 3, act=[0] * 3, stash=[0] * 3,
+                   weight=[0] * 3, grad=[0] * 3, comm=[0] * 3, p=2, m=1)
+    # stage 0 = rows {0,1}: with m=1 GPIPE on 2 devices the F of stage 1 starts at c_F(0)
+    r = O.simulate(pr, 1, W.SEQ, W.GPIPE, [2], trace=True)
+    f1 = [t for t in r["trace"][1] if t[0] == 0][0]
+    assert f1[3] == ex["c_F"]
+
+
+def test_serial_example():
+    ex = SPEC["serial"]
+    tf, tb, tw = ex["t"]
+    pr = homo(1, 1, ex["m"], tf, tb, tw)
+    for pol in range(4):
+        r = O.simulate(pr, 1, W.SEQ, pol, [])
+        assert r["makespan"] == ex["makespan"]
+        assert r["bubble"] == 0.0
+
+
+# ---------------------------------------------------------------- placements (R12)
+@pytest.mark.parametrize("key,placement", [("interleaved_4_2", W.INTERLEAVED),
+                                           ("wave_4_2", W.WAVE), ("wave_8_4", W.WAVE)])
+def test_placement_examples(key, placement):
+    ex = SPEC[key]
+    v = ex["S"] // ex["p"]
+    assert [O.device_of_stage(placement, ex["p"], v, s) for s in range(ex["S"])] == ex["dev"]
+
+
+def test_combo_table():
+    assert [O.combo(1, k) for k in range(5)] == [(0, 0), (0, 1), (0, 2), (0, 3), None]
+    assert [O.combo(2, k) for k in range(7)] == [(1, 0), (1, 1), (1, 2), (1, 3), (2, 0), (2, 3), None]
+
+
+# ---------------------------------------------------------------- orders (R9-R11)
+def _fmt(lst):
+    return [("F" if k == 0 else "B") + str(j + 1) for (k, s, j) in lst]
+
+
+def test_s1f1b_lists_spec_example():
+    ex = SPEC["s1f1b_lists"]
+    pr = homo(2, 2, 3, 1, 1, 1)
+    assert _fmt(O.fixed_order(pr, 1, W.SEQ, W.ONEF1B, [1], 0)) == ex["dev0"]
+    assert _fmt(O.fixed_order(pr, 1, W.SEQ, W.ONEF1B, [1], 1)) == ex["dev1"]
+
+
+def test_interleaved_order_megatron_structure():
+    """R10: warm-up length, chunk pattern and completeness of each list."""
+    p, v, m = 4, 2, 8
+    pr = homo(p * v, p, m, 1, 1, 1)
+    for d in range(p):
+        lst = O.fixed_order(pr, v, W.INTERLEAVED, W.ONEF1B, seq_cuts(p * v), d)
+        w = min(m * v, 2 * (p - d - 1) + (v - 1) * p)
+        kinds = [k for k, _, _ in lst]
+        assert kinds[:w] == [0] * w and kinds[w] == 0 and kinds[w + 1] == 1
+        assert sorted((k, s, j) for k, s, j in lst) == sorted(
+            (k, c * p + d, j) for k in (0, 1) for c in range(v) for j in range(m))
+        fw = [(s, j) for k, s, j in lst if k == 0]
+        # the first p forwards are chunk 0, micro-batches 0..p-1; then chunk 1
+        assert fw[:p] == [(d, j) for j in range(p)]
+        assert fw[p:2 * p] == [(p + d, j) for j in range(p)]
+
+
+# ---------------------------------------------------------------- closed forms
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("mult", [0, 1, 2, 4])
+@pytest.mark.parametrize("c", [0, 1, 2, 7])
+def test_gpipe_makespan_closed_form(p, mult, c):
+    """GPipe: (m+p-1)(t_f+t_b) + 2(p-1)c with uniform comm c (north_star closed form)."""
+    m = 1 if mult == 0 else mult * p
+    tf, tb, tw = 3, 4, 2
+    pr = homo(p, p, m, tf, tb, tw, comm=c)
+    r = O.simulate(pr, 1, W.SEQ, W.GPIPE, seq_cuts(p))
+    assert r["makespan"] == (m + p - 1) * (tf + tb + tw) + 2 * (p - 1) * c
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 8, 16, 32])
+def test_s1f1b_makespan_and_bubble_closed_form(p, m):
+    """S-1F1B at zero comm: (m+p-1)(t_f+t_b) for any m; bubble = (p-1)/(m+p-1)."""
+    tf, tb, tw = 5, 7, 3
+    pr = homo(p, p, m, tf, tb, tw)
+    r = O.simulate(pr, 1, W.SEQ, W.ONEF1B, seq_cuts(p))
+    assert r["makespan"] == (m + p - 1) * (tf + tb + tw)
+    busy = sum(r["busy_d"])
+    assert Fraction(p * r["makespan"] - busy, p * r["makespan"]) == Fraction(p - 1, m + p - 1)
+    assert abs(r["bubble"] - (p - 1) / (m + p - 1)) < 1e-12
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("v", [2, 3, 4])
+@pytest.mark.parametrize("q", [1, 2, 4])
+def test_interleaved_1f1b_closed_form(p, v, q):
+    """I-1F1B: makespan (vm+p-1)(f+b) in per-chunk costs, bubble (p-1)/(vm+p-1) (1/v of S-1F1B's)."""
+    m = q * p
+    tf, tb, tw = 2, 3, 1
+    pr = homo(p * v, p, m, tf, tb, tw)
+    r = O.simulate(pr, v, W.INTERLEAVED, W.ONEF1B, seq_cuts(p * v))
+    assert r["makespan"] == (v * m + p - 1) * (tf + tb + tw)
+    assert abs(r["bubble"] - (p - 1) / (v * m + p - 1)) < 1e-12
+    r1 = O.simulate(homo(p, p, m, v * tf, v * tb, v * tw), 1, W.SEQ, W.ONEF1B, seq_cuts(p))
+    # the same model on v-times coarser stages (S-1F1B): bubble (p-1)/(m+p-1)
+    assert abs(r1["bubble"] - (p - 1) / (m + p - 1)) < 1e-12 and r["bubble"] < r1["bubble"]
+
+
+def test_s1f1b_worked_example_scaled():
+    """S:209 (t_F = t_B = 1, t_W = 0, fused) in units of 2 ticks (t_W >= 1 by R17)."""
+    ex = SPEC["s1f1b_p2_m2"]
+    pr = homo(2, 2, 2, 2, 1, 1)
+    r = O.simulate(pr, 1, W.SEQ, W.ONEF1B, [1])
+    assert r["makespan"] == ex["scale"] * ex["makespan"]
+    assert r["T_d"] == [ex["scale"] * t for t in ex["T_d"]]
+
+
+def test_zb_wfill_7_vs_immediate_w_8():
+    ex = SPEC["zb_p2_m2"]
+    pr = homo(2, 2, 2, 1, 1, 1)
+    assert O.simulate(pr, 1, W.SEQ, W.ZB, [1])["makespan"] == ex["makespan_wfill"]
+    # immediate W: the 1F1B list with each W right after its B (independent checker)
+    lists = []
+    for d in range(2):
+        lst = []
+        for (k, s, j) in O.fixed_order(pr, 1, W.SEQ, W.ONEF1B, [1], d):
+            lst.append((k, s, j))
+            if k == 1:
+                lst.append((2, s, j))
+        lists.append(lst)
+    mk, _, _ = O.longest_path(pr, 1, W.SEQ, [1], False, lists)
+    assert mk == ex["makespan_immediate_w"]
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("q", [1, 2, 4])
+def test_zb_equal_costs_closed_form(p, q):
+    """ZB W-fill with t_F = t_B = t_W = t and m >= p: (3m+p-1) t (R13)."""
+    m, t = q * p, 3
+    pr = homo(p, p, m, t, t, t)
+    assert O.simulate(pr, 1, W.SEQ, W.ZB, seq_cuts(p))["makespan"] == (3 * m + p - 1) * t
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("m", [1, 2, 4, 8, 16])
+def test_greedy_closed_form(p, m):
+    """GREEDY, cap = inf, zero comm, homogeneous: (m+p-1)(t_f+t_b) + m t_w (R14)."""
+    tf, tb, tw = 4, 6, 3
+    pr = homo(p, p, m, tf, tb, tw)
+    assert O.simulate(pr, 1, W.SEQ, W.GREEDY, seq_cuts(p))["makespan"] == \
+        (m + p - 1) * (tf + tb) + m * tw
+
+
+# ---------------------------------------------------------------- memory (R16, Eq. 2)
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("m", [2, 4, 8])
+def test_peak_memory_closed_forms_v1(p, m):
+    pr = homo(p, p, m, 1, 1, 1, act=3, stash=2)  # one unit = 5 bytes per stage per mb
+    g = O.simulate(pr, 1, W.SEQ, W.GPIPE, seq_cuts(p))
+    assert g["M_d"] == [5 * m] * p
+    o = O.simulate(pr, 1, W.SEQ, W.ONEF1B, seq_cuts(p))
+    assert o["M_d"] == [5 * min(p - d, m) for d in range(p)]
+
+
+@pytest.mark.parametrize("p,v", [(2, 2), (4, 2), (4, 3), (2, 4)])
+def test_peak_memory_closed_forms_interleaved(p, v):
+    m = 2 * p
+    pr = homo(p * v, p, m, 1, 1, 1, act=1)
+    o = O.simulate(pr, v, W.INTERLEAVED, W.ONEF1B, seq_cuts(p * v))
+    assert o["M_d"] == [min(m * v, 2 * (p - d - 1) + (v - 1) * p + 1) for d in range(p)]
+    g = O.simulate(pr, v, W.INTERLEAVED, W.GPIPE, seq_cuts(p * v))
+    assert g["M_d"] == [m * v] * p
+
+
+def test_gpipe_memory_cap_example():
+    """GPipe with nmb=4 holds 4 units; capacity 3 units is violated, 4 is not."""
+    ex = SPEC["gpipe_mem"]
+    u = 7
+    pr = homo(2, 2, ex["m"], 1, 1, 1, act=u, weight=100, cap=100 + ex["cap_units"] * u)
+    r = O.simulate(pr, 1, W.SEQ, W.GPIPE, [1])
+    assert r["status"] == 2 and r["makespan"] == O.INT64_MAX
+    assert r["peak_mem"] == 100 + 4 * u  # static (weight of one row) + 4 units
+    pr.cap = 100 + 4 * u
+    assert O.simulate(pr, 1, W.SEQ, W.GPIPE, [1])["status"] == 0
+
+
+def test_greedy_and_zb_respect_or_report_cap():
+    rng = W.SplitMix64(99)
+    for _ in range(60):
+        p = 2 + rng.next() % 3
+        m = p * (1 + rng.next() % 2)
+        pr = W.random_problem(rng, 2 * p + 1, p, m, bytes_max=9, cap=60 + rng.next() % 80)
+        cuts = sorted(set(range(1, 2 * p + 1)) - {int(1 + rng.next() % (2 * p))})
+        cuts = cuts[:2 * p - 1]
+        for pol in (W.ZB, W.GREEDY):
+            r = O.simulate(pr, 2, W.INTERLEAVED, pol, cuts)
+            if r["status"] == 0:
+                assert max(r["M_d"]) <= pr.cap
+            if pol == W.GREEDY and r["status"] != 3:
+                assert max(r["M_d"]) <= pr.cap
+
+
+# ---------------------------------------------------------------- seed (R20)
+@pytest.mark.parametrize("key", ["balanced_1", "balanced_2"])
+def test_seed_spec_examples(key):
+    ex = SPEC[key]
+    val, cuts = O.seed_minmax(ex["w"], ex["S"])
+    assert (val, cuts) == (ex["max"], ex["cuts"])
+
+
+def test_seed_brute_force():
+    rng = W.SplitMix64(3)
+    for _ in range(150):
+        L = 2 + rng.next() % 11
+        S = 1 + rng.next() % min(4, L)
+        w = [1 + rng.next() % 9 for _ in range(L)]
+        best = None
+        for cuts in itertools.combinations(range(1, L), S - 1):
+            b = [0, *cuts, L]
+            val = max(sum(w[b[i]:b[i + 1]]) for i in range(S))
+            if best is None or (val, cuts) < best:
+                best = (val, cuts)
+        assert O.seed_minmax(w, S) == (best[0], list(best[1]))
+
+
+# ---------------------------------------------------------------- space (R19)
+def test_full_count_and_colex_order():
+    pr = homo(9, 2, 2, 1, 1, 1)
+    sp = W.Space([W.Group(2, W.FULL, combo_mask=0x1)])  # S = 4 -> C(8, 3)
+    out = O.enumerate_space(pr, sp)
+    assert len(out) == math.comb(8, 3) == O.space_size(pr, sp)
+    inner = [tuple(pl["cuts"][1:-1]) for _, pl in out]
+    assert inner == sorted(itertools.combinations(range(1, 9), 3), key=lambda t: t[::-1])
+    assert [i for i, _ in out] == list(range(len(out)))
+
+
+def _ball_key(delta):
+    return tuple(2 * abs(x) - (1 if x < 0 else 0) for x in delta)  # 0,-1,+1,-2,+2 -> 0,1,2,3,4
+
+
+@pytest.mark.parametrize("n,R", [(1, 3), (3, 2), (4, 3), (2, 5)])
+def test_ball_count_bijection_and_order(n, R):
+    L = 40
+    seed = [5 * (i + 1) for i in range(n)]
+    p = n + 1
+    pr = homo(L, p, 2, 1, 1, 1)
+    sp = W.Space([W.Group(1, W.BALL, R, seed_cuts=seed, combo_mask=0x1)])
+    out = O.enumerate_space(pr, sp)
+    closed = sum(2 ** k * math.comb(n, k) * math.comb(R, k) for k in range(0, min(n, R) + 1))
+    assert len(out) == closed == O.space_size(pr, sp)
+    deltas = [tuple(c - s for c, s in zip(pl["cuts"][1:-1], seed)) for _, pl in out]
+    brute = [d for d in itertools.product(range(-R, R + 1), repeat=n) if sum(map(abs, d)) <= R]
+    assert sorted(deltas) == sorted(brute)
+    assert deltas == sorted(deltas, key=_ball_key)
+
+
+def test_decode_matches_enumeration():
+    pr = W.random_problem(W.SplitMix64(5), 10, 2, 4)
+    sp = W.Space([W.Group(1, W.FULL, combo_mask=0xF), W.Group(2, W.BALL, 3, combo_mask=0x35),
+                  W.Group(4, W.FULL, combo_mask=0x3F)])
+    out = O.enumerate_space(pr, sp)
+    assert len(out) == O.space_size(pr, sp)
+    for idx, pl in out:
+        assert O.decode(pr, sp, idx) == pl
+
+
+def test_config_space_sizes():
+    """|space| of the five configs; closed forms computed here."""
+    def ball(n, R):
+        return sum(2 ** k * math.comb(n, k) * math.comb(R, k) for k in range(min(n, R) + 1))
+    exp = {1: 7 * 4 + 35 * 6 + 1 * 6, 2: math.comb(33, 7),
+           3: 4 * ball(7, 16) + 6 * ball(15, 8), 4: 6 * ball(15, 8),
+           5: 4 * ball(15, 9) + 6 * ball(31, 6) + 6 * ball(63, 4)}
+    for cid in range(1, 6):
+        pr, sp = W.config(cid)
+        assert O.space_size(pr, sp) == exp[cid]
+    assert exp[2] == 4_272_048 and 9.4e8 < exp[5] < 9.6e8
+
+
+# ---------------------------------------------------------------- cfg1 anchors
+def test_cfg1_unit_advisory_golden():
+    g = CFG1
+    pr = W.cfg1_unit()
+    sp = W.Space([W.Group(1, W.FULL, combo_mask=0xF), W.Group(2, W.FULL), W.Group(4, W.FULL)])
+    assert O.space_size(pr, sp) == g["full"]["N"]
+    b = O.search(pr, sp, prune=False)
+    assert (b["index"], b["makespan"]) == (g["full"]["argmin_index"], g["full"]["makespan"])
+    assert b["plan"]["cuts"] == g["full"]["plan"]["cuts"]
+    ev = O.eval_indices(pr, sp, range(g["full"]["N"]))
+    assert int(ev["makespan"].max()) == g["full"]["worst_makespan"] == int(ev["makespan"][0])
+    for name, pol in (("GPIPE", 0), ("ONEF1B", 1), ("ZB", 2), ("GREEDY", 3)):
+        assert O.simulate(pr, 1, W.SEQ, pol, [4])["makespan"] == g["uniform_v1_cut4"][name]
+    lit = W.Space([W.Group(1, W.FULL, combo_mask=0x7), W.Group(2, W.FULL, combo_mask=0x17),
+                   W.Group(4, W.FULL, combo_mask=0x17)])
+    assert O.space_size(pr, lit) == g["literal_three_policy"]["N"]
+    bl = O.search(pr, lit, prune=False)
+    assert (bl["index"], bl["makespan"]) == (g["literal_three_policy"]["argmin_index"],
+                                             g["literal_three_policy"]["makespan"])
+    evl = O.eval_indices(pr, lit, range(165))
+    ties = [i for i in range(165) if evl["makespan"][i] == 218]
+    assert ties == g["literal_three_policy"]["tied_indices"]
