@@ -33,6 +33,12 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#define ADAPTIS_API __attribute__((visibility("default")))
+#else
+#define ADAPTIS_API
+#endif
+
 #define ADAPTIS_MAX_P 32      /* pipeline devices per candidate (lanes of one warp)   */
 #define ADAPTIS_MAX_V 4       /* virtual stages per device                            */
 #define ADAPTIS_MAX_S 64      /* stages S = p*v                                       */
@@ -146,6 +152,7 @@ typedef struct {             /* output of adaptis_search                        
   uint64_t n_candidates;     /* |space| (all ranks)                                          */
   uint64_t n_evaluated;      /* candidates this rank evaluated                               */
   uint64_t n_invalid;        /* of those, invalid decodes (status 1)                         */
+  uint64_t n_tasks;          /* F/B/W tasks this rank simulated (work counter for the roofline) */
   float    kernel_ms;        /* device time of this rank's evaluation kernels                */
 } adaptis_best;
 
@@ -163,38 +170,38 @@ typedef int (*adaptis_allreduce_min_fn)(int64_t* dev_key, void* cuda_stream, voi
  * sharding (block-cyclic chunks of 65536 indices, chunk k -> rank k mod world).
  * EINVAL if world < 1 or rank not in [0, world); ECUDA if the device is
  * unusable. */
-adaptis_status adaptis_ctx_create(int cuda_device, int rank, int world, adaptis_ctx** out);
-void           adaptis_ctx_destroy(adaptis_ctx* ctx);
-adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_allreduce_min_fn fn, void* user);
+ADAPTIS_API adaptis_status adaptis_ctx_create(int cuda_device, int rank, int world, adaptis_ctx** out);
+ADAPTIS_API void           adaptis_ctx_destroy(adaptis_ctx* ctx);
+ADAPTIS_API adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_allreduce_min_fn fn, void* user);
 /* The CUDA stream (cudaStream_t) every kernel of this context is queued on. */
-void*          adaptis_ctx_stream(adaptis_ctx* ctx);
+ADAPTIS_API void*          adaptis_ctx_stream(adaptis_ctx* ctx);
 /* Number of kernel launches this context has issued since creation. */
-uint64_t       adaptis_ctx_launch_count(const adaptis_ctx* ctx);
+ADAPTIS_API uint64_t       adaptis_ctx_launch_count(const adaptis_ctx* ctx);
 
 /* |space| for this problem (the candidate space). EINVAL on an
  * invalid problem/space; EOVERFLOW if the count does not fit in 63 bits. */
-adaptis_status adaptis_space_size(const adaptis_problem* problem, const adaptis_space* space,
+ADAPTIS_API adaptis_status adaptis_space_size(const adaptis_problem* problem, const adaptis_space* space,
                                   uint64_t* n_out);
 
 /* Decode a global index into its (v, placement, policy, cuts) candidate, in the
  * canonical order of R19. EINVAL if index >= |space|. An invalid BALL decode
  * is still returned (its cuts are not strictly increasing). */
-adaptis_status adaptis_decode(const adaptis_problem* problem, const adaptis_space* space,
+ADAPTIS_API adaptis_status adaptis_decode(const adaptis_problem* problem, const adaptis_space* space,
                               uint64_t index, adaptis_plan* out);
 
 /* Validate, derive host tables (prefix sums, seeds, counts) and upload them to
  * the device once, so repeated evaluations start with inputs resident in HBM. */
-adaptis_status adaptis_prepare(adaptis_ctx* ctx, const adaptis_problem* problem,
+ADAPTIS_API adaptis_status adaptis_prepare(adaptis_ctx* ctx, const adaptis_problem* problem,
                                const adaptis_space* space, adaptis_prepared** out);
-void           adaptis_prepared_free(adaptis_prepared* prep);
+ADAPTIS_API void           adaptis_prepared_free(adaptis_prepared* prep);
 
 /* Evaluate candidates [first, first+count) of the space (Alg. 1 Steps 1-3 per
  * candidate) and write per-candidate results. Unlike search this is not
  * sharded: the context's GPU evaluates the whole range. */
-adaptis_status adaptis_eval_batch(adaptis_ctx* ctx, const adaptis_problem* problem,
+ADAPTIS_API adaptis_status adaptis_eval_batch(adaptis_ctx* ctx, const adaptis_problem* problem,
                                   const adaptis_space* space, uint64_t first, uint64_t count,
                                   const adaptis_results_soa* out, int out_on_device);
-adaptis_status adaptis_eval_prepared(adaptis_ctx* ctx, adaptis_prepared* prep,
+ADAPTIS_API adaptis_status adaptis_eval_prepared(adaptis_ctx* ctx, adaptis_prepared* prep,
                                      uint64_t first, uint64_t count,
                                      const adaptis_results_soa* out, int out_on_device);
 
@@ -203,14 +210,14 @@ adaptis_status adaptis_eval_prepared(adaptis_ctx* ctx, adaptis_prepared* prep,
  * rank evaluates its shard and the allreduce hook combines the packed keys;
  * every rank returns the same `out`. EINFEASIBLE if no candidate is feasible
  * (out->index = UINT64_MAX). */
-adaptis_status adaptis_search(adaptis_ctx* ctx, const adaptis_problem* problem,
+ADAPTIS_API adaptis_status adaptis_search(adaptis_ctx* ctx, const adaptis_problem* problem,
                               const adaptis_space* space, adaptis_best* out);
-adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* prep,
+ADAPTIS_API adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* prep,
                                        adaptis_best* out);
 
 /* Message of the last failure on `ctx` (or of the calling thread when ctx is NULL). */
-const char*    adaptis_last_error(const adaptis_ctx* ctx);
-const char*    adaptis_status_str(adaptis_status s);
+ADAPTIS_API const char*    adaptis_last_error(const adaptis_ctx* ctx);
+ADAPTIS_API const char*    adaptis_status_str(adaptis_status s);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,356 @@
+"""Thin ctypes binding of libadaptis.so (include/adaptis.h).
+
+Argument marshalling only: every step of the hot path (decode, stage sums,
+simulation, argmin) runs in the library's CUDA kernels. PyTorch is used for
+device memory, streams and torch.distributed (the allreduce hook), nothing
+else. There is no CPU fallback: if libadaptis.so is missing or has no GPU to
+run on, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+import threading
+from typing import Optional
+
+import numpy as np
+
+from . import workloads as W
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libadaptis.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "adaptis.h")
+MAX_P, MAX_V, MAX_S, MAX_GROUPS = 32, 4, 64, 4
+INT64_MAX = (1 << 63) - 1
+UINT64_MAX = (1 << 64) - 1
+
+OK, EINVAL, EINFEASIBLE, EOVERFLOW, ECUDA, ECOLL = range(6)
+
+
+class AdaptisError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("%s (status %d)" % (msg, status))
+        self.status = status
+
+
+class _Layers(C.Structure):
+    _fields_ = [("L", C.c_int32)] + [(n, C.POINTER(C.c_int64)) for n in (
+        "t_f", "t_b", "t_w", "act_bytes", "stash_bytes", "weight_bytes", "grad_bytes", "comm_ticks")]
+
+
+class _Problem(C.Structure):
+    _fields_ = [("layers", _Layers), ("p", C.c_int32), ("m", C.c_int32),
+                ("mem_cap_bytes", C.c_int64), ("tick_seconds", C.c_double),
+                ("tokens_per_microbatch", C.c_int64)]
+
+
+class _Group(C.Structure):
+    _fields_ = [("v", C.c_int32), ("part_mode", C.c_int32), ("radius", C.c_int32),
+                ("seed_cuts", C.POINTER(C.c_int16)), ("combo_mask", C.c_uint32)]
+
+
+class _Space(C.Structure):
+    _fields_ = [("n_groups", C.c_int32), ("group", _Group * MAX_GROUPS)]
+
+
+class _Plan(C.Structure):
+    _fields_ = [("v", C.c_int32), ("placement", C.c_int32), ("policy", C.c_int32),
+                ("S", C.c_int32), ("cuts", C.c_int16 * (MAX_S + 1))]
+
+
+class _ResultsSoa(C.Structure):
+    _fields_ = [("makespan", C.c_void_p), ("peak_mem_bytes", C.c_void_p),
+                ("bubble_ratio", C.c_void_p), ("status", C.c_void_p)]
+
+
+class _Result(C.Structure):
+    _fields_ = [("makespan", C.c_int64), ("peak_mem_bytes", C.c_int64),
+                ("bubble_ratio", C.c_float), ("throughput", C.c_double), ("status", C.c_uint8)]
+
+
+class _Best(C.Structure):
+    _fields_ = [("index", C.c_uint64), ("plan", _Plan), ("result", _Result), ("p", C.c_int32),
+                ("T_d", C.c_int64 * MAX_P), ("busy_d", C.c_int64 * MAX_P),
+                ("M_d", C.c_int64 * MAX_P), ("n_candidates", C.c_uint64),
+                ("n_evaluated", C.c_uint64), ("n_invalid", C.c_uint64), ("n_tasks", C.c_uint64),
+                ("kernel_ms", C.c_float)]
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+
+_lock = threading.Lock()
+_lib = None
+
+
+def exported_symbols():
+    """Entry points declared in include/adaptis.h."""
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(adaptis_[a-z_]+)\s*\(", src)) - {"adaptis_allreduce_min_fn"})
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError("libadaptis.so not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+            L = C.CDLL(LIB_PATH)
+            st = C.c_int
+            L.adaptis_status_str.restype = C.c_char_p
+            L.adaptis_last_error.restype = C.c_char_p
+            L.adaptis_last_error.argtypes = [C.c_void_p]
+            L.adaptis_ctx_create.restype = st
+            L.adaptis_ctx_create.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+            L.adaptis_ctx_destroy.argtypes = [C.c_void_p]
+            L.adaptis_ctx_set_allreduce.restype = st
+            L.adaptis_ctx_set_allreduce.argtypes = [C.c_void_p, ALLREDUCE_FN, C.c_void_p]
+            L.adaptis_ctx_stream.restype = C.c_void_p
+            L.adaptis_ctx_stream.argtypes = [C.c_void_p]
+            L.adaptis_ctx_launch_count.restype = C.c_uint64
+            L.adaptis_ctx_launch_count.argtypes = [C.c_void_p]
+            L.adaptis_space_size.restype = st
+            L.adaptis_space_size.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.POINTER(C.c_uint64)]
+            L.adaptis_decode.restype = st
+            L.adaptis_decode.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.c_uint64, C.POINTER(_Plan)]
+            L.adaptis_prepare.restype = st
+            L.adaptis_prepare.argtypes = [C.c_void_p, C.POINTER(_Problem), C.POINTER(_Space),
+                                          C.POINTER(C.c_void_p)]
+            L.adaptis_prepared_free.argtypes = [C.c_void_p]
+            L.adaptis_eval_batch.restype = st
+            L.adaptis_eval_batch.argtypes = [C.c_void_p, C.POINTER(_Problem), C.POINTER(_Space),
+                                             C.c_uint64, C.c_uint64, C.POINTER(_ResultsSoa), C.c_int]
+            L.adaptis_eval_prepared.restype = st
+            L.adaptis_eval_prepared.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                                C.POINTER(_ResultsSoa), C.c_int]
+            L.adaptis_search.restype = st
+            L.adaptis_search.argtypes = [C.c_void_p, C.POINTER(_Problem), C.POINTER(_Space), C.POINTER(_Best)]
+            L.adaptis_search_prepared.restype = st
+            L.adaptis_search_prepared.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Best)]
+            _lib = L
+    return _lib
+
+
+def _err(ctx_ptr=None) -> str:
+    return (lib().adaptis_last_error(ctx_ptr) or b"").decode()
+
+
+class _Marshal:
+    """C views of a workloads.Problem / Space; keeps the numpy buffers alive."""
+
+    def __init__(self, pr: W.Problem, sp: Optional[W.Space] = None):
+        self.keep = []
+        ptrs = {}
+        for src, dst in (("t_f", "t_f"), ("t_b", "t_b"), ("t_w", "t_w"), ("act", "act_bytes"),
+                         ("stash", "stash_bytes"), ("weight", "weight_bytes"),
+                         ("grad", "grad_bytes"), ("comm", "comm_ticks")):
+            a = np.ascontiguousarray(np.asarray(getattr(pr, src), dtype=np.int64))
+            self.keep.append(a)
+            ptrs[dst] = a.ctypes.data_as(C.POINTER(C.c_int64))
+        self.problem = _Problem(layers=_Layers(L=len(pr.t_f), **ptrs), p=pr.p, m=pr.m,
+                                mem_cap_bytes=int(pr.cap), tick_seconds=float(pr.tick_seconds),
+                                tokens_per_microbatch=int(pr.tokens_per_microbatch))
+        self.space = None
+        if sp is not None:
+            s = _Space(n_groups=len(sp.groups))
+            for i, g in enumerate(sp.groups):
+                seed = None
+                if g.seed_cuts is not None:
+                    arr = (C.c_int16 * len(g.seed_cuts))(*g.seed_cuts)
+                    self.keep.append(arr)
+                    seed = C.cast(arr, C.POINTER(C.c_int16))
+                s.group[i] = _Group(v=g.v, part_mode=g.part_mode, radius=g.radius,
+                                    seed_cuts=seed, combo_mask=g.combo_mask)
+            self.space = s
+
+
+def _check(status, ctx_ptr=None):
+    if status != OK:
+        raise AdaptisError(status, _err(ctx_ptr))
+
+
+def plan_dict(pl: _Plan) -> dict:
+    return {"v": pl.v, "placement": pl.placement, "policy": pl.policy, "S": pl.S,
+            "cuts": [int(pl.cuts[i]) for i in range(pl.S + 1)]}
+
+
+def space_size(pr: W.Problem, sp: W.Space) -> int:
+    """|space| (host-only entry point; no GPU needed)."""
+    m = _Marshal(pr, sp)
+    n = C.c_uint64()
+    _check(lib().adaptis_space_size(C.byref(m.problem), C.byref(m.space), C.byref(n)))
+    return int(n.value)
+
+
+def decode(pr: W.Problem, sp: W.Space, index: int) -> dict:
+    """Candidate index -> plan, canonical order R19 (host-only entry point)."""
+    m = _Marshal(pr, sp)
+    pl = _Plan()
+    _check(lib().adaptis_decode(C.byref(m.problem), C.byref(m.space), index, C.byref(pl)))
+    return plan_dict(pl)
+
+
+class Context:
+    """One adaptis_ctx bound to a CUDA device (and a rank of a sharded search)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, group=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("adaptis needs a CUDA device (no CPU fallback)")
+        torch.cuda.init()
+        self.device = device
+        self.ptr = C.c_void_p()
+        _check(lib().adaptis_ctx_create(device, rank, world, C.byref(self.ptr)))
+        self._cb = None
+        self._group = group
+        if world > 1:
+            self._install_allreduce(group)
+
+    def _install_allreduce(self, group):
+        import torch
+        import torch.distributed as dist
+        dev = self.device
+
+        def _allreduce(dev_key, stream, _user):
+            try:
+                # zero-copy view of the 8-byte key in device memory
+                buf = _device_int64_view(dev_key, dev)
+                t = torch.empty(1, dtype=torch.int64, device="cuda:%d" % dev)
+                ext = torch.cuda.ExternalStream(stream, device=dev)
+                with torch.cuda.stream(ext):
+                    t.copy_(buf)
+                    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+                    buf.copy_(t)
+                ext.synchronize()
+                return 0
+            except Exception as e:  # noqa: BLE001 - reported as ADAPTIS_ECOLL
+                import sys
+                print("adaptis allreduce failed:", repr(e), file=sys.stderr)
+                return 1
+
+        self._cb = ALLREDUCE_FN(_allreduce)
+        _check(lib().adaptis_ctx_set_allreduce(self.ptr, self._cb, None), self.ptr)
+
+    @property
+    def stream(self) -> int:
+        return lib().adaptis_ctx_stream(self.ptr)
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().adaptis_ctx_launch_count(self.ptr))
+
+    def close(self):
+        if self.ptr:
+            lib().adaptis_ctx_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    # ------------------------------------------------------------------
+    def prepare(self, pr: W.Problem, sp: W.Space) -> "Prepared":
+        return Prepared(self, pr, sp)
+
+    def eval_batch(self, pr: W.Problem, sp: W.Space, first: int, count: int) -> dict:
+        """Per-candidate results for [first, first+count), host buffers (e2e path)."""
+        m = _Marshal(pr, sp)
+        out = _host_results(count)
+        soa = _soa_from_numpy(out)
+        _check(lib().adaptis_eval_batch(self.ptr, C.byref(m.problem), C.byref(m.space), first, count,
+                                        C.byref(soa), 0), self.ptr)
+        return out
+
+    def search(self, pr: W.Problem, sp: W.Space) -> dict:
+        """adaptis_search with host inputs (validate + upload + evaluate + reduce)."""
+        m = _Marshal(pr, sp)
+        b = _Best()
+        st = lib().adaptis_search(self.ptr, C.byref(m.problem), C.byref(m.space), C.byref(b))
+        return _best_dict(b, st, self.ptr)
+
+
+class Prepared:
+    """Problem tables resident in HBM (adaptis_prepare) for repeated evaluation."""
+
+    def __init__(self, ctx: Context, pr: W.Problem, sp: W.Space):
+        self.ctx = ctx
+        self.m = _Marshal(pr, sp)
+        self.ptr = C.c_void_p()
+        _check(lib().adaptis_prepare(ctx.ptr, C.byref(self.m.problem), C.byref(self.m.space),
+                                     C.byref(self.ptr)), ctx.ptr)
+        self.N = space_size(pr, sp)
+
+    def close(self):
+        if self.ptr:
+            lib().adaptis_prepared_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def search(self) -> dict:
+        b = _Best()
+        st = lib().adaptis_search_prepared(self.ctx.ptr, self.ptr, C.byref(b))
+        return _best_dict(b, st, self.ctx.ptr)
+
+    def eval(self, first: int, count: int, device_out: bool = False):
+        """Results for [first, first+count): numpy (host) or torch CUDA tensors."""
+        if device_out:
+            import torch
+            dev = "cuda:%d" % self.ctx.device
+            out = {"makespan": torch.empty(count, dtype=torch.int64, device=dev),
+                   "peak_mem": torch.empty(count, dtype=torch.int64, device=dev),
+                   "bubble": torch.empty(count, dtype=torch.float32, device=dev),
+                   "status": torch.empty(count, dtype=torch.uint8, device=dev)}
+            soa = _ResultsSoa(out["makespan"].data_ptr(), out["peak_mem"].data_ptr(),
+                              out["bubble"].data_ptr(), out["status"].data_ptr())
+            torch.cuda.current_stream(self.ctx.device).synchronize()
+            _check(lib().adaptis_eval_prepared(self.ctx.ptr, self.ptr, first, count, C.byref(soa), 1),
+                   self.ctx.ptr)
+            return out
+        out = _host_results(count)
+        soa = _soa_from_numpy(out)
+        _check(lib().adaptis_eval_prepared(self.ctx.ptr, self.ptr, first, count, C.byref(soa), 0),
+               self.ctx.ptr)
+        return out
+
+
+def _host_results(count):
+    return {"makespan": np.zeros(count, np.int64), "peak_mem": np.zeros(count, np.int64),
+            "bubble": np.zeros(count, np.float32), "status": np.zeros(count, np.uint8)}
+
+
+def _soa_from_numpy(out):
+    return _ResultsSoa(out["makespan"].ctypes.data, out["peak_mem"].ctypes.data,
+                       out["bubble"].ctypes.data, out["status"].ctypes.data)
+
+
+def _best_dict(b: _Best, st: int, ctx_ptr) -> dict:
+    if st not in (OK, EINFEASIBLE):
+        raise AdaptisError(st, _err(ctx_ptr))
+    p = b.p
+    return {"status": st, "index": int(b.index), "plan": plan_dict(b.plan),
+            "makespan": int(b.result.makespan), "peak_mem": int(b.result.peak_mem_bytes),
+            "bubble": float(b.result.bubble_ratio), "throughput": float(b.result.throughput),
+            "cand_status": int(b.result.status),
+            "T_d": list(b.T_d[:p]), "busy_d": list(b.busy_d[:p]), "M_d": list(b.M_d[:p]),
+            "n_candidates": int(b.n_candidates), "n_evaluated": int(b.n_evaluated),
+            "n_invalid": int(b.n_invalid), "n_tasks": int(b.n_tasks),
+            "kernel_ms": float(b.kernel_ms)}
+
+
+def _device_int64_view(ptr: int, device: int):
+    """A 1-element int64 torch tensor aliasing device memory at ptr."""
+    import torch
+
+    class _Holder:
+        def __init__(self, p):
+            self.__cuda_array_interface__ = {"shape": (1,), "typestr": "<i8", "data": (p, False),
+                                             "version": 3}
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Holder(ptr), device="cuda:%d" % device)

@@ -1,0 +1,697 @@
+// adaptis_host.cu — the C ABI of libadaptis.so (include/adaptis.h): validation,
+// host-derived tables (prefix columns, binomials, L1-ball counts, min-max seed),
+// device residency, segment launches, the cross-GPU argmin and the winner report.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "adaptis_decode.cuh"
+#include "adaptis_internal.h"
+
+using namespace adaptis;
+
+namespace {
+
+thread_local std::string g_tls_error;
+
+struct Seg {               // one (group, combo) segment of the canonical order (R19)
+  int group, combo, v, S, placement, policy, part_mode, radius;
+  uint64_t base, count;
+};
+
+// fixed combo table (R12)
+bool combo_of(int v, int k, int* placement, int* policy) {
+  if (v == 1) {
+    if (k < 0 || k > 3) return false;
+    *placement = ADAPTIS_SEQ; *policy = k; return true;
+  }
+  if (k >= 0 && k <= 3) { *placement = ADAPTIS_INTERLEAVED; *policy = k; return true; }
+  if (k == 4) { *placement = ADAPTIS_WAVE; *policy = ADAPTIS_GPIPE; return true; }
+  if (k == 5) { *placement = ADAPTIS_WAVE; *policy = ADAPTIS_GREEDY; return true; }
+  return false;
+}
+
+uint64_t sat_add(uint64_t a, uint64_t b) { return a > UINT64_MAX - b ? UINT64_MAX : a + b; }
+uint64_t sat_mul(uint64_t a, uint64_t b) {
+  if (a == 0 || b == 0) return 0;
+  return a > UINT64_MAX / b ? UINT64_MAX : a * b;
+}
+
+}  // namespace
+
+struct adaptis_prepared {
+  // host copies
+  int L = 0, p = 0, m = 0, n_groups = 0;
+  int64_t cap = 0;
+  double tick_seconds = 0;
+  int64_t tokens_per_mb = 0;
+  std::vector<Seg> segs;
+  uint64_t N = 0;
+  int key_bits = 1;
+  bool use_int64 = false;
+  std::vector<uint64_t> h_binom, h_ball;
+  std::vector<int16_t> h_seeds;
+  int group_v[ADAPTIS_MAX_GROUPS] = {0};
+  // device
+  int64_t* d_cols = nullptr;
+  int64_t* d_comm = nullptr;
+  uint64_t* d_binom = nullptr;
+  uint64_t* d_ball = nullptr;
+  int16_t* d_seeds = nullptr;
+  DevTables tabs{};
+  adaptis_ctx* owner = nullptr;
+};
+
+struct adaptis_ctx {
+  int device = 0, rank = 0, world = 1, num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  adaptis_allreduce_min_fn allreduce = nullptr;
+  void* allreduce_user = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+  // scratch
+  unsigned long long* d_scratch = nullptr;  // [0] key, [1] n_invalid, [2..] cursors/overflow counts
+  size_t scratch_words = 0;
+  uint64_t* d_overflow = nullptr;
+  size_t overflow_cap = 0;
+  int64_t* d_gring = nullptr;
+  size_t gring_bytes = 0;
+  int64_t* d_report = nullptr;
+};
+
+namespace {
+
+adaptis_status fail(adaptis_ctx* ctx, adaptis_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf; else g_tls_error = buf;
+  return s;
+}
+
+#define CU(ctx, call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(ctx, ADAPTIS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));         \
+  } while (0)
+
+// -- validation (S:62-66 style: the message names the field) -------------------
+adaptis_status validate(adaptis_ctx* ctx, const adaptis_problem* pr, const adaptis_space* sp) {
+  if (!pr) return fail(ctx, ADAPTIS_EINVAL, "problem is NULL");
+  if (!sp) return fail(ctx, ADAPTIS_EINVAL, "space is NULL");
+  const adaptis_layers& Ly = pr->layers;
+  if (Ly.L < 2 || Ly.L > 32767) return fail(ctx, ADAPTIS_EINVAL, "layers.L = %d not in [2, 32767]", Ly.L);
+  const int64_t* cols[8] = {Ly.t_f, Ly.t_b, Ly.t_w, Ly.act_bytes, Ly.stash_bytes, Ly.weight_bytes,
+                            Ly.grad_bytes, Ly.comm_ticks};
+  const char* names[8] = {"t_f", "t_b", "t_w", "act_bytes", "stash_bytes", "weight_bytes",
+                          "grad_bytes", "comm_ticks"};
+  for (int c = 0; c < 8; ++c) {
+    if (!cols[c]) return fail(ctx, ADAPTIS_EINVAL, "layers.%s is NULL", names[c]);
+    const int n = (c == 7) ? Ly.L - 1 : Ly.L;
+    for (int l = 0; l < n; ++l) {
+      if (c < 3 && cols[c][l] < 1)  // R17: strictly positive durations
+        return fail(ctx, ADAPTIS_EINVAL, "layers.%s[%d] < 1", names[c], l);
+      if (cols[c][l] < 0) return fail(ctx, ADAPTIS_EINVAL, "layers.%s[%d] < 0", names[c], l);
+      if (cols[c][l] > (int64_t)1 << 52)
+        return fail(ctx, ADAPTIS_EINVAL, "layers.%s[%d] > 2^52", names[c], l);
+    }
+  }
+  if (pr->p < 1 || pr->p > ADAPTIS_MAX_P) return fail(ctx, ADAPTIS_EINVAL, "p = %d not in [1, 32]", pr->p);
+  if (pr->m < 1 || pr->m > 65535) return fail(ctx, ADAPTIS_EINVAL, "m = %d not in [1, 65535]", pr->m);
+  if (pr->mem_cap_bytes < 0) return fail(ctx, ADAPTIS_EINVAL, "mem_cap_bytes < 0");
+  if (sp->n_groups < 1 || sp->n_groups > ADAPTIS_MAX_GROUPS)
+    return fail(ctx, ADAPTIS_EINVAL, "space.n_groups = %d not in [1, 4]", sp->n_groups);
+  for (int g = 0; g < sp->n_groups; ++g) {
+    const adaptis_group& G = sp->group[g];
+    if (G.v < 1 || G.v > ADAPTIS_MAX_V)
+      return fail(ctx, ADAPTIS_EINVAL, "space.group[%d].v = %d not in [1, 4]", g, G.v);
+    const int S = pr->p * G.v;
+    if (S > ADAPTIS_MAX_S) return fail(ctx, ADAPTIS_EINVAL, "space.group[%d]: S = p*v = %d > 64", g, S);
+    if (S > Ly.L) return fail(ctx, ADAPTIS_EINVAL, "space.group[%d]: S = %d > layers.L = %d", g, S, Ly.L);
+    if (G.v > 1 && pr->m % pr->p != 0)
+      return fail(ctx, ADAPTIS_EINVAL, "space.group[%d]: v > 1 requires m %% p == 0 (R10)", g);
+    if (G.part_mode != ADAPTIS_PART_FULL && G.part_mode != ADAPTIS_PART_BALL)
+      return fail(ctx, ADAPTIS_EINVAL, "space.group[%d].part_mode = %d", g, G.part_mode);
+    if (G.part_mode == ADAPTIS_PART_BALL && (G.radius < 0 || G.radius > kMaxRadius))
+      return fail(ctx, ADAPTIS_EINVAL, "space.group[%d].radius = %d not in [0, %d]", g, G.radius, kMaxRadius);
+    if (G.part_mode == ADAPTIS_PART_FULL && Ly.L > kMaxBinomN)
+      return fail(ctx, ADAPTIS_EINVAL, "space.group[%d]: FULL partitions need L <= %d", g, kMaxBinomN);
+    int nc = 0, a, b;
+    for (int k = 0; k < 32; ++k)
+      if ((G.combo_mask >> k) & 1u) {
+        if (!combo_of(G.v, k, &a, &b))
+          return fail(ctx, ADAPTIS_EINVAL, "space.group[%d].combo_mask bit %d is not a combo for v = %d", g, k, G.v);
+        ++nc;
+      }
+    if (nc == 0) return fail(ctx, ADAPTIS_EINVAL, "space.group[%d].combo_mask is empty", g);
+    if (G.part_mode == ADAPTIS_PART_BALL && G.seed_cuts) {
+      int prev = 0;
+      for (int i = 0; i < S - 1; ++i) {
+        if (G.seed_cuts[i] <= prev || G.seed_cuts[i] >= Ly.L)
+          return fail(ctx, ADAPTIS_EINVAL, "space.group[%d].seed_cuts[%d] = %d not increasing in [1, L-1]",
+                      g, i, G.seed_cuts[i]);
+        prev = G.seed_cuts[i];
+      }
+    }
+  }
+  return ADAPTIS_OK;
+}
+
+// -- R20 seed: min-max contiguous S-way split of w, lexicographically smallest cuts.
+// Parametric search on the bound V with a greedy feasibility test (the
+// oracle's exact DP is an independent implementation).
+int min_parts(const std::vector<int64_t>& pre, int from, int L, int64_t V) {
+  // fewest contiguous parts of rows [from, L) with every part sum <= V (greedy), or INT_MAX
+  int parts = 0, i = from;
+  while (i < L) {
+    if (pre[i + 1] - pre[i] > V) return 1 << 30;
+    int j = i + 1;
+    while (j < L && pre[j + 1] - pre[i] <= V) ++j;
+    ++parts;
+    i = j;
+  }
+  return parts;
+}
+
+void seed_minmax(const adaptis_layers& Ly, int S, int16_t* cuts) {
+  const int L = Ly.L;
+  std::vector<int64_t> pre(L + 1, 0);
+  for (int l = 0; l < L; ++l) pre[l + 1] = pre[l] + Ly.t_f[l] + Ly.t_b[l] + Ly.t_w[l];
+  int64_t lo = 0, hi = pre[L];
+  for (int l = 0; l < L; ++l) lo = std::max(lo, pre[l + 1] - pre[l]);
+  while (lo < hi) {  // smallest V with a split into <= S parts (then exactly S: L >= S)
+    int64_t mid = lo + (hi - lo) / 2;
+    if (min_parts(pre, 0, L, mid) <= S) hi = mid; else lo = mid + 1;
+  }
+  const int64_t V = lo;
+  int pos = 0;
+  for (int t = 1; t <= S - 1; ++t) {
+    for (int j = pos + 1; j <= L; ++j) {
+      if (pre[j] - pre[pos] > V) break;
+      const int rest = S - t;  // parts left for rows [j, L)
+      if (L - j >= rest && min_parts(pre, j, L, V) <= rest) { cuts[t - 1] = (int16_t)j; pos = j; break; }
+    }
+  }
+}
+
+adaptis_status build_space(adaptis_ctx* ctx, const adaptis_problem* pr, const adaptis_space* sp,
+                           adaptis_prepared* P) {
+  adaptis_status st = validate(ctx, pr, sp);
+  if (st != ADAPTIS_OK) return st;
+  const adaptis_layers& Ly = pr->layers;
+  P->L = Ly.L; P->p = pr->p; P->m = pr->m; P->cap = pr->mem_cap_bytes;
+  P->tick_seconds = pr->tick_seconds; P->tokens_per_mb = pr->tokens_per_microbatch;
+  P->n_groups = sp->n_groups;
+  // binomials C(n, k) (saturating), n < kMaxBinomN, k <= MAX_S
+  P->h_binom.assign((size_t)kMaxBinomN * (ADAPTIS_MAX_S + 1), 0);
+  for (int n = 0; n < kMaxBinomN; ++n) {
+    uint64_t c = 1;  // C(n, 0); C(n, k) = C(n, k-1) * (n-k+1) / k, exact while it fits
+    for (int k = 0; k <= ADAPTIS_MAX_S && k <= n; ++k) {
+      if (k > 0) {
+        if (c == UINT64_MAX) { P->h_binom[(size_t)n * (ADAPTIS_MAX_S + 1) + k] = UINT64_MAX; continue; }
+        unsigned __int128 x = (unsigned __int128)c * (uint64_t)(n - k + 1) / (uint64_t)k;
+        c = x > (unsigned __int128)UINT64_MAX ? UINT64_MAX : (uint64_t)x;
+      }
+      P->h_binom[(size_t)n * (ADAPTIS_MAX_S + 1) + k] = c;
+    }
+  }
+  // L1-ball counts by the closed form sum_k 2^k C(n,k) C(r,k)
+  P->h_ball.assign((size_t)ADAPTIS_MAX_GROUPS * ADAPTIS_MAX_S * (kMaxRadius + 1), 0);
+  P->h_seeds.assign((size_t)ADAPTIS_MAX_GROUPS * ADAPTIS_MAX_S, 0);
+  auto C = [&](int n, int k) -> uint64_t {
+    if (k < 0 || k > n) return 0;
+    if (n < kMaxBinomN) return P->h_binom[(size_t)n * (ADAPTIS_MAX_S + 1) + std::min(k, n - k)];
+    return UINT64_MAX;
+  };
+  uint64_t total = 0;
+  P->segs.clear();
+  for (int g = 0; g < sp->n_groups; ++g) {
+    const adaptis_group& G = sp->group[g];
+    const int S = pr->p * G.v;
+    P->group_v[g] = G.v;
+    uint64_t parts;
+    if (G.part_mode == ADAPTIS_PART_FULL) {
+      parts = C(Ly.L - 1, S - 1);
+    } else {
+      for (int n = 0; n < ADAPTIS_MAX_S; ++n)
+        for (int r = 0; r <= G.radius; ++r) {
+          uint64_t t = 0;
+          for (int k = 0; k <= std::min(n, r); ++k)
+            t = sat_add(t, sat_mul(sat_mul(1ull << std::min(k, 63), C(n, k)), C(r, k)));
+          P->h_ball[((size_t)g * ADAPTIS_MAX_S + n) * (kMaxRadius + 1) + r] = t;
+        }
+      parts = P->h_ball[((size_t)g * ADAPTIS_MAX_S + (S - 1)) * (kMaxRadius + 1) + G.radius];
+      int16_t* seed = &P->h_seeds[(size_t)g * ADAPTIS_MAX_S];
+      if (G.seed_cuts) for (int i = 0; i < S - 1; ++i) seed[i] = G.seed_cuts[i];
+      else seed_minmax(Ly, S, seed);
+    }
+    for (int k = 0; k < 32; ++k) {
+      Seg s{};
+      if (!((G.combo_mask >> k) & 1u) || !combo_of(G.v, k, &s.placement, &s.policy)) continue;
+      s.group = g; s.combo = k; s.v = G.v; s.S = S; s.part_mode = G.part_mode; s.radius = G.radius;
+      s.base = total; s.count = parts;
+      if (parts == UINT64_MAX || total > ((1ull << 63) - 1) - parts)
+        return fail(ctx, ADAPTIS_EOVERFLOW, "space size does not fit in 63 bits");
+      total += parts;
+      P->segs.push_back(s);
+    }
+  }
+  P->N = total;
+  // packed key: makespan << key_bits | index must fit in 63 bits
+  int bits = 1;
+  while (bits < 63 && (total - 1) >> bits) ++bits;
+  P->key_bits = bits;
+  // makespan bound U: every schedule's makespan is a path through the task DAG
+  // plus list edges, so U = m * (sum of all durations + 2 * sum of boundary comms)
+  unsigned __int128 U = 0;
+  for (int l = 0; l < Ly.L; ++l) U += (unsigned __int128)(Ly.t_f[l] + Ly.t_b[l] + Ly.t_w[l]);
+  for (int l = 0; l + 1 < Ly.L; ++l) U += 2 * (unsigned __int128)Ly.comm_ticks[l];
+  U *= (unsigned __int128)pr->m;
+  if (bits >= 63 || U >= ((unsigned __int128)1 << (63 - bits)))
+    return fail(ctx, ADAPTIS_EOVERFLOW, "makespan bound and %d index bits exceed the 63-bit key", bits);
+  P->use_int64 = U >= ((unsigned __int128)1 << 31) - 1;
+  return ADAPTIS_OK;
+}
+
+adaptis_status upload(adaptis_ctx* ctx, const adaptis_problem* pr, adaptis_prepared* P) {
+  const adaptis_layers& Ly = pr->layers;
+  const int L = Ly.L;
+  std::vector<int64_t> cols((size_t)kNumCols * L);
+  for (int l = 0; l < L; ++l) {
+    cols[(size_t)kColTF * L + l] = Ly.t_f[l];
+    cols[(size_t)kColTB * L + l] = Ly.t_b[l];
+    cols[(size_t)kColTW * L + l] = Ly.t_w[l];
+    cols[(size_t)kColAct * L + l] = Ly.act_bytes[l];
+    cols[(size_t)kColStash * L + l] = Ly.stash_bytes[l];
+    cols[(size_t)kColWG * L + l] = Ly.weight_bytes[l] + Ly.grad_bytes[l];
+  }
+  std::vector<int64_t> comm(Ly.comm_ticks, Ly.comm_ticks + L);
+  comm[L - 1] = 0;
+  CU(ctx, cudaSetDevice(ctx->device));
+  CU(ctx, cudaMalloc(&P->d_cols, cols.size() * 8));
+  CU(ctx, cudaMalloc(&P->d_comm, comm.size() * 8));
+  CU(ctx, cudaMalloc(&P->d_binom, P->h_binom.size() * 8));
+  CU(ctx, cudaMalloc(&P->d_ball, P->h_ball.size() * 8));
+  CU(ctx, cudaMalloc(&P->d_seeds, P->h_seeds.size() * 2));
+  CU(ctx, cudaMemcpyAsync(P->d_cols, cols.data(), cols.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(P->d_comm, comm.data(), comm.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(P->d_binom, P->h_binom.data(), P->h_binom.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(P->d_ball, P->h_ball.data(), P->h_ball.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(P->d_seeds, P->h_seeds.data(), P->h_seeds.size() * 2, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors die on return
+  P->tabs.cols = P->d_cols; P->tabs.comm = P->d_comm; P->tabs.binom = P->d_binom;
+  P->tabs.ball = P->d_ball; P->tabs.seeds = P->d_seeds;
+  return ADAPTIS_OK;
+}
+
+adaptis_status ensure_scratch(adaptis_ctx* ctx, size_t words, size_t overflow_cap) {
+  if (words > ctx->scratch_words) {
+    if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+    ctx->d_scratch = nullptr;
+    CU(ctx, cudaMalloc(&ctx->d_scratch, words * 8));
+    ctx->scratch_words = words;
+  }
+  if (overflow_cap > ctx->overflow_cap) {
+    if (ctx->d_overflow) cudaFree(ctx->d_overflow);
+    ctx->d_overflow = nullptr;
+    CU(ctx, cudaMalloc(&ctx->d_overflow, overflow_cap * 8));
+    ctx->overflow_cap = overflow_cap;
+  }
+  if (!ctx->d_report) CU(ctx, cudaMalloc(&ctx->d_report, 3 * ADAPTIS_MAX_P * 8));
+  return ADAPTIS_OK;
+}
+
+// The block-cyclic shard of [lo, hi): chunks of 2^16 indices, chunk k -> rank k mod world.
+void shard(uint64_t lo, uint64_t hi, int rank, int world, SegLaunch* s) {
+  s->n_pos = 0; s->n0 = 0; s->start0 = lo; s->first_chunk = 0; s->world = world;
+  if (hi <= lo) return;
+  const uint64_t CH = 1ull << kChunkBits;
+  const uint64_t c_lo = lo >> kChunkBits, c_hi = (hi - 1) >> kChunkBits;
+  const uint64_t w = (uint64_t)world;
+  uint64_t c0 = c_lo + (((uint64_t)rank + w - (c_lo % w)) % w);
+  if (c0 > c_hi) return;
+  s->first_chunk = c0;
+  s->start0 = std::max(lo, c0 * CH);
+  const uint64_t end0 = std::min(hi, (c0 + 1) * CH);
+  s->n0 = end0 - s->start0;
+  uint64_t n = s->n0;
+  for (uint64_t c = c0 + w; c <= c_hi; c += w) n += std::min(hi, (c + 1) * CH) - c * CH;
+  s->n_pos = n;
+}
+
+constexpr size_t kOverflowPerSeg = 1u << 20;
+constexpr size_t kHdr = 4;
+
+SegLaunch make_launch(const adaptis_prepared* P, const Seg& sg) {
+  SegLaunch s{};
+  s.L = P->L; s.p = P->p; s.m = P->m; s.cap = P->cap;
+  int p2 = 1, lg = 0;
+  while (p2 < P->p) { p2 <<= 1; ++lg; }
+  s.p2 = p2; s.log2p2 = lg; s.G = 32 / p2;
+  s.v = sg.v; s.S = sg.S; s.placement = sg.placement; s.policy = sg.policy;
+  s.part_mode = sg.part_mode; s.radius = sg.radius; s.group = sg.group;
+  s.seg_base = sg.base;
+  s.key_bits = P->key_bits;
+  s.ring_k = kRingK;
+  s.use_int64 = P->use_int64 ? 1 : 0;
+  return s;
+}
+
+// Evaluate [lo, hi) (global indices) on this context's GPU: every segment it
+// touches is launched; overflowed candidates are re-run by the fallback kernel.
+// mode_search: pack keys into d_key; else write SoA results at idx - eval_first.
+adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uint64_t hi,
+                         bool mode_search, int rank, int world, const adaptis_results_soa* dout,
+                         uint64_t eval_first, int64_t* report, float* kernel_ms) {
+  const size_t nseg = P->segs.size();
+  // scratch words: [0] key, [1] invalid, [2] tasks, [4 + 2i] cursor i,
+  // [5 + 2i] overflow count i, then the same pair per segment for the fallback
+  adaptis_status st = ensure_scratch(ctx, kHdr + 4 * nseg, kOverflowPerSeg * nseg);
+  if (st != ADAPTIS_OK) return st;
+  unsigned long long* key = ctx->d_scratch;
+  unsigned long long* ninv = ctx->d_scratch + 1;
+  unsigned long long* ntask = ctx->d_scratch + 2;
+  std::vector<unsigned long long> init(kHdr + 4 * nseg, 0);
+  init[0] = (~0ull) >> 1;
+  CU(ctx, cudaMemcpyAsync(ctx->d_scratch, init.data(), init.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  std::vector<SegLaunch> launched(nseg);
+  std::vector<char> active(nseg, 0);
+  for (size_t i = 0; i < nseg; ++i) {
+    const Seg& sg = P->segs[i];
+    const uint64_t a = std::max(lo, sg.base), b = std::min(hi, sg.base + sg.count);
+    if (a >= b) continue;
+    SegLaunch s = make_launch(P, sg);
+    shard(a, b, rank, world, &s);
+    if (s.n_pos == 0) continue;
+    s.key = mode_search ? key : nullptr;
+    s.eval_first = eval_first;
+    if (!mode_search && dout) {
+      s.out_makespan = dout->makespan; s.out_peak = dout->peak_mem_bytes;
+      s.out_bubble = dout->bubble_ratio; s.out_status = dout->status;
+    }
+    s.out_report = report;
+    s.cursor = ctx->d_scratch + kHdr + 2 * i;
+    s.overflow_count = reinterpret_cast<unsigned int*>(ctx->d_scratch + kHdr + 1 + 2 * i);
+    s.overflow_idx = ctx->d_overflow + kOverflowPerSeg * i;
+    s.overflow_cap = (unsigned)kOverflowPerSeg;
+    s.n_invalid = ninv;
+    s.n_tasks = ntask;
+    int e = launch_segment(P->tabs, s, ctx->num_sms, ctx->stream, false, 0);
+    if (e) return fail(ctx, ADAPTIS_ECUDA, "kernel launch (segment %zu): %s", i, cudaGetErrorString((cudaError_t)e));
+    ctx->launches++;
+    launched[i] = s;
+    active[i] = 1;
+  }
+  // fallback for candidates whose fast-path rings filled up (exact re-run, rings >= m)
+  std::vector<unsigned long long> words(kHdr + 2 * nseg);
+  CU(ctx, cudaMemcpyAsync(words.data(), ctx->d_scratch, words.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  for (size_t i = 0; i < nseg; ++i) {
+    if (!active[i]) continue;
+    const unsigned int cnt = (unsigned int)(words[kHdr + 1 + 2 * i] & 0xffffffffu);
+    if (cnt == 0) continue;
+    SegLaunch s = launched[i];
+    int K = 1;
+    while (K < P->m) K <<= 1;
+    s.ring_k = K;
+    if (cnt <= kOverflowPerSeg) {
+      s.list_idx = s.overflow_idx;
+      s.n_pos = cnt;
+    }  // else: re-run the whole segment shard in fallback mode
+    s.cursor = ctx->d_scratch + kHdr + 2 * nseg + 2 * i;
+    s.overflow_count = reinterpret_cast<unsigned int*>(ctx->d_scratch + kHdr + 1 + 2 * nseg + 2 * i);
+    s.overflow_cap = 0;
+    const size_t tsz = P->use_int64 ? 8 : 4;
+    const size_t per_warp = (size_t)2 * K * s.G * s.S * tsz;
+    const size_t budget = (size_t)1 << 30;
+    unsigned grid_limit = (unsigned)std::max<size_t>(1, budget / (per_warp * kWarpsPerCta));
+    grid_limit = std::min<unsigned>(grid_limit, (unsigned)ctx->num_sms * 8);
+    const size_t need = per_warp * kWarpsPerCta * grid_limit;
+    if (need > ctx->gring_bytes) {
+      if (ctx->d_gring) cudaFree(ctx->d_gring);
+      ctx->d_gring = nullptr;
+      CU(ctx, cudaMalloc(&ctx->d_gring, need));
+      ctx->gring_bytes = need;
+    }
+    s.gring = ctx->d_gring;
+    int e = launch_segment(P->tabs, s, ctx->num_sms, ctx->stream, true, grid_limit);
+    if (e) return fail(ctx, ADAPTIS_ECUDA, "fallback launch: %s", cudaGetErrorString((cudaError_t)e));
+    ctx->launches++;
+  }
+  CU(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  if (kernel_ms) CU(ctx, cudaEventElapsedTime(kernel_ms, ctx->ev0, ctx->ev1));
+  return ADAPTIS_OK;
+}
+
+}  // namespace
+
+// ================================================================================
+extern "C" {
+
+const char* adaptis_status_str(adaptis_status s) {
+  switch (s) {
+    case ADAPTIS_OK: return "ok";
+    case ADAPTIS_EINVAL: return "invalid argument";
+    case ADAPTIS_EINFEASIBLE: return "no feasible candidate";
+    case ADAPTIS_EOVERFLOW: return "key overflow";
+    case ADAPTIS_ECUDA: return "cuda error";
+    case ADAPTIS_ECOLL: return "collective error";
+  }
+  return "unknown";
+}
+
+const char* adaptis_last_error(const adaptis_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_tls_error.c_str();
+}
+
+adaptis_status adaptis_ctx_create(int cuda_device, int rank, int world, adaptis_ctx** out) {
+  if (!out) return fail(nullptr, ADAPTIS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(nullptr, ADAPTIS_EINVAL, "rank = %d, world = %d", rank, world);
+  adaptis_ctx* c = new adaptis_ctx();
+  c->device = cuda_device; c->rank = rank; c->world = world;
+  cudaError_t e = cudaSetDevice(cuda_device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e != cudaSuccess) {
+    fail(nullptr, ADAPTIS_ECUDA, "device %d: %s", cuda_device, cudaGetErrorString(e));
+    delete c;
+    return ADAPTIS_ECUDA;
+  }
+  *out = c;
+  return ADAPTIS_OK;
+}
+
+void adaptis_ctx_destroy(adaptis_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  cudaFree(c->d_scratch); cudaFree(c->d_overflow); cudaFree(c->d_gring); cudaFree(c->d_report);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_allreduce_min_fn fn, void* user) {
+  if (!ctx) return fail(nullptr, ADAPTIS_EINVAL, "ctx is NULL");
+  ctx->allreduce = fn; ctx->allreduce_user = user;
+  return ADAPTIS_OK;
+}
+
+void* adaptis_ctx_stream(adaptis_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+uint64_t adaptis_ctx_launch_count(const adaptis_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+adaptis_status adaptis_space_size(const adaptis_problem* problem, const adaptis_space* space,
+                                  uint64_t* n_out) {
+  if (!n_out) return fail(nullptr, ADAPTIS_EINVAL, "n_out is NULL");
+  adaptis_prepared P;
+  adaptis_status st = build_space(nullptr, problem, space, &P);
+  if (st != ADAPTIS_OK) return st;
+  *n_out = P.N;
+  return ADAPTIS_OK;
+}
+
+static void fill_plan(const adaptis_prepared& P, uint64_t index, adaptis_plan* out, bool* valid) {
+  memset(out, 0, sizeof(*out));
+  for (const Seg& s : P.segs) {
+    if (index < s.base || index >= s.base + s.count) continue;
+    out->v = s.v; out->placement = s.placement; out->policy = s.policy; out->S = s.S;
+    bool ok = decode_cuts(P.h_binom.data(), P.h_ball.data(), P.h_seeds.data(), s.group, s.part_mode,
+                          s.radius, s.S, P.L, index - s.base, out->cuts);
+    if (valid) *valid = ok;
+    return;
+  }
+}
+
+adaptis_status adaptis_decode(const adaptis_problem* problem, const adaptis_space* space,
+                              uint64_t index, adaptis_plan* out) {
+  if (!out) return fail(nullptr, ADAPTIS_EINVAL, "out is NULL");
+  adaptis_prepared P;
+  adaptis_status st = build_space(nullptr, problem, space, &P);
+  if (st != ADAPTIS_OK) return st;
+  if (index >= P.N) return fail(nullptr, ADAPTIS_EINVAL, "index %llu >= |space| = %llu",
+                                (unsigned long long)index, (unsigned long long)P.N);
+  fill_plan(P, index, out, nullptr);
+  return ADAPTIS_OK;
+}
+
+adaptis_status adaptis_prepare(adaptis_ctx* ctx, const adaptis_problem* problem,
+                               const adaptis_space* space, adaptis_prepared** out) {
+  if (!ctx) return fail(nullptr, ADAPTIS_EINVAL, "ctx is NULL");
+  if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");
+  *out = nullptr;
+  adaptis_prepared* P = new adaptis_prepared();
+  adaptis_status st = build_space(ctx, problem, space, P);
+  if (st == ADAPTIS_OK) st = upload(ctx, problem, P);
+  if (st != ADAPTIS_OK) { adaptis_prepared_free(P); return st; }
+  P->owner = ctx;
+  *out = P;
+  return ADAPTIS_OK;
+}
+
+void adaptis_prepared_free(adaptis_prepared* P) {
+  if (!P) return;
+  cudaFree(P->d_cols); cudaFree(P->d_comm); cudaFree(P->d_binom); cudaFree(P->d_ball);
+  cudaFree(P->d_seeds);
+  delete P;
+}
+
+adaptis_status adaptis_eval_prepared(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t first,
+                                     uint64_t count, const adaptis_results_soa* out,
+                                     int out_on_device) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");
+  if (first > P->N || count > P->N - first)
+    return fail(ctx, ADAPTIS_EINVAL, "range [%llu, +%llu) exceeds |space| = %llu",
+                (unsigned long long)first, (unsigned long long)count, (unsigned long long)P->N);
+  if (count == 0) return ADAPTIS_OK;
+  CU(ctx, cudaSetDevice(ctx->device));
+  adaptis_results_soa dout = *out;
+  void* tmp[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (!out_on_device) {
+    if (out->makespan) { CU(ctx, cudaMalloc(&tmp[0], count * 8)); dout.makespan = (int64_t*)tmp[0]; }
+    if (out->peak_mem_bytes) { CU(ctx, cudaMalloc(&tmp[1], count * 8)); dout.peak_mem_bytes = (int64_t*)tmp[1]; }
+    if (out->bubble_ratio) { CU(ctx, cudaMalloc(&tmp[2], count * 4)); dout.bubble_ratio = (float*)tmp[2]; }
+    if (out->status) { CU(ctx, cudaMalloc(&tmp[3], count)); dout.status = (uint8_t*)tmp[3]; }
+  }
+  adaptis_status st = run_range(ctx, P, first, first + count, false, 0, 1, &dout, first, nullptr, nullptr);
+  if (st == ADAPTIS_OK && !out_on_device) {
+    if (out->makespan) CU(ctx, cudaMemcpyAsync(out->makespan, tmp[0], count * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->peak_mem_bytes) CU(ctx, cudaMemcpyAsync(out->peak_mem_bytes, tmp[1], count * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->bubble_ratio) CU(ctx, cudaMemcpyAsync(out->bubble_ratio, tmp[2], count * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->status) CU(ctx, cudaMemcpyAsync(out->status, tmp[3], count, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  for (void* t : tmp) if (t) cudaFree(t);
+  return st;
+}
+
+adaptis_status adaptis_eval_batch(adaptis_ctx* ctx, const adaptis_problem* problem,
+                                  const adaptis_space* space, uint64_t first, uint64_t count,
+                                  const adaptis_results_soa* out, int out_on_device) {
+  adaptis_prepared* P = nullptr;
+  adaptis_status st = adaptis_prepare(ctx, problem, space, &P);
+  if (st != ADAPTIS_OK) return st;
+  st = adaptis_eval_prepared(ctx, P, first, count, out, out_on_device);
+  adaptis_prepared_free(P);
+  return st;
+}
+
+adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, adaptis_best* out) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");
+  if (ctx->world > 1 && !ctx->allreduce)
+    return fail(ctx, ADAPTIS_EINVAL, "world = %d needs adaptis_ctx_set_allreduce", ctx->world);
+  CU(ctx, cudaSetDevice(ctx->device));
+  memset(out, 0, sizeof(*out));
+  float ms = 0;
+  adaptis_status st = run_range(ctx, P, 0, P->N, true, ctx->rank, ctx->world, nullptr, 0, nullptr, &ms);
+  if (st != ADAPTIS_OK) return st;
+  unsigned long long words[3] = {0, 0, 0};
+  CU(ctx, cudaMemcpyAsync(words, ctx->d_scratch, 24, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  out->n_invalid = words[1];
+  out->n_tasks = words[2];
+  out->kernel_ms = ms;
+  out->n_candidates = P->N;
+  {
+    SegLaunch tmp{};
+    uint64_t n = 0;
+    for (const Seg& sg : P->segs) { shard(sg.base, sg.base + sg.count, ctx->rank, ctx->world, &tmp); n += tmp.n_pos; }
+    out->n_evaluated = n;
+  }
+  if (ctx->world > 1) {  // one 8-byte allreduce(MIN) over the ranks
+    if (ctx->allreduce(reinterpret_cast<int64_t*>(ctx->d_scratch), (void*)ctx->stream, ctx->allreduce_user) != 0)
+      return fail(ctx, ADAPTIS_ECOLL, "allreduce callback failed");
+    CU(ctx, cudaMemcpyAsync(words, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  const unsigned long long key = words[0];
+  out->p = P->p;
+  if (key == (~0ull >> 1)) {
+    out->index = UINT64_MAX;
+    out->result.makespan = INT64_MAX;
+    return fail(ctx, ADAPTIS_EINFEASIBLE, "no candidate satisfies the memory constraint (Eq. 2)");
+  }
+  const uint64_t idx = key & ((1ull << P->key_bits) - 1);
+  out->index = idx;
+  fill_plan(*P, idx, &out->plan, nullptr);
+  // winner report: the same kernel on the single winning index
+  std::vector<int64_t> rep(3 * P->p);
+  int64_t mk = 0, pk = 0; float bub = 0; uint8_t stt = 0;
+  int64_t *dmk = nullptr, *dpk = nullptr; float* dbub = nullptr; uint8_t* dst = nullptr;
+  CU(ctx, cudaMalloc(&dmk, 8)); CU(ctx, cudaMalloc(&dpk, 8)); CU(ctx, cudaMalloc(&dbub, 4)); CU(ctx, cudaMalloc(&dst, 1));
+  adaptis_results_soa so{dmk, dpk, dbub, dst};
+  st = run_range(ctx, P, idx, idx + 1, false, 0, 1, &so, idx, ctx->d_report, nullptr);
+  if (st == ADAPTIS_OK) {
+    CU(ctx, cudaMemcpyAsync(&mk, dmk, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(&pk, dpk, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(&bub, dbub, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(&stt, dst, 1, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(rep.data(), ctx->d_report, rep.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  cudaFree(dmk); cudaFree(dpk); cudaFree(dbub); cudaFree(dst);
+  if (st != ADAPTIS_OK) return st;
+  out->result.makespan = mk;
+  out->result.peak_mem_bytes = pk;
+  out->result.bubble_ratio = bub;
+  out->result.status = stt;
+  out->result.throughput = (mk > 0 && P->tick_seconds > 0)
+      ? (double)P->m * (double)P->tokens_per_mb / ((double)mk * P->tick_seconds) : 0.0;
+  for (int d = 0; d < P->p; ++d) {
+    out->T_d[d] = rep[d];
+    out->busy_d[d] = rep[P->p + d];
+    out->M_d[d] = rep[2 * P->p + d];
+  }
+  if (mk != (int64_t)(key >> P->key_bits))
+    return fail(ctx, ADAPTIS_ECUDA, "winner re-evaluation disagrees with its search key");
+  return ADAPTIS_OK;
+}
+
+adaptis_status adaptis_search(adaptis_ctx* ctx, const adaptis_problem* problem,
+                              const adaptis_space* space, adaptis_best* out) {
+  adaptis_prepared* P = nullptr;
+  adaptis_status st = adaptis_prepare(ctx, problem, space, &P);
+  if (st != ADAPTIS_OK) return st;
+  st = adaptis_search_prepared(ctx, P, out);
+  adaptis_prepared_free(P);
+  return st;
+}
+
+}  // extern "C"
