@@ -177,6 +177,9 @@ ADAPTIS_API adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_a
 ADAPTIS_API void*          adaptis_ctx_stream(adaptis_ctx* ctx);
 /* Number of kernel launches this context has issued since creation. */
 ADAPTIS_API uint64_t       adaptis_ctx_launch_count(const adaptis_ctx* ctx);
+/* Candidates re-evaluated by the exact fallback kernel (shared-memory rings
+ * too small for their dependency lag) since creation. */
+ADAPTIS_API uint64_t       adaptis_ctx_fallback_count(const adaptis_ctx* ctx);
 
 /* |space| for this problem (the candidate space). EINVAL on an
  * invalid problem/space; EOVERFLOW if the count does not fit in 63 bits. */

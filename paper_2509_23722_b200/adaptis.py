@@ -109,6 +109,8 @@ def lib():
             L.adaptis_ctx_stream.argtypes = [C.c_void_p]
             L.adaptis_ctx_launch_count.restype = C.c_uint64
             L.adaptis_ctx_launch_count.argtypes = [C.c_void_p]
+            L.adaptis_ctx_fallback_count.restype = C.c_uint64
+            L.adaptis_ctx_fallback_count.argtypes = [C.c_void_p]
             L.adaptis_space_size.restype = st
             L.adaptis_space_size.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.POINTER(C.c_uint64)]
             L.adaptis_decode.restype = st
@@ -238,6 +240,10 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(lib().adaptis_ctx_launch_count(self.ptr))
+
+    @property
+    def fallback_count(self) -> int:
+        return int(lib().adaptis_ctx_fallback_count(self.ptr))
 
     def close(self):
         if self.ptr:

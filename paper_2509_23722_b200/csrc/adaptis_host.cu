@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -75,6 +76,7 @@ struct adaptis_ctx {
   void* allreduce_user = nullptr;
   std::string err;
   uint64_t launches = 0;
+  uint64_t fallback_cands = 0;
   // scratch
   unsigned long long* d_scratch = nullptr;  // [0] key, [1] n_invalid, [2..] cursors/overflow counts
   size_t scratch_words = 0;
@@ -349,7 +351,41 @@ void shard(uint64_t lo, uint64_t hi, int rank, int world, SegLaunch* s) {
 }
 
 constexpr size_t kOverflowPerSeg = 1u << 20;
+
+// fast-path ring slots per stage and direction: GREEDY's F-first rule lets a
+// producer run further ahead than the fixed orders do (DESIGN.md §"Rings")
+int ring_slots(int policy, int m) {
+  int k = kRingK;
+  if (policy == ADAPTIS_GREEDY) k = 32;
+  const char* e = getenv(policy == ADAPTIS_GREEDY ? "ADAPTIS_RING_K_GREEDY" : "ADAPTIS_RING_K");
+  if (e && atoi(e) > 0) k = atoi(e);
+  int mp = 1;
+  while (mp < m) mp <<= 1;
+  if (k > mp) k = mp;
+  int pw = 1;
+  while (pw < k) pw <<= 1;
+  return pw;
+}
 constexpr size_t kHdr = 4;
+
+// global-memory ring scratch for a launch with s.ring_k slots; bounds the grid
+adaptis_status ensure_gring(adaptis_ctx* ctx, const adaptis_prepared* P, const SegLaunch& s,
+                            unsigned* grid_limit) {
+  const size_t tsz = P->use_int64 ? 8 : 4;
+  const size_t per_warp = (size_t)2 * s.ring_k * s.G * s.S * tsz;
+  const size_t budget = (size_t)1 << 30;
+  unsigned gl = (unsigned)std::max<size_t>(1, budget / (per_warp * kWarpsPerCta));
+  gl = std::min<unsigned>(gl, (unsigned)ctx->num_sms * 8);
+  const size_t need = per_warp * kWarpsPerCta * gl;
+  if (need > ctx->gring_bytes) {
+    if (ctx->d_gring) cudaFree(ctx->d_gring);
+    ctx->d_gring = nullptr;
+    CU(ctx, cudaMalloc(&ctx->d_gring, need));
+    ctx->gring_bytes = need;
+  }
+  *grid_limit = gl;
+  return ADAPTIS_OK;
+}
 
 SegLaunch make_launch(const adaptis_prepared* P, const Seg& sg) {
   SegLaunch s{};
@@ -361,7 +397,7 @@ SegLaunch make_launch(const adaptis_prepared* P, const Seg& sg) {
   s.part_mode = sg.part_mode; s.radius = sg.radius; s.group = sg.group;
   s.seg_base = sg.base;
   s.key_bits = P->key_bits;
-  s.ring_k = kRingK;
+  s.ring_k = ring_slots(sg.policy, P->m);
   s.use_int64 = P->use_int64 ? 1 : 0;
   return s;
 }
@@ -406,7 +442,22 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     s.overflow_cap = (unsigned)kOverflowPerSeg;
     s.n_invalid = ninv;
     s.n_tasks = ntask;
-    int e = launch_segment(P->tabs, s, ctx->num_sms, ctx->stream, false, 0);
+    // GREEDY with m beyond the shared-memory ring depth: full-depth rings in
+    // global memory from the start (its F-first rule can run m items ahead)
+    const bool direct_global = s.policy == ADAPTIS_GREEDY && P->m > s.ring_k;
+    int e;
+    if (direct_global) {
+      int K = 1;
+      while (K < P->m) K <<= 1;
+      s.ring_k = K;
+      unsigned grid_limit = 0;
+      st = ensure_gring(ctx, P, s, &grid_limit);
+      if (st != ADAPTIS_OK) return st;
+      s.gring = ctx->d_gring;
+      e = launch_segment(P->tabs, s, ctx->num_sms, ctx->stream, true, grid_limit);
+    } else {
+      e = launch_segment(P->tabs, s, ctx->num_sms, ctx->stream, false, 0);
+    }
     if (e) return fail(ctx, ADAPTIS_ECUDA, "kernel launch (segment %zu): %s", i, cudaGetErrorString((cudaError_t)e));
     ctx->launches++;
     launched[i] = s;
@@ -420,6 +471,7 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     if (!active[i]) continue;
     const unsigned int cnt = (unsigned int)(words[kHdr + 1 + 2 * i] & 0xffffffffu);
     if (cnt == 0) continue;
+    ctx->fallback_cands += cnt;
     SegLaunch s = launched[i];
     int K = 1;
     while (K < P->m) K <<= 1;
@@ -431,18 +483,9 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     s.cursor = ctx->d_scratch + kHdr + 2 * nseg + 2 * i;
     s.overflow_count = reinterpret_cast<unsigned int*>(ctx->d_scratch + kHdr + 1 + 2 * nseg + 2 * i);
     s.overflow_cap = 0;
-    const size_t tsz = P->use_int64 ? 8 : 4;
-    const size_t per_warp = (size_t)2 * K * s.G * s.S * tsz;
-    const size_t budget = (size_t)1 << 30;
-    unsigned grid_limit = (unsigned)std::max<size_t>(1, budget / (per_warp * kWarpsPerCta));
-    grid_limit = std::min<unsigned>(grid_limit, (unsigned)ctx->num_sms * 8);
-    const size_t need = per_warp * kWarpsPerCta * grid_limit;
-    if (need > ctx->gring_bytes) {
-      if (ctx->d_gring) cudaFree(ctx->d_gring);
-      ctx->d_gring = nullptr;
-      CU(ctx, cudaMalloc(&ctx->d_gring, need));
-      ctx->gring_bytes = need;
-    }
+    unsigned grid_limit = 0;
+    st = ensure_gring(ctx, P, s, &grid_limit);
+    if (st != ADAPTIS_OK) return st;
     s.gring = ctx->d_gring;
     int e = launch_segment(P->tabs, s, ctx->num_sms, ctx->stream, true, grid_limit);
     if (e) return fail(ctx, ADAPTIS_ECUDA, "fallback launch: %s", cudaGetErrorString((cudaError_t)e));
@@ -515,6 +558,7 @@ adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_allreduce_min
 
 void* adaptis_ctx_stream(adaptis_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 uint64_t adaptis_ctx_launch_count(const adaptis_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t adaptis_ctx_fallback_count(const adaptis_ctx* ctx) { return ctx ? ctx->fallback_cands : 0; }
 
 adaptis_status adaptis_space_size(const adaptis_problem* problem, const adaptis_space* space,
                                   uint64_t* n_out) {

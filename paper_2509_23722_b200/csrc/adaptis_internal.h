@@ -63,6 +63,34 @@ struct SegLaunch {
   int use_int64;                // 0: int32 ticks (host-proved bound), 1: int64 ticks
 };
 
+#ifdef __CUDACC__
+#define ADAPTIS_LAYOUT_HD __host__ __device__ __forceinline__
+#else
+#define ADAPTIS_LAYOUT_HD inline
+#endif
+
+// Shared-memory layout of one warp of the segment kernel (after the CTA's
+// prefix table): task records [3 kinds][V chunks][32 lanes], memory deltas
+// (split policies), the slots' cuts, and the fast-path rings
+// [2 directions][K slots][G*S stages].
+struct WarpLayout {
+  int rec_off, dmem_off, cuts_off, ring_off, per_warp;
+  ADAPTIS_LAYOUT_HD size_t prefix_bytes(int L) const {
+    return ((size_t)kNumCols * (L + 1) * 8 + 15) & ~(size_t)15;
+  }
+};
+ADAPTIS_LAYOUT_HD int align16(int x) { return (x + 15) & ~15; }
+ADAPTIS_LAYOUT_HD WarpLayout warp_layout(int S, int G, int V, int K, int tsz, int rsz, bool gring) {
+  WarpLayout l;
+  int off = 0;
+  l.rec_off = off;  off += 3 * V * 32 * rsz;
+  l.dmem_off = off; off += 3 * V * 32 * 8;
+  l.cuts_off = off; off += align16(G * (S + 1) * 2);
+  l.ring_off = off; if (!gring) off += 2 * K * G * S * tsz;
+  l.per_warp = align16(off);
+  return l;
+}
+
 // launchers implemented in adaptis_kernels.cu
 int launch_segment(const DevTables& t, const SegLaunch& s, int num_sms, void* stream,
                    bool fallback, unsigned grid_limit);

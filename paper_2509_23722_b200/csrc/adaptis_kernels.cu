@@ -1,21 +1,24 @@
 // adaptis_kernels.cu — sm_100a kernels of the AdaPtis hot path (arXiv 2509.23722).
 //
 // One persistent kernel per (v-group, combo) segment of the candidate space.
-// Each warp evaluates G = 32 / p2 candidates at a time (p2 = p rounded up to a
-// power of two); within a candidate slot, lane d is pipeline device d. Per
-// candidate the warp runs, in order (DESIGN.md §"Kernel"):
-//   a1 decode        index -> cuts (colex / L1-ball unranking, one lane per slot)
+// A warp holds G = 32 / p2 candidate slots (p2 = p rounded up to a power of
+// two); inside a slot, lane d is pipeline device d. Slots are refilled
+// independently from a warp-local queue of index positions, so invalid and
+// over-capacity candidates never occupy simulation rounds. Per candidate
+// (DESIGN.md §"Kernel"):
+//   a1 decode        index -> cuts (colex / L1-ball unranking, lane 0 of the slot)
 //   a2 stage sums    prefix differences of the CTA's shared-memory prefix table,
 //                    built once per CTA by a warp-shuffle scan of coalesced loads
-//   a3 device sums   static memory, busy time, edge latencies (R3-R6)
-//   a4 memory check  fused fixed orders: exact peak from the order alone (R16)
+//   a3 device sums   static memory, busy time, edge latencies (R3-R6), folded
+//                    into per-(kind, chunk) task records in shared memory
+//   a4 memory check  fused fixed orders: exact peak from the order alone (R16,
+//                    periodic closed form for the Megatron interleaved order)
 //   a5 simulation    dataflow rounds (GPIPE / ONEF1B / ZB, Lemmas 1-2) or
-//                    bounded-lag rounds (GREEDY, Lemma 3); cross-device
-//                    finish times travel through per-stage shared-memory rings
+//                    bounded-lag rounds (GREEDY, Lemma 3); cross-device arrival
+//                    times travel through per-stage rings in shared memory
 //   a6 metrics       segmented shuffle reductions (makespan, busy, peak)
 //   a7 argmin        packed (makespan << bits | index) warp min -> atomicMin
-// Timing is integer ticks: int32 when the host proved the makespan bound fits,
-// int64 otherwise (bit-exact either way).
+// Ticks are int32 when the host proved the makespan bound fits, else int64.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -27,17 +30,21 @@
 namespace adaptis {
 
 constexpr unsigned FULLMASK = 0xffffffffu;
+constexpr int kQueueBlock = 64;  // positions claimed per warp atomic
 
 template <typename T> struct TT;
 template <> struct TT<int32_t> { static constexpr int32_t INF = INT32_MAX; };
 template <> struct TT<int64_t> { static constexpr int64_t INF = INT64_MAX; };
 
 template <typename T>
-struct StageC {   // per (lane, own chunk) constants of one candidate
-  T dF, dB, dW;   // task durations (dB includes c_W when fused, R2)
-  T oF, oB;       // latency added to F(s) -> F(s+1) and B(s) -> B(s-1) (R3-R6)
-  int64_t act, stash;
+struct __align__(16) Rec {  // one task kind of one own stage (chunk) of a lane
+  T dur;        // duration (B includes c_W when fused, R2)
+  T oc;         // latency added to the successor's arrival (R3-R6; 0 when co-located)
+  int in_off;   // ring offset of the input slot row, -1 = no cross-stage input
+  int out_off;  // ring offset of the output slot row, -1 = no successor
 };
+
+enum : int { F_INVALID = 1, F_PREOVER = 2, F_STUCK = 4, F_OVERFLOW = 8 };
 
 __device__ __forceinline__ int stage_of(int placement, int p, int c, int d) {
   if (placement == ADAPTIS_SEQ) return d;
@@ -47,69 +54,92 @@ __device__ __forceinline__ int stage_of(int placement, int p, int c, int d) {
 __device__ __forceinline__ int dev_of(int placement, int p, int s) {
   if (placement == ADAPTIS_SEQ) return s;
   if (placement == ADAPTIS_INTERLEAVED) return s % p;
-  int c = s / p, j = s - c * p;
+  const int c = s / p, j = s - c * p;
   return (c & 1) ? p - 1 - j : j;
 }
 
 template <typename X>
-__device__ __forceinline__ X shfl_xor(X v, int o) { return __shfl_xor_sync(FULLMASK, v, o); }
-
-// segmented reductions over aligned groups of p2 lanes
-template <typename X>
 __device__ __forceinline__ X seg_max(X v, int p2) {
-  for (int o = 1; o < p2; o <<= 1) { X w = shfl_xor(v, o); v = w > v ? w : v; }
+  for (int o = 1; o < p2; o <<= 1) { X w = __shfl_xor_sync(FULLMASK, v, o); v = w > v ? w : v; }
   return v;
 }
 template <typename X>
 __device__ __forceinline__ X seg_min(X v, int p2) {
-  for (int o = 1; o < p2; o <<= 1) { X w = shfl_xor(v, o); v = w < v ? w : v; }
+  for (int o = 1; o < p2; o <<= 1) { X w = __shfl_xor_sync(FULLMASK, v, o); v = w < v ? w : v; }
   return v;
 }
 template <typename X>
 __device__ __forceinline__ X seg_sum(X v, int p2) {
-  for (int o = 1; o < p2; o <<= 1) v += shfl_xor(v, o);
+  for (int o = 1; o < p2; o <<= 1) v += __shfl_xor_sync(FULLMASK, v, o);
   return v;
+}
+template <typename T>
+__device__ __forceinline__ T sat_add(T a, T b) {
+  return a > TT<T>::INF - b ? TT<T>::INF : a + b;
 }
 
 // incremental position in Megatron's virtual order (R10): k -> (chunk, mb)
 struct VPos {
-  int q, c, g;  // k = (g * v + c) * p + q
-  __device__ __forceinline__ void reset() { q = 0; c = 0; g = 0; }
+  int q, c, mb0;  // k = (g * v + c) * p + q, mb = g * p + q = mb0 + q
+  __device__ __forceinline__ void reset() { q = 0; c = 0; mb0 = 0; }
   __device__ __forceinline__ void next(int p, int v) {
-    if (++q == p) { q = 0; if (++c == v) { c = 0; ++g; } }
+    if (++q == p) { q = 0; if (++c == v) { c = 0; mb0 += p; } }
   }
-  __device__ __forceinline__ int mb(int p) const { return g * p + q; }
+  __device__ __forceinline__ int mb() const { return mb0 + q; }
 };
+
+// R16 for the Megatron order (R9/R10): the in-flight bytes right after the
+// (w+i+1)-th forward and before the (i+1)-th backward are
+// D(i) = Fsum(w+i+1) - Bsum(i), and D is periodic in i with period p*v, so the
+// peak of the whole list is max(D(i), i < min(p*v, m*v - w)) (Fsum(m*v) when
+// the warm-up covers everything).
+template <int V>
+__device__ __forceinline__ int64_t chunk_prefix(const int64_t (&a)[V], int p, int n, bool bwd) {
+  const int P = p * V;
+  const int q = n / P, r = n - q * P, cf = r / p;
+  int64_t A = 0, s = 0;
+#pragma unroll
+  for (int c = 0; c < V; ++c) {
+    const int64_t ac = bwd ? a[V - 1 - c] : a[c];
+    A += ac;
+    if (c < cf) s += (int64_t)p * ac;
+    if (c == cf) s += (int64_t)(r - cf * p) * ac;
+  }
+  return (int64_t)q * p * A + s;
+}
+template <int V>
+__device__ int64_t megatron_peak(const int64_t (&a)[V], int p, int m, int w) {
+  const int tot = m * V;
+  if (w >= tot) return chunk_prefix<V>(a, p, tot, false);
+  const int lim = min(p * V, tot - w);
+  int64_t best = 0;
+  for (int i = 0; i < lim; ++i) {
+    const int64_t x = chunk_prefix<V>(a, p, w + i + 1, false) - chunk_prefix<V>(a, p, i, true);
+    best = x > best ? x : best;
+  }
+  return best;
+}
 
 __device__ __forceinline__ uint64_t pos_to_index(const SegLaunch& sl, uint64_t pos) {
   if (sl.list_idx) return sl.list_idx[pos];
   if (pos < sl.n0) return sl.start0 + pos;
-  uint64_t q = pos - sl.n0;
-  uint64_t t = q >> kChunkBits;
+  const uint64_t q = pos - sl.n0;
+  const uint64_t t = q >> kChunkBits;
   return ((sl.first_chunk + (t + 1) * (uint64_t)sl.world) << kChunkBits) +
          (q & ((1ull << kChunkBits) - 1));
 }
 
-// ------------------------------------------------------------------------------
-// Ring addressing: ring[dir][slot j % K][cand g][stage s]
-template <typename T>
-struct Rings {
-  T* base;
-  int K, RS, gS;  // RS = G*S row stride, gS = g*S
-  __device__ __forceinline__ T* at(int dir, int j, int s) const {
-    return base + ((size_t)dir * K + (j & (K - 1))) * RS + gS + s;
-  }
-};
-
-template <int POLICY, int V, typename T, bool FALLBACK>
+template <int POLICY, int V, typename T, bool GRING>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 seg_kernel(const DevTables tab, const SegLaunch sl) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int L = sl.L, p = sl.p, m = sl.m, S = sl.S, p2 = sl.p2, G = sl.G;
   constexpr bool FUSED = (POLICY == ADAPTIS_GPIPE || POLICY == ADAPTIS_ONEF1B);
+  constexpr bool ZB = (POLICY == ADAPTIS_ZB);
+  constexpr bool GREEDY = (POLICY == ADAPTIS_GREEDY);
   constexpr T INF = TT<T>::INF;
   constexpr T EMPTY = (T)-1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int L = sl.L, p = sl.p, m = sl.m, S = sl.S, p2 = sl.p2, G = sl.G;
 
   // ---- a2 prologue: per-CTA prefix table of the layer columns (warp-shuffle scan)
   int64_t* pre = reinterpret_cast<int64_t*>(smem);
@@ -119,9 +149,10 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
     int64_t* dst = pre + (size_t)col * (L + 1);
     if (lane == 0) dst[0] = 0;
     for (int b = 0; b < L; b += 32) {
-      int64_t x = (b + lane < L) ? src[b + lane] : 0;   // coalesced 8-byte loads
+      int64_t x = (b + lane < L) ? src[b + lane] : 0;  // coalesced 8-byte loads
+#pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int64_t y = __shfl_up_sync(FULLMASK, x, o);
+        const int64_t y = __shfl_up_sync(FULLMASK, x, o);
         if (lane >= o) x += y;
       }
       if (b + lane < L) dst[b + lane + 1] = carry + x;
@@ -130,369 +161,93 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   }
   __syncthreads();
 
-  // ---- per-warp shared regions
-  size_t off = ((size_t)kNumCols * (L + 1) * 8 + 15) & ~(size_t)15;
-  const size_t cuts_bytes = (((size_t)G * (S + 1) * 2) + 15) & ~(size_t)15;
-  const size_t sc_bytes = (size_t)(V > 1 ? V : 0) * 32 * sizeof(StageC<T>);
-  const size_t ring_bytes = FALLBACK ? 0 : (size_t)2 * sl.ring_k * G * S * sizeof(T);
-  const size_t per_warp = cuts_bytes + sc_bytes + ring_bytes;
-  unsigned char* wbase = smem + off + per_warp * warp;
-  int16_t* cuts_all = reinterpret_cast<int16_t*>(wbase);
-  StageC<T>* scs = reinterpret_cast<StageC<T>*>(wbase + cuts_bytes);
-  T* ring_base;
-  if constexpr (FALLBACK) {
+  // ---- per-warp shared regions (layout mirrored by smem_bytes())
+  const WarpLayout lay =
+      warp_layout(S, G, V, sl.ring_k, (int)sizeof(T), (int)sizeof(Rec<T>), GRING);
+  unsigned char* wbase = smem + lay.prefix_bytes(L) + (size_t)lay.per_warp * warp;
+  Rec<T>* recs = reinterpret_cast<Rec<T>*>(wbase + lay.rec_off);
+  int64_t* dmem = reinterpret_cast<int64_t*>(wbase + lay.dmem_off);
+  int16_t* cuts_all = reinterpret_cast<int16_t*>(wbase + lay.cuts_off);
+  T* ring;
+  if constexpr (GRING) {
     const size_t gw = (size_t)blockIdx.x * kWarpsPerCta + warp;
-    ring_base = reinterpret_cast<T*>(sl.gring) + gw * 2 * (size_t)sl.ring_k * G * S;
+    ring = reinterpret_cast<T*>(sl.gring) + gw * 2 * (size_t)sl.ring_k * G * S;
   } else {
-    ring_base = reinterpret_cast<T*>(wbase + cuts_bytes + sc_bytes);
+    ring = reinterpret_cast<T*>(wbase + lay.ring_off);
   }
 
   const int g = lane >> sl.log2p2;
   const int d = lane & (p2 - 1);
-  const unsigned slot_mask = (p2 == 32) ? FULLMASK : (((1u << p2) - 1u) << (g * p2));
+  const bool dev_lane = d < p;
+  const int leader = g * p2;
+  const unsigned smask = (p2 == 32) ? FULLMASK : (((1u << p2) - 1u) << leader);
   int16_t* cuts = cuts_all + g * (S + 1);
-  Rings<T> R{ring_base, sl.ring_k, G * S, g * S};
+  const int KM = sl.ring_k - 1;
+  const int RS = G * S;             // ring row stride: [dir][slot][g*S + s]
+  const int BOFF = sl.ring_k * RS;  // start of the backward direction
+  const int tot = m * V;
+  const int wup =
+      dev_lane ? (V == 1 ? min(m, p - d - 1) : min(tot, 2 * (p - d - 1) + (V - 1) * p)) : 0;
+  const int nleft = leader + (d == 0 ? p - 1 : d - 1);  // neighbour devices (wrap)
+  const int nright = leader + (d + 1 >= p ? 0 : d + 1);
+#define REC(kind, c) recs[((kind) * V + (c)) * 32 + lane]
+#define DMEM(kind, c) dmem[((kind) * V + (c)) * 32 + lane]
 
-  unsigned long long wkey = ~0ull >> 1;  // running warp minimum (INT64_MAX)
-  unsigned long long winvalid = 0;
-  unsigned long long wtasks = 0;
-
-  for (;;) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(sl.cursor, (unsigned long long)G);
-    base = __shfl_sync(FULLMASK, base, 0);
-    if (base >= sl.n_pos) break;
-    const uint64_t pos = base + g;
-    const bool slot_on = pos < sl.n_pos;
-    const uint64_t idx = slot_on ? pos_to_index(sl, pos) : 0;
-
-    // ---- a1 decode (lane 0 of each slot)
-    bool valid = false;
-    if (slot_on && d == 0)
-      valid = decode_cuts(tab.binom, tab.ball, tab.seeds, sl.group, sl.part_mode, sl.radius, sl.S,
-                          sl.L, idx - sl.seg_base, cuts);
-    valid = __shfl_sync(FULLMASK, valid, g * p2);
-    __syncwarp();
-    const bool lane_on = slot_on && valid && d < p;
-
-    // ---- a2/a3 aggregation for this lane's stages
-    StageC<T> sc1{};  // V == 1 keeps the constants in registers
-    int64_t busy = 0, stat = 0;
-    T dmin = INF, cmin = INF;
-    if (lane_on) {
+  // ---- lane / slot state
+  bool active = false;  // slot simulates a candidate (uniform within the slot)
+  bool done = true;     // this lane has no task left
+  int flags = 0;        // slot-uniform F_* bits
+  uint64_t idx = 0;
+  T free_t = 0;
+  int64_t dyn = 0, peak = 0, busy = 0, stat = 0;
+  T window = INF;
+  // fixed orders
+  int nF = 0, nB = 0, nW = 0;
+  VPos fp, bp, wp;
+  fp.reset(); bp.reset(); wp.reset();
+  int tk = 2, tc = 0, tj = 0;  // cached next F/B task (tk: 0 F, 1 B, 2 none)
+  Rec<T> tr{};
+  // GREEDY per-chunk counters and F-gate bytes
+  int gF[V], gB[V], gW[V];
+  int64_t gA[V];
 #pragma unroll
-      for (int c = 0; c < V; ++c) {
-        const int s = stage_of(sl.placement, p, c, d);
-        const int a = cuts[s], b = cuts[s + 1];
-        StageC<T> x;
-        const int64_t cF = pre[kColTF * (L + 1) + b] - pre[kColTF * (L + 1) + a];
-        const int64_t cB = pre[kColTB * (L + 1) + b] - pre[kColTB * (L + 1) + a];
-        const int64_t cW = pre[kColTW * (L + 1) + b] - pre[kColTW * (L + 1) + a];
-        x.dF = (T)cF;
-        x.dB = (T)(FUSED ? cB + cW : cB);
-        x.dW = (T)cW;
-        x.act = pre[kColAct * (L + 1) + b] - pre[kColAct * (L + 1) + a];
-        x.stash = pre[kColStash * (L + 1) + b] - pre[kColStash * (L + 1) + a];
-        stat += pre[kColWG * (L + 1) + b] - pre[kColWG * (L + 1) + a];
-        busy += (int64_t)m * (cF + cB + cW);
-        x.oF = 0;
-        x.oB = 0;
-        if (s < S - 1 && dev_of(sl.placement, p, s + 1) != d) {
-          x.oF = (T)tab.comm[b - 1];
-          cmin = x.oF < cmin ? x.oF : cmin;
-        }
-        if (s > 0 && dev_of(sl.placement, p, s - 1) != d) {
-          x.oB = (T)tab.comm[a - 1];
-          cmin = x.oB < cmin ? x.oB : cmin;
-        }
-        T mn = (T)cF < (T)cB ? (T)cF : (T)cB;
-        mn = (T)cW < mn ? (T)cW : mn;
-        dmin = mn < dmin ? mn : dmin;
-        if constexpr (V == 1) sc1 = x; else scs[c * 32 + lane] = x;
-      }
-    }
-    __syncwarp();
-    auto SC = [&](int c) -> StageC<T> {
-      if constexpr (V == 1) { (void)c; return sc1; } else { return scs[c * 32 + lane]; }
-    };
+  for (int c = 0; c < V; ++c) { gF[c] = gB[c] = gW[c] = 0; gA[c] = 0; }
+  // queue (warp-uniform) and accumulators
+  uint64_t qpos = 0, qend = 0;
+  bool exhausted = false;
+  unsigned long long wkey = ~0ull >> 1, winvalid = 0, wtasks = 0;
 
-    // ---- ring reset (this warp's slots)
-    if constexpr (!FALLBACK) {
-      const int n = 2 * sl.ring_k * G * S;
-      for (int i = lane; i < n; i += 32) ring_base[i] = EMPTY;
-    } else {
-      const int n = 2 * sl.ring_k * G * S;
-      for (int i = lane; i < n; i += 32) ring_base[i] = EMPTY;
-    }
-    __syncwarp();
+  auto next_task = [&]() {
+    if (nF < tot && (POLICY == ADAPTIS_GPIPE || nF - nB <= wup)) { tk = 0; tc = fp.c; tj = fp.mb(); }
+    else if (nB < tot) { tk = 1; tc = V - 1 - bp.c; tj = bp.mb(); }
+    else { tk = 2; return; }
+    tr = REC(tk, tc);
+  };
 
-    // ---- state
-    const int tot = m * V;
-    int w = 0;  // warm-up (R9, R10)
-    if (V == 1) w = min(m, p - d - 1);
-    else w = min(tot, 2 * (p - d - 1) + (V - 1) * p);
-    T free_t = 0;
-    int64_t dyn = 0, peak = 0;
-    bool done = !lane_on;
-    bool over = false;
-    int status = 0;  // slot status, decided below
-
-    // ---- a4: fused fixed orders: exact peak from the order alone (R16)
-    if constexpr (FUSED) {
-      if (lane_on) {
-        if constexpr (POLICY == ADAPTIS_GPIPE) {
-          int64_t sum = 0;
-#pragma unroll
-          for (int c = 0; c < V; ++c) { StageC<T> x = SC(c); sum += x.act + x.stash; }
-          peak = sum * m;
-        } else if constexpr (V == 1) {
-          peak = (int64_t)min(m, w + 1) * (sc1.act + sc1.stash);
-        } else {
-          VPos fp, bp;
-          fp.reset(); bp.reset();
-          int nF = 0, nB = 0;
-          int64_t dd = 0;
-          while (nF < tot || nB < tot) {
-            const bool isF = nF < tot && nF - nB <= w;
-            if (isF) {
-              StageC<T> x = SC(fp.c);
-              dd += x.act + x.stash;
-              peak = dd > peak ? dd : peak;
-              fp.next(p, V); ++nF;
-            } else {
-              StageC<T> x = SC(V - 1 - bp.c);
-              dd -= x.act + x.stash;
-              bp.next(p, V); ++nB;
-            }
-          }
-        }
-        over = stat + peak > sl.cap;
-      }
-    }
-    const bool pre_over = FUSED && (__ballot_sync(FULLMASK, over) & slot_mask);
-    if (pre_over) done = true;  // fused fixed order infeasible by Eq. 2: no simulation
-
-    // GREEDY window (Lemma 3): every unscheduled task starts at >= t* and no new
-    // cross-device arrival can precede t* + dmin + cmin.
-    T window = INF;
-    if constexpr (POLICY == ADAPTIS_GREEDY) {
-      const T dm = seg_min(dmin, p2);
-      const T cm = seg_min(cmin, p2);
-      window = (cm == INF) ? INF : dm + cm;
-    }
-
-    // ---- a5: simulation rounds
-    int nF = 0, nB = 0, nW = 0;          // fixed orders: device-level counters
-    VPos fp, bp, wp;
-    fp.reset(); bp.reset(); wp.reset();
-    int gF[V], gB[V], gW[V];             // GREEDY: per-chunk counters
-#pragma unroll
-    for (int c = 0; c < V; ++c) { gF[c] = 0; gB[c] = 0; gW[c] = 0; }
-    bool slot_live = slot_on && valid && !pre_over;
-    bool overflow = false;
-    bool stuck = false;
-
-    while (__any_sync(FULLMASK, slot_live)) {
-      bool go = false, blocked = false;
-      // action record
-      int act_kind = -1, act_c = 0, act_j = 0, act_s = 0;
-      T act_start = 0, r_in = 0;
-      bool has_out = false, need_in = false;
-      T tstar = INF;
-
-      if constexpr (POLICY == ADAPTIS_GREEDY) {
-        T at = INF;
-        if (slot_live && !done) {
-          T rFc[V], rBc[V];
-          bool cF[V], cB[V], cW[V];
-          T rmin = INF;
-#pragma unroll
-          for (int c = 0; c < V; ++c) {
-            const int s = stage_of(sl.placement, p, c, d);
-            StageC<T> x = SC(c);
-            cF[c] = false; cB[c] = false; cW[c] = gW[c] < gB[c];
-            rFc[c] = 0; rBc[c] = 0;
-            if (gF[c] < m && stat + dyn + x.act + x.stash <= sl.cap) {
-              T r = (s == 0) ? (T)0 : *R.at(0, gF[c], s);
-              if (r >= 0) { cF[c] = true; rFc[c] = r; rmin = r < rmin ? r : rmin; }
-            }
-            if (gB[c] < gF[c]) {
-              T r = (s == S - 1) ? (T)0 : *R.at(1, gB[c], s);
-              if (r >= 0) { cB[c] = true; rBc[c] = r; rmin = r < rmin ? r : rmin; }
-            }
-            if (cW[c]) rmin = 0 < rmin ? 0 : rmin;
-          }
-          if (rmin != INF) {
-            at = free_t > rmin ? free_t : rmin;
-            // key (kind F < B < W, mb, stage); stage order == chunk order
-            int bj = INT_MAX;
-#pragma unroll
-            for (int c = 0; c < V; ++c)
-              if (cF[c] && rFc[c] <= at && gF[c] < bj) { bj = gF[c]; act_kind = 0; act_c = c; }
-            if (act_kind < 0) {
-#pragma unroll
-              for (int c = 0; c < V; ++c)
-                if (cB[c] && rBc[c] <= at && gB[c] < bj) { bj = gB[c]; act_kind = 1; act_c = c; }
-            }
-            if (act_kind < 0) {
-#pragma unroll
-              for (int c = 0; c < V; ++c)
-                if (cW[c] && gW[c] < bj) { bj = gW[c]; act_kind = 2; act_c = c; }
-            }
-            act_j = bj;
-          }
-        }
-        tstar = seg_min(at, p2);
-        if (act_kind >= 0 && at - tstar < window) {
-          act_s = stage_of(sl.placement, p, act_c, d);
-          act_start = at;
-          if (act_kind == 0) { need_in = act_s > 0; has_out = act_s < S - 1; }
-          else if (act_kind == 1) { need_in = act_s < S - 1; has_out = act_s > 0; }
-          bool out_ok = true;
-          if (has_out)
-            out_ok = *R.at(act_kind, act_j, act_kind == 0 ? act_s + 1 : act_s - 1) == EMPTY;
-          go = out_ok;
-          blocked = !out_ok;
-        }
-      } else {
-        // fixed F/B lists (+ ZB's W fill)
-        if (slot_live && !done) {
-          const bool x_exists = nF < tot || nB < tot;
-          const bool hasW = (POLICY == ADAPTIS_ZB) && nW < nB;
-          bool doW = false;
-          if (x_exists) {
-            const bool isF = nF < tot && (POLICY == ADAPTIS_GPIPE || nF - nB <= w);
-            const int c = isF ? fp.c : V - 1 - bp.c;
-            const int j = isF ? fp.mb(p) : bp.mb(p);
-            const int s = stage_of(sl.placement, p, c, d);
-            StageC<T> x = SC(c);
-            bool forced = false;
-            if constexpr (POLICY == ADAPTIS_ZB)
-              forced = isF && hasW && stat + dyn + x.act + x.stash > sl.cap;
-            if (forced) {
-              doW = true;
-            } else {
-              need_in = isF ? (s > 0) : (s < S - 1);
-              T r = need_in ? *R.at(isF ? 0 : 1, j, s) : (T)0;
-              if (r >= 0) {
-                if (hasW && free_t < r) {
-                  doW = true;  // R13 (ii): fill the bubble before r with the oldest W
-                } else {
-                  act_kind = isF ? 0 : 1; act_c = c; act_j = j; act_s = s; r_in = r;
-                  act_start = free_t > r ? free_t : r;
-                  has_out = isF ? (s < S - 1) : (s > 0);
-                  bool out_ok = true;
-                  if (has_out) out_ok = *R.at(act_kind, j, isF ? s + 1 : s - 1) == EMPTY;
-                  go = out_ok;
-                  blocked = !out_ok;
-                }
-              }
-            }
-          } else if (hasW) {
-            doW = true;
-          }
-          if (doW) {
-            act_kind = 2; act_c = V - 1 - wp.c; act_j = wp.mb(p);
-            act_s = stage_of(sl.placement, p, act_c, d);
-            act_start = free_t; need_in = false; has_out = false; go = true;
-          }
-        }
-      }
-      __syncwarp();
-      // ---- execute (write phase)
-      if (go) {
-        ++wtasks;
-        StageC<T> x = SC(act_c);
-        const T dur = act_kind == 0 ? x.dF : (act_kind == 1 ? x.dB : x.dW);
-        const T fin = act_start + dur;
-        free_t = fin;
-        if (act_kind == 0) {
-          dyn += x.act + x.stash;
-          peak = dyn > peak ? dyn : peak;
-          if (has_out) *R.at(0, act_j, act_s + 1) = fin + x.oF;
-          if (need_in) *R.at(0, act_j, act_s) = EMPTY;
-          if constexpr (POLICY == ADAPTIS_GREEDY) {
-#pragma unroll
-            for (int c = 0; c < V; ++c) gF[c] += (c == act_c);
-          } else {
-            ++nF; fp.next(p, V);
-          }
-          if constexpr (POLICY == ADAPTIS_ZB)
-            if (sl.key && stat + dyn > sl.cap) over = true;  // search: Eq. 2 already violated
-        } else if (act_kind == 1) {
-          dyn -= x.act + (FUSED ? x.stash : 0);
-          if (has_out) *R.at(1, act_j, act_s - 1) = fin + x.oB;
-          if (need_in) *R.at(1, act_j, act_s) = EMPTY;
-          if constexpr (POLICY == ADAPTIS_GREEDY) {
-#pragma unroll
-            for (int c = 0; c < V; ++c) gB[c] += (c == act_c);
-          } else {
-            ++nB; bp.next(p, V);
-          }
-        } else {
-          dyn -= x.stash;
-          if constexpr (POLICY == ADAPTIS_GREEDY) {
-#pragma unroll
-            for (int c = 0; c < V; ++c) gW[c] += (c == act_c);
-          } else {
-            ++nW; wp.next(p, V);
-          }
-        }
-        // lane completion
-        if constexpr (POLICY == ADAPTIS_GREEDY) {
-          bool all = true;
-#pragma unroll
-          for (int c = 0; c < V; ++c) all = all && gF[c] == m && gB[c] == m && gW[c] == m;
-          done = all;
-        } else if constexpr (POLICY == ADAPTIS_ZB) {
-          done = nF == tot && nB == tot && nW == tot;
-        } else {
-          done = nF == tot && nB == tot;
-        }
-      }
-      (void)r_in;
-      __syncwarp();
-      // ---- progress bookkeeping per slot
-      const unsigned go_m = __ballot_sync(FULLMASK, go);
-      const unsigned blk_m = __ballot_sync(FULLMASK, blocked);
-      const unsigned done_m = __ballot_sync(FULLMASK, done || !(d < p));
-      const unsigned over_m = __ballot_sync(FULLMASK, over);
-      if (slot_live) {
-        if ((done_m & slot_mask) == slot_mask) {
-          slot_live = false;
-        } else if (over_m & slot_mask) {
-          slot_live = false;  // search mode ZB: already over the cap
-        } else if (!(go_m & slot_mask)) {
-          slot_live = false;
-          if (blk_m & slot_mask) overflow = true; else stuck = true;
-        }
-      }
-    }
-
-    // ---- a6 metrics (all lanes participate in the shuffles)
-    const bool contrib = slot_on && valid && d < p;
+  // collective: write results of the slots with `fl` set (all lanes execute)
+  auto finalize = [&](bool fl) {
+    const bool contrib = fl && dev_lane;
     const int64_t mk = seg_max(contrib ? (int64_t)free_t : (int64_t)0, p2);
-    const int64_t sumbusy = seg_sum(contrib ? busy : (int64_t)0, p2);
+    const int64_t sb = seg_sum(contrib ? busy : (int64_t)0, p2);
     const int64_t Md = stat + peak;
     const int64_t Mmax = seg_max(contrib ? Md : (int64_t)0, p2);
-    const bool any_over = (__ballot_sync(FULLMASK, contrib && Md > sl.cap) & slot_mask) != 0;
-    if (!slot_on) status = -1;
-    else if (!valid) status = ADAPTIS_CAND_INVALID;
-    else if (overflow) status = -2;  // re-evaluated by the fallback kernel
-    else if (FUSED && any_over) status = ADAPTIS_CAND_OVER_CAP;
-    else if (stuck) status = ADAPTIS_CAND_STUCK;
-    else if (any_over) status = ADAPTIS_CAND_OVER_CAP;
+    const bool anyover = (__ballot_sync(FULLMASK, contrib && Md > sl.cap) & smask) != 0;
+    int status;
+    if (flags & F_INVALID) status = ADAPTIS_CAND_INVALID;
+    else if (flags & F_OVERFLOW) status = -2;
+    else if (FUSED && ((flags & F_PREOVER) || anyover)) status = ADAPTIS_CAND_OVER_CAP;
+    else if (flags & F_STUCK) status = ADAPTIS_CAND_STUCK;
+    else if (anyover) status = ADAPTIS_CAND_OVER_CAP;
     else status = ADAPTIS_CAND_OK;
-
-    if (d == 0 && slot_on) {
+    if (fl && d == 0) {
       if (status == -2) {
-        unsigned int k = atomicAdd(sl.overflow_count, 1u);
+        const unsigned k = atomicAdd(sl.overflow_count, 1u);
         if (k < sl.overflow_cap) sl.overflow_idx[k] = idx;
       } else {
         if (status == ADAPTIS_CAND_INVALID) ++winvalid;
         if (sl.key) {
           if (status == ADAPTIS_CAND_OK) {
-            unsigned long long key = ((unsigned long long)mk << sl.key_bits) | idx;
+            const unsigned long long key = ((unsigned long long)mk << sl.key_bits) | idx;
             wkey = key < wkey ? key : wkey;
           }
         } else {
@@ -502,8 +257,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           if (sl.out_peak)
             sl.out_peak[o] = (status == 0 || status == ADAPTIS_CAND_OVER_CAP) ? Mmax : 0;
           if (sl.out_bubble)
-            sl.out_bubble[o] = status == 0
-                ? (float)(1.0 - (double)sumbusy / ((double)p * (double)mk)) : 0.0f;
+            sl.out_bubble[o] =
+                status == 0 ? (float)(1.0 - (double)sb / ((double)p * (double)mk)) : 0.0f;
         }
       }
     }
@@ -512,34 +267,335 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       sl.out_report[p + d] = busy;
       sl.out_report[2 * p + d] = Md;
     }
-    __syncwarp();
-  }
+  };
 
-  // ---- a7 argmin: warp min -> one atomicMin per warp
-  if (sl.key) {
-    for (int o = 16; o > 0; o >>= 1) {
-      unsigned long long x = __shfl_xor_sync(FULLMASK, wkey, o);
-      wkey = x < wkey ? x : wkey;
+  for (;;) {
+    // ================= maintenance: finalize finished slots, refill idle ones
+    {
+      const unsigned live_m = __ballot_sync(FULLMASK, active && !done);
+      const bool fin = active && !(live_m & smask);
+      const unsigned fin_m = __ballot_sync(FULLMASK, fin);
+      if (fin_m) {
+        finalize(fin);
+        if (fin) active = false;
+      }
+      const unsigned idle_m = __ballot_sync(FULLMASK, !active);
+      if (idle_m && !exhausted) {
+        for (int it = 0; it < 4; ++it) {
+          const unsigned want_m = __ballot_sync(FULLMASK, !active && d == 0);
+          if (want_m == 0) break;
+          if (qpos >= qend) {
+            unsigned long long b = 0;
+            if (lane == 0) b = atomicAdd(sl.cursor, (unsigned long long)kQueueBlock);
+            b = __shfl_sync(FULLMASK, b, 0);
+            if (b >= sl.n_pos) { exhausted = true; break; }
+            qpos = b;
+            qend = b + kQueueBlock < sl.n_pos ? b + kQueueBlock : sl.n_pos;
+          }
+          const unsigned nw = __popc(want_m);
+          const unsigned rank = __popc(want_m & ((1u << leader) - 1u));
+          const uint64_t avail = qend - qpos;
+          const bool take = !active && (uint64_t)rank < avail;
+          const uint64_t mypos = qpos + rank;
+          qpos += (uint64_t)nw < avail ? (uint64_t)nw : avail;
+
+          // ---- a1 decode
+          bool valid = false;
+          if (take) idx = pos_to_index(sl, mypos);
+          if (take && d == 0)
+            valid = decode_cuts(tab.binom, tab.ball, tab.seeds, sl.group, sl.part_mode, sl.radius,
+                                S, L, idx - sl.seg_base, cuts);
+          valid = __shfl_sync(FULLMASK, valid, leader);
+          __syncwarp();
+          const bool lane_on = take && valid && dev_lane;
+          if (take) {
+            flags = valid ? 0 : F_INVALID;
+            free_t = 0; dyn = 0; peak = 0; busy = 0; stat = 0;
+          }
+          // ---- a2/a3 aggregation into task records
+          T dmin = INF, cmin = INF;
+          int64_t ac[V];
+#pragma unroll
+          for (int c = 0; c < V; ++c) ac[c] = 0;
+          if (lane_on) {
+#pragma unroll
+            for (int c = 0; c < V; ++c) {
+              const int s = stage_of(sl.placement, p, c, d);
+              const int a = cuts[s], b = cuts[s + 1];
+              const int64_t cF = pre[kColTF * (L + 1) + b] - pre[kColTF * (L + 1) + a];
+              const int64_t cB = pre[kColTB * (L + 1) + b] - pre[kColTB * (L + 1) + a];
+              const int64_t cW = pre[kColTW * (L + 1) + b] - pre[kColTW * (L + 1) + a];
+              const int64_t act = pre[kColAct * (L + 1) + b] - pre[kColAct * (L + 1) + a];
+              const int64_t sta = pre[kColStash * (L + 1) + b] - pre[kColStash * (L + 1) + a];
+              stat += pre[kColWG * (L + 1) + b] - pre[kColWG * (L + 1) + a];
+              busy += (int64_t)m * (cF + cB + cW);
+              T oF = 0, oB = 0;
+              if (s < S - 1 && dev_of(sl.placement, p, s + 1) != d) {
+                oF = (T)tab.comm[b - 1];
+                cmin = oF < cmin ? oF : cmin;
+              }
+              if (s > 0 && dev_of(sl.placement, p, s - 1) != d) {
+                oB = (T)tab.comm[a - 1];
+                cmin = oB < cmin ? oB : cmin;
+              }
+              T mn = (T)cF < (T)cB ? (T)cF : (T)cB;
+              mn = (T)cW < mn ? (T)cW : mn;
+              dmin = mn < dmin ? mn : dmin;
+              const int row = g * S + s;
+              Rec<T> rf, rb, rw;
+              rf.dur = (T)cF; rf.oc = oF;
+              rf.in_off = s > 0 ? row : -1;
+              rf.out_off = s < S - 1 ? row + 1 : -1;
+              rb.dur = (T)(FUSED ? cB + cW : cB); rb.oc = oB;
+              rb.in_off = s < S - 1 ? BOFF + row : -1;
+              rb.out_off = s > 0 ? BOFF + row - 1 : -1;
+              rw.dur = (T)cW; rw.oc = 0; rw.in_off = -1; rw.out_off = -1;
+              REC(0, c) = rf;
+              REC(1, c) = rb;
+              REC(2, c) = rw;
+              if constexpr (!FUSED) {
+                DMEM(0, c) = act + sta;
+                DMEM(1, c) = -act;
+                DMEM(2, c) = -sta;
+              }
+              ac[c] = act + sta;
+            }
+          }
+          // ---- a4 memory precheck of the fused fixed orders (R16)
+          if constexpr (FUSED) {
+            if (lane_on) {
+              if constexpr (POLICY == ADAPTIS_GPIPE) {
+                int64_t A = 0;
+#pragma unroll
+                for (int c = 0; c < V; ++c) A += ac[c];
+                peak = A * m;
+              } else {
+                peak = megatron_peak<V>(ac, p, m, wup);
+              }
+            }
+            const bool ov = lane_on && stat + peak > sl.cap;
+            const unsigned ov_m = __ballot_sync(FULLMASK, ov);
+            if (take && valid && (ov_m & smask)) flags |= F_PREOVER;
+          }
+          if constexpr (GREEDY) {
+            const T dm = seg_min(dmin, p2), cm = seg_min(cmin, p2);
+            if (take) {
+              window = (cm == INF) ? INF : dm + cm;
+#pragma unroll
+              for (int c = 0; c < V; ++c) gA[c] = ac[c];
+            }
+          }
+          // ---- ring reset for the slots being set up
+          if (take && dev_lane) {
+            for (int s = d; s < S; s += p)
+              for (int k = 0; k < 2 * sl.ring_k; ++k) ring[(size_t)k * RS + g * S + s] = EMPTY;
+          }
+          __syncwarp();
+          const bool survivor = take && valid && !(flags & F_PREOVER);
+          const unsigned nonsurv_m = __ballot_sync(FULLMASK, take && !survivor);
+          if (nonsurv_m) finalize(take && !survivor);
+          if (survivor) {
+            active = true;
+            done = !dev_lane;
+            nF = nB = nW = 0;
+            fp.reset(); bp.reset(); wp.reset();
+#pragma unroll
+            for (int c = 0; c < V; ++c) { gF[c] = gB[c] = gW[c] = 0; }
+            if constexpr (!GREEDY) { if (dev_lane) next_task(); }
+          }
+          __syncwarp();
+        }
+      }
+      if (__ballot_sync(FULLMASK, active) == 0) {
+        if (exhausted) break;
+        continue;
+      }
     }
-    if (lane == 0 && wkey != (~0ull >> 1)) atomicMin(sl.key, wkey);
+
+    // ================= a5: one simulation round
+    bool progressed = false, blocked = false;
+    const bool live = active && !done;
+    if constexpr (!GREEDY) {
+      T r = 0;
+      int iaddr = -1, oaddr = -1;
+      bool ofree = true;
+      if (live && tk < 2) {  // phase A: read the input arrival and the output slot
+        iaddr = tr.in_off >= 0 ? tr.in_off + (tj & KM) * RS : -1;
+        oaddr = tr.out_off >= 0 ? tr.out_off + (tj & KM) * RS : -1;
+        r = iaddr >= 0 ? ring[iaddr] : (T)0;
+        ofree = oaddr < 0 || ring[oaddr] == EMPTY;
+      }
+      __syncwarp();
+      if (live) {  // phase B: execute
+        if constexpr (ZB) {
+          // R13: (i) memory-forced W before an F that does not fit, (ii) W fill while free < r
+          for (;;) {
+            if (nW >= nB) break;
+            bool runW;
+            if (tk == 2) runW = true;
+            else if (tk == 0 && stat + dyn + DMEM(0, tc) > sl.cap) runW = true;
+            else runW = r >= 0 && free_t < r;
+            if (!runW) break;
+            const int c = V - 1 - wp.c;
+            free_t += REC(2, c).dur;
+            dyn += DMEM(2, c);
+            ++nW; wp.next(p, V); ++wtasks;
+            progressed = true;
+          }
+        }
+        bool xgo = tk < 2 && r >= 0;
+        if constexpr (ZB) xgo = xgo && (nW >= nB || free_t >= r);
+        if (xgo && !ofree) { blocked = true; xgo = false; }
+        if (xgo) {
+          const T fin = (free_t > r ? free_t : r) + tr.dur;
+          free_t = fin;
+          if (oaddr >= 0) ring[oaddr] = fin + tr.oc;
+          if (iaddr >= 0) ring[iaddr] = EMPTY;
+          if constexpr (ZB) {
+            dyn += DMEM(tk, tc);
+            if (tk == 0) {
+              peak = dyn > peak ? dyn : peak;
+              if (sl.key && stat + dyn > sl.cap) done = true;  // search: Eq. 2 already violated
+            }
+          }
+          if (tk == 0) { ++nF; fp.next(p, V); } else { ++nB; bp.next(p, V); }
+          ++wtasks;
+          progressed = true;
+          next_task();
+        }
+        if (tk == 2 && (!ZB || nW == tot)) done = true;
+      }
+    } else {
+      // ---- GREEDY (R14) in bounded-lag rounds (Lemma 3 with neighbour bounds)
+      T at = INF;
+      int ak = -1, acx = 0, aj = 0;
+      if (live) {
+        T rF[V], rB[V];
+        bool cFv[V], cBv[V], cWv[V];
+        T rmin = INF;
+#pragma unroll
+        for (int c = 0; c < V; ++c) {
+          const int s = stage_of(sl.placement, p, c, d);
+          const int row = g * S + s;
+          cFv[c] = false; cBv[c] = false; cWv[c] = gW[c] < gB[c];
+          rF[c] = 0; rB[c] = 0;
+          if (gF[c] < m && stat + dyn + gA[c] <= sl.cap) {
+            const T r = s > 0 ? ring[row + (gF[c] & KM) * RS] : (T)0;
+            if (r >= 0) { cFv[c] = true; rF[c] = r; rmin = r < rmin ? r : rmin; }
+          }
+          if (gB[c] < gF[c]) {
+            const T r = s < S - 1 ? ring[BOFF + row + (gB[c] & KM) * RS] : (T)0;
+            if (r >= 0) { cBv[c] = true; rB[c] = r; rmin = r < rmin ? r : rmin; }
+          }
+          if (cWv[c]) rmin = 0;
+        }
+        if (rmin != INF) {
+          at = free_t > rmin ? free_t : rmin;
+          int bj = INT_MAX;  // key (kind F < B < W, mb, stage); stage order == chunk order
+#pragma unroll
+          for (int c = 0; c < V; ++c)
+            if (cFv[c] && rF[c] <= at && gF[c] < bj) { bj = gF[c]; ak = 0; acx = c; }
+          if (ak < 0) {
+#pragma unroll
+            for (int c = 0; c < V; ++c)
+              if (cBv[c] && rB[c] <= at && gB[c] < bj) { bj = gB[c]; ak = 1; acx = c; }
+          }
+          if (ak < 0) {
+#pragma unroll
+            for (int c = 0; c < V; ++c)
+              if (cWv[c] && gW[c] < bj) { bj = gW[c]; ak = 2; acx = c; }
+          }
+          aj = bj;
+        }
+      }
+      // Every unscheduled task starts at >= t*; a neighbour n starts its next task
+      // at >= min(at_n, t* + window); so no new arrival reaches this lane before
+      // `bound` and its decision at `at` < bound is final.
+      const T tstar = seg_min(at, p2);
+      const T atl = __shfl_sync(FULLMASK, at, nleft);
+      const T atr = __shfl_sync(FULLMASK, at, nright);
+      T lim = atl < atr ? atl : atr;
+      const T tw = sat_add(tstar, window);
+      lim = lim < tw ? lim : tw;
+      const T bound = sat_add(lim, window);
+      int oaddr = -1, iaddr = -1;
+      bool go = false;
+      if (ak >= 0 && at < bound) {
+        const int s = stage_of(sl.placement, p, acx, d);
+        const int row = g * S + s;
+        if (ak == 0) {
+          iaddr = s > 0 ? row + (aj & KM) * RS : -1;
+          oaddr = s < S - 1 ? row + 1 + (aj & KM) * RS : -1;
+        } else if (ak == 1) {
+          iaddr = s < S - 1 ? BOFF + row + (aj & KM) * RS : -1;
+          oaddr = s > 0 ? BOFF + row - 1 + (aj & KM) * RS : -1;
+        }
+        const bool ofree = oaddr < 0 || ring[oaddr] == EMPTY;
+        go = ofree;
+        blocked = !ofree;
+      }
+      __syncwarp();
+      if (go) {
+        const Rec<T> rc = REC(ak, acx);
+        const T fin = at + rc.dur;
+        free_t = fin;
+        if (oaddr >= 0) ring[oaddr] = fin + rc.oc;
+        if (iaddr >= 0) ring[iaddr] = EMPTY;
+        dyn += DMEM(ak, acx);
+        if (ak == 0) peak = dyn > peak ? dyn : peak;
+#pragma unroll
+        for (int c = 0; c < V; ++c) {
+          gF[c] += (ak == 0 && c == acx);
+          gB[c] += (ak == 1 && c == acx);
+          gW[c] += (ak == 2 && c == acx);
+        }
+        bool all = true;
+#pragma unroll
+        for (int c = 0; c < V; ++c) all = all && gW[c] == m;
+        done = all;
+        ++wtasks;
+        progressed = true;
+      }
+    }
+    __syncwarp();
+    // ---- deadlock detection per slot (rare): no lane of a live slot progressed
+    {
+      const unsigned prog_m = __ballot_sync(FULLMASK, progressed);
+      const unsigned live_m = __ballot_sync(FULLMASK, active && !done);
+      const unsigned blk_m = __ballot_sync(FULLMASK, blocked);
+      if (active && (live_m & smask) && !(prog_m & smask)) {
+        flags |= (blk_m & smask) ? F_OVERFLOW : F_STUCK;
+        done = true;
+      }
+    }
   }
+#undef REC
+#undef DMEM
+
+  // ---- a7 argmin: warp min -> one atomicMin per warp; counters
   for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(FULLMASK, wkey, o);
+    wkey = x < wkey ? x : wkey;
     winvalid += __shfl_xor_sync(FULLMASK, winvalid, o);
     wtasks += __shfl_xor_sync(FULLMASK, wtasks, o);
   }
-  if (lane == 0 && winvalid) atomicAdd(sl.n_invalid, winvalid);
-  if (lane == 0 && wtasks) atomicAdd(sl.n_tasks, wtasks);
+  if (lane == 0) {
+    if (sl.key && wkey != (~0ull >> 1)) atomicMin(sl.key, wkey);
+    if (winvalid) atomicAdd(sl.n_invalid, winvalid);
+    if (wtasks) atomicAdd(sl.n_tasks, wtasks);
+  }
 }
 
 // ------------------------------------------------------------------------------
+static WarpLayout host_layout(const SegLaunch& s, bool gring) {
+  const int tsz = s.use_int64 ? 8 : 4;
+  const int rsz = s.use_int64 ? (int)sizeof(Rec<int64_t>) : (int)sizeof(Rec<int32_t>);
+  return warp_layout(s.S, s.G, s.v, s.ring_k, tsz, rsz, gring);
+}
+
 size_t smem_bytes(const SegLaunch& s, bool fallback) {
-  const size_t tsz = s.use_int64 ? 8 : 4;
-  const size_t pre = ((size_t)kNumCols * (s.L + 1) * 8 + 15) & ~(size_t)15;
-  const size_t cuts = (((size_t)s.G * (s.S + 1) * 2) + 15) & ~(size_t)15;
-  const size_t scsz = s.use_int64 ? sizeof(StageC<int64_t>) : sizeof(StageC<int32_t>);
-  const size_t sc = (size_t)(s.v > 1 ? s.v : 0) * 32 * scsz;
-  const size_t ring = fallback ? 0 : (size_t)2 * s.ring_k * s.G * s.S * tsz;
-  return pre + kWarpsPerCta * (cuts + sc + ring);
+  const WarpLayout l = host_layout(s, fallback);
+  return l.prefix_bytes(s.L) + (size_t)kWarpsPerCta * l.per_warp;
 }
 
 using KFn = void (*)(const DevTables, const SegLaunch);
@@ -572,7 +628,7 @@ static KFn pick(const SegLaunch& s, bool fb) {
 
 int occupancy_ctas_per_sm(const SegLaunch& s, bool fallback) {
   KFn f = pick(s, fallback);
-  size_t sm = smem_bytes(s, fallback);
+  const size_t sm = smem_bytes(s, fallback);
   if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return 0;
   int n = 0;
@@ -584,7 +640,7 @@ int occupancy_ctas_per_sm(const SegLaunch& s, bool fallback) {
 int launch_segment(const DevTables& t, const SegLaunch& s, int num_sms, void* stream,
                    bool fallback, unsigned grid_limit) {
   KFn f = pick(s, fallback);
-  size_t sm = smem_bytes(s, fallback);
+  const size_t sm = smem_bytes(s, fallback);
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return (int)e;
   int per_sm = 0;
@@ -592,14 +648,12 @@ int launch_segment(const DevTables& t, const SegLaunch& s, int num_sms, void* st
   if (e != cudaSuccess) return (int)e;
   if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
   unsigned grid = (unsigned)num_sms * (unsigned)per_sm;
-  // no more CTAs than there is work for
   const uint64_t warps_needed = (s.n_pos + s.G - 1) / s.G;
   const uint64_t ctas_needed = (warps_needed + kWarpsPerCta - 1) / kWarpsPerCta;
   if (ctas_needed < grid) grid = (unsigned)(ctas_needed ? ctas_needed : 1);
   if (grid_limit && grid > grid_limit) grid = grid_limit;
   f<<<grid, kWarpsPerCta * 32, sm, (cudaStream_t)stream>>>(t, s);
-  e = cudaGetLastError();
-  return (int)e;
+  return (int)cudaGetLastError();
 }
 
 }  // namespace adaptis
