@@ -180,6 +180,22 @@ ADAPTIS_API uint64_t       adaptis_ctx_launch_count(const adaptis_ctx* ctx);
 /* Candidates re-evaluated by the exact fallback kernel (shared-memory rings
  * too small for their dependency lag) since creation. */
 ADAPTIS_API uint64_t       adaptis_ctx_fallback_count(const adaptis_ctx* ctx);
+/* Per-launch record of the most recent evaluation (search or eval) of a
+ * context: one entry per (group, combo) segment launched. */
+typedef struct {
+  int32_t group, combo, v, placement, policy;
+  int32_t fallback;          /* candidates re-run by the fallback kernel            */
+  uint64_t candidates;       /* candidates this launch evaluated                    */
+  uint64_t tasks;            /* F/B/W tasks it simulated                             */
+  float ms;                  /* device time of the launch (+ its fallback), CUDA events */
+} adaptis_launch_info;
+/* Copies up to `max` records of the last evaluation into `out`; returns how
+ * many there are. The winner re-evaluation of a search is not included. */
+ADAPTIS_API int            adaptis_ctx_launch_info(const adaptis_ctx* ctx, adaptis_launch_info* out, int max);
+/* Cumulative work counters of this context since creation: out[0] simulated
+ * tasks, out[1] warp simulation rounds, out[2] live device-lane rounds (lane
+ * utilisation = out[0] / out[2]; tasks per warp-round = out[0] / out[1]). */
+ADAPTIS_API void           adaptis_ctx_counters(const adaptis_ctx* ctx, uint64_t out[3]);
 
 /* |space| for this problem (the candidate space). EINVAL on an
  * invalid problem/space; EOVERFLOW if the count does not fit in 63 bits. */
@@ -217,6 +233,15 @@ ADAPTIS_API adaptis_status adaptis_search(adaptis_ctx* ctx, const adaptis_proble
                               const adaptis_space* space, adaptis_best* out);
 ADAPTIS_API adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* prep,
                                        adaptis_best* out);
+
+/* The candidates rank `rank` of `world` evaluates in a sharded search
+ * (block-cyclic chunks of 65536 global indices, chunk k -> rank k mod world,
+ * within every (group, combo) segment), in the order the kernels visit them.
+ * Writes up to `cap` indices to `out` (may be NULL) and their total count to
+ * *n_out. Host-only; used to check that the shards partition [0, |space|). */
+ADAPTIS_API adaptis_status adaptis_shard_indices(const adaptis_problem* problem,
+                                                 const adaptis_space* space, int rank, int world,
+                                                 uint64_t* out, uint64_t cap, uint64_t* n_out);
 
 /* Message of the last failure on `ctx` (or of the calling thread when ctx is NULL). */
 ADAPTIS_API const char*    adaptis_last_error(const adaptis_ctx* ctx);

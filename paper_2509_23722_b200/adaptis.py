@@ -77,6 +77,12 @@ class _Best(C.Structure):
                 ("kernel_ms", C.c_float)]
 
 
+class _LaunchInfo(C.Structure):
+    _fields_ = [("group", C.c_int32), ("combo", C.c_int32), ("v", C.c_int32),
+                ("placement", C.c_int32), ("policy", C.c_int32), ("fallback", C.c_int32),
+                ("candidates", C.c_uint64), ("tasks", C.c_uint64), ("ms", C.c_float)]
+
+
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
 
 _lock = threading.Lock()
@@ -111,6 +117,9 @@ def lib():
             L.adaptis_ctx_launch_count.argtypes = [C.c_void_p]
             L.adaptis_ctx_fallback_count.restype = C.c_uint64
             L.adaptis_ctx_fallback_count.argtypes = [C.c_void_p]
+            L.adaptis_ctx_counters.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+            L.adaptis_ctx_launch_info.restype = C.c_int
+            L.adaptis_ctx_launch_info.argtypes = [C.c_void_p, C.POINTER(_LaunchInfo), C.c_int]
             L.adaptis_space_size.restype = st
             L.adaptis_space_size.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.POINTER(C.c_uint64)]
             L.adaptis_decode.restype = st
@@ -125,6 +134,9 @@ def lib():
             L.adaptis_eval_prepared.restype = st
             L.adaptis_eval_prepared.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
                                                 C.POINTER(_ResultsSoa), C.c_int]
+            L.adaptis_shard_indices.restype = st
+            L.adaptis_shard_indices.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.c_int, C.c_int,
+                                                C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(C.c_uint64)]
             L.adaptis_search.restype = st
             L.adaptis_search.argtypes = [C.c_void_p, C.POINTER(_Problem), C.POINTER(_Space), C.POINTER(_Best)]
             L.adaptis_search_prepared.restype = st
@@ -192,6 +204,24 @@ def decode(pr: W.Problem, sp: W.Space, index: int) -> dict:
     return plan_dict(pl)
 
 
+def shard_indices(pr: W.Problem, sp: W.Space, rank: int, world: int) -> np.ndarray:
+    """Global indices rank `rank` evaluates in a `world`-way sharded search (host-only)."""
+    m = _Marshal(pr, sp)
+    n = C.c_uint64()
+    _check(lib().adaptis_shard_indices(C.byref(m.problem), C.byref(m.space), rank, world, None, 0,
+                                       C.byref(n)))
+    out = np.zeros(n.value, np.uint64)
+    _check(lib().adaptis_shard_indices(C.byref(m.problem), C.byref(m.space), rank, world,
+                                       out.ctypes.data_as(C.POINTER(C.c_uint64)), n.value, C.byref(n)))
+    return out
+
+
+def pack_key(makespan: int, index: int, n_candidates: int) -> int:
+    """The packed argmin key of the search (makespan << bits | index)."""
+    bits = max(1, (n_candidates - 1).bit_length())
+    return (makespan << bits) | index
+
+
 class Context:
     """One adaptis_ctx bound to a CUDA device (and a rank of a sharded search)."""
 
@@ -240,6 +270,18 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(lib().adaptis_ctx_launch_count(self.ptr))
+
+    @property
+    def counters(self) -> dict:
+        a = (C.c_uint64 * 3)()
+        lib().adaptis_ctx_counters(self.ptr, a)
+        return {"tasks": int(a[0]), "rounds": int(a[1]), "live_lane_rounds": int(a[2])}
+
+    def launch_info(self) -> list:
+        """Per-segment launches of the last evaluation (device ms via CUDA events)."""
+        arr = (_LaunchInfo * 64)()
+        n = lib().adaptis_ctx_launch_info(self.ptr, arr, 64)
+        return [{k: getattr(arr[i], k) for k, _ in _LaunchInfo._fields_} for i in range(min(n, 64))]
 
     @property
     def fallback_count(self) -> int:

@@ -66,4 +66,16 @@ ADAPTIS_HD bool decode_cuts(const uint64_t* binom, const uint64_t* ball, const i
   return ok && (L > prev);
 }
 
+// Block-cyclic shard map: the global index range [lo, hi) is cut
+// into chunks of 2^kChunkBits indices, chunk k belonging to rank k mod world;
+// position `pos` of this rank's share maps to a global index. first_chunk, n0
+// and start0 describe the rank's first (possibly partial) chunk.
+ADAPTIS_HD uint64_t shard_index(uint64_t pos, uint64_t n0, uint64_t start0, uint64_t first_chunk,
+                                int world) {
+  if (pos < n0) return start0 + pos;
+  const uint64_t q = pos - n0;
+  const uint64_t t = q >> kChunkBits;
+  return ((first_chunk + (t + 1) * (uint64_t)world) << kChunkBits) + (q & ((1ull << kChunkBits) - 1));
+}
+
 }  // namespace adaptis

@@ -77,6 +77,10 @@ struct adaptis_ctx {
   std::string err;
   uint64_t launches = 0;
   uint64_t fallback_cands = 0;
+  uint64_t counters[3] = {0, 0, 0};
+  uint64_t last_tasks = 0;
+  std::vector<cudaEvent_t> seg_events;
+  std::vector<adaptis_launch_info> last_info;
   // scratch
   unsigned long long* d_scratch = nullptr;  // [0] key, [1] n_invalid, [2..] cursors/overflow counts
   size_t scratch_words = 0;
@@ -355,18 +359,19 @@ constexpr size_t kOverflowPerSeg = 1u << 20;
 // fast-path ring slots per stage and direction: GREEDY's F-first rule lets a
 // producer run further ahead than the fixed orders do (DESIGN.md §"Rings")
 int ring_slots(int policy, int m) {
-  int k = kRingK;
-  if (policy == ADAPTIS_GREEDY) k = 32;
-  const char* e = getenv(policy == ADAPTIS_GREEDY ? "ADAPTIS_RING_K_GREEDY" : "ADAPTIS_RING_K");
-  if (e && atoi(e) > 0) k = atoi(e);
   int mp = 1;
   while (mp < m) mp <<= 1;
+  if (policy == ADAPTIS_GREEDY) return mp;  // GREEDY rings are never full: >= m slots
+  int k = kRingK;
+  const char* e = getenv("ADAPTIS_RING_K");
+  if (e && atoi(e) > 0) k = atoi(e);
   if (k > mp) k = mp;
   int pw = 1;
   while (pw < k) pw <<= 1;
   return pw;
 }
-constexpr size_t kHdr = 4;
+constexpr size_t kHdr = 8;  // [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds
+constexpr size_t kGreedySmemRing = 16384;  // per warp
 
 // global-memory ring scratch for a launch with s.ring_k slots; bounds the grid
 adaptis_status ensure_gring(adaptis_ctx* ctx, const adaptis_prepared* P, const SegLaunch& s,
@@ -405,20 +410,26 @@ SegLaunch make_launch(const adaptis_prepared* P, const Seg& sg) {
 // Evaluate [lo, hi) (global indices) on this context's GPU: every segment it
 // touches is launched; overflowed candidates are re-run by the fallback kernel.
 // mode_search: pack keys into d_key; else write SoA results at idx - eval_first.
+// Scratch words: [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds,
+// then per segment i at kHdr + kSegWords*i: [0] cursor [1] overflow count
+// [2] tasks [3] fallback cursor [4] fallback overflow count.
+constexpr size_t kSegWords = 6;
 adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uint64_t hi,
                          bool mode_search, int rank, int world, const adaptis_results_soa* dout,
                          uint64_t eval_first, int64_t* report, float* kernel_ms) {
   const size_t nseg = P->segs.size();
-  // scratch words: [0] key, [1] invalid, [2] tasks, [4 + 2i] cursor i,
-  // [5 + 2i] overflow count i, then the same pair per segment for the fallback
-  adaptis_status st = ensure_scratch(ctx, kHdr + 4 * nseg, kOverflowPerSeg * nseg);
+  const size_t nwords = kHdr + kSegWords * nseg;
+  adaptis_status st = ensure_scratch(ctx, nwords, kOverflowPerSeg * nseg);
   if (st != ADAPTIS_OK) return st;
-  unsigned long long* key = ctx->d_scratch;
-  unsigned long long* ninv = ctx->d_scratch + 1;
-  unsigned long long* ntask = ctx->d_scratch + 2;
-  std::vector<unsigned long long> init(kHdr + 4 * nseg, 0);
+  while (ctx->seg_events.size() < 2 * nseg) {
+    cudaEvent_t e;
+    CU(ctx, cudaEventCreate(&e));
+    ctx->seg_events.push_back(e);
+  }
+  unsigned long long* W = ctx->d_scratch;
+  std::vector<unsigned long long> init(nwords, 0);
   init[0] = (~0ull) >> 1;
-  CU(ctx, cudaMemcpyAsync(ctx->d_scratch, init.data(), init.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(W, init.data(), nwords * 8, cudaMemcpyHostToDevice, ctx->stream));
   CU(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   std::vector<SegLaunch> launched(nseg);
   std::vector<char> active(nseg, 0);
@@ -429,27 +440,30 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     SegLaunch s = make_launch(P, sg);
     shard(a, b, rank, world, &s);
     if (s.n_pos == 0) continue;
-    s.key = mode_search ? key : nullptr;
+    unsigned long long* sw = W + kHdr + kSegWords * i;
+    s.key = mode_search ? W : nullptr;
     s.eval_first = eval_first;
     if (!mode_search && dout) {
       s.out_makespan = dout->makespan; s.out_peak = dout->peak_mem_bytes;
       s.out_bubble = dout->bubble_ratio; s.out_status = dout->status;
     }
     s.out_report = report;
-    s.cursor = ctx->d_scratch + kHdr + 2 * i;
-    s.overflow_count = reinterpret_cast<unsigned int*>(ctx->d_scratch + kHdr + 1 + 2 * i);
+    s.cursor = sw + 0;
+    s.overflow_count = reinterpret_cast<unsigned int*>(sw + 1);
     s.overflow_idx = ctx->d_overflow + kOverflowPerSeg * i;
     s.overflow_cap = (unsigned)kOverflowPerSeg;
-    s.n_invalid = ninv;
-    s.n_tasks = ntask;
-    // GREEDY with m beyond the shared-memory ring depth: full-depth rings in
-    // global memory from the start (its F-first rule can run m items ahead)
-    const bool direct_global = s.policy == ADAPTIS_GREEDY && P->m > s.ring_k;
+    s.n_invalid = W + 1;
+    s.n_tasks = sw + 2;
+    s.n_rounds = W + 3;
+    // GREEDY rings hold all m items (its F-first rule can run m items ahead);
+    // they live in global memory when they do not fit the shared-memory budget
+    const size_t ring_bytes = (size_t)2 * s.ring_k * s.G * s.S * (P->use_int64 ? 8 : 4);
+    static const size_t greedy_smem_ring =
+        getenv("ADAPTIS_GREEDY_SMEM_RING") ? (size_t)atol(getenv("ADAPTIS_GREEDY_SMEM_RING")) : kGreedySmemRing;
+    const bool direct_global = s.policy == ADAPTIS_GREEDY && ring_bytes > greedy_smem_ring;
+    CU(ctx, cudaEventRecord(ctx->seg_events[2 * i], ctx->stream));
     int e;
     if (direct_global) {
-      int K = 1;
-      while (K < P->m) K <<= 1;
-      s.ring_k = K;
       unsigned grid_limit = 0;
       st = ensure_gring(ctx, P, s, &grid_limit);
       if (st != ADAPTIS_OK) return st;
@@ -459,17 +473,21 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
       e = launch_segment(P->tabs, s, ctx->num_sms, ctx->stream, false, 0);
     }
     if (e) return fail(ctx, ADAPTIS_ECUDA, "kernel launch (segment %zu): %s", i, cudaGetErrorString((cudaError_t)e));
+    CU(ctx, cudaEventRecord(ctx->seg_events[2 * i + 1], ctx->stream));
     ctx->launches++;
     launched[i] = s;
     active[i] = 1;
   }
   // fallback for candidates whose fast-path rings filled up (exact re-run, rings >= m)
-  std::vector<unsigned long long> words(kHdr + 2 * nseg);
-  CU(ctx, cudaMemcpyAsync(words.data(), ctx->d_scratch, words.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<unsigned long long> words(nwords);
+  CU(ctx, cudaMemcpyAsync(words.data(), W, nwords * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
+  std::vector<float> seg_ms(nseg, 0.0f);
+  for (size_t i = 0; i < nseg; ++i)
+    if (active[i]) CU(ctx, cudaEventElapsedTime(&seg_ms[i], ctx->seg_events[2 * i], ctx->seg_events[2 * i + 1]));
   for (size_t i = 0; i < nseg; ++i) {
     if (!active[i]) continue;
-    const unsigned int cnt = (unsigned int)(words[kHdr + 1 + 2 * i] & 0xffffffffu);
+    const unsigned int cnt = (unsigned int)(words[kHdr + kSegWords * i + 1] & 0xffffffffu);
     if (cnt == 0) continue;
     ctx->fallback_cands += cnt;
     SegLaunch s = launched[i];
@@ -480,20 +498,45 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
       s.list_idx = s.overflow_idx;
       s.n_pos = cnt;
     }  // else: re-run the whole segment shard in fallback mode
-    s.cursor = ctx->d_scratch + kHdr + 2 * nseg + 2 * i;
-    s.overflow_count = reinterpret_cast<unsigned int*>(ctx->d_scratch + kHdr + 1 + 2 * nseg + 2 * i);
+    unsigned long long* sw = W + kHdr + kSegWords * i;
+    s.cursor = sw + 3;
+    s.overflow_count = reinterpret_cast<unsigned int*>(sw + 4);
     s.overflow_cap = 0;
     unsigned grid_limit = 0;
     st = ensure_gring(ctx, P, s, &grid_limit);
     if (st != ADAPTIS_OK) return st;
     s.gring = ctx->d_gring;
+    CU(ctx, cudaEventRecord(ctx->seg_events[2 * i], ctx->stream));
     int e = launch_segment(P->tabs, s, ctx->num_sms, ctx->stream, true, grid_limit);
     if (e) return fail(ctx, ADAPTIS_ECUDA, "fallback launch: %s", cudaGetErrorString((cudaError_t)e));
+    CU(ctx, cudaEventRecord(ctx->seg_events[2 * i + 1], ctx->stream));
     ctx->launches++;
+    active[i] = 2;
   }
   CU(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   if (kernel_ms) CU(ctx, cudaEventElapsedTime(kernel_ms, ctx->ev0, ctx->ev1));
+  CU(ctx, cudaMemcpy(words.data(), W, nwords * 8, cudaMemcpyDeviceToHost));
+  ctx->counters[1] += words[3];
+  ctx->counters[2] += words[4];
+  ctx->last_info.clear();
+  uint64_t tasks = 0;
+  for (size_t i = 0; i < nseg; ++i) {
+    if (!active[i]) continue;
+    float fb = 0.0f;
+    if (active[i] == 2) CU(ctx, cudaEventElapsedTime(&fb, ctx->seg_events[2 * i], ctx->seg_events[2 * i + 1]));
+    const Seg& sg = P->segs[i];
+    adaptis_launch_info li{};
+    li.group = sg.group; li.combo = sg.combo; li.v = sg.v; li.placement = sg.placement;
+    li.policy = sg.policy; li.candidates = launched[i].n_pos;
+    li.tasks = words[kHdr + kSegWords * i + 2];
+    li.ms = seg_ms[i] + fb;
+    li.fallback = active[i] == 2 ? (int32_t)(words[kHdr + kSegWords * i + 1] & 0xffffffffu) : 0;
+    tasks += li.tasks;
+    ctx->last_info.push_back(li);
+  }
+  ctx->counters[0] += tasks;
+  ctx->last_tasks = tasks;
   return ADAPTIS_OK;
 }
 
@@ -544,6 +587,7 @@ void adaptis_ctx_destroy(adaptis_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_scratch); cudaFree(c->d_overflow); cudaFree(c->d_gring); cudaFree(c->d_report);
+  for (cudaEvent_t e : c->seg_events) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -559,6 +603,15 @@ adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_allreduce_min
 void* adaptis_ctx_stream(adaptis_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 uint64_t adaptis_ctx_launch_count(const adaptis_ctx* ctx) { return ctx ? ctx->launches : 0; }
 uint64_t adaptis_ctx_fallback_count(const adaptis_ctx* ctx) { return ctx ? ctx->fallback_cands : 0; }
+int adaptis_ctx_launch_info(const adaptis_ctx* ctx, adaptis_launch_info* out, int max) {
+  if (!ctx) return 0;
+  const int n = (int)ctx->last_info.size();
+  for (int i = 0; i < n && i < max && out; ++i) out[i] = ctx->last_info[i];
+  return n;
+}
+void adaptis_ctx_counters(const adaptis_ctx* ctx, uint64_t out[3]) {
+  for (int i = 0; i < 3; ++i) out[i] = ctx ? ctx->counters[i] : 0;
+}
 
 adaptis_status adaptis_space_size(const adaptis_problem* problem, const adaptis_space* space,
                                   uint64_t* n_out) {
@@ -670,7 +723,8 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   CU(ctx, cudaMemcpyAsync(words, ctx->d_scratch, 24, cudaMemcpyDeviceToHost, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   out->n_invalid = words[1];
-  out->n_tasks = words[2];
+  out->n_tasks = ctx->last_tasks;
+  const std::vector<adaptis_launch_info> search_info = ctx->last_info;
   out->kernel_ms = ms;
   out->n_candidates = P->N;
   {
@@ -711,6 +765,7 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
     CU(ctx, cudaStreamSynchronize(ctx->stream));
   }
   cudaFree(dmk); cudaFree(dpk); cudaFree(dbub); cudaFree(dst);
+  ctx->last_info = search_info;  // report the search's launches, not the re-evaluation
   if (st != ADAPTIS_OK) return st;
   out->result.makespan = mk;
   out->result.peak_mem_bytes = pk;
@@ -725,6 +780,26 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   }
   if (mk != (int64_t)(key >> P->key_bits))
     return fail(ctx, ADAPTIS_ECUDA, "winner re-evaluation disagrees with its search key");
+  return ADAPTIS_OK;
+}
+
+adaptis_status adaptis_shard_indices(const adaptis_problem* problem, const adaptis_space* space,
+                                     int rank, int world, uint64_t* out, uint64_t cap,
+                                     uint64_t* n_out) {
+  if (!n_out) return fail(nullptr, ADAPTIS_EINVAL, "n_out is NULL");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(nullptr, ADAPTIS_EINVAL, "rank = %d, world = %d", rank, world);
+  adaptis_prepared P;
+  adaptis_status st = build_space(nullptr, problem, space, &P);
+  if (st != ADAPTIS_OK) return st;
+  uint64_t n = 0;
+  for (const Seg& sg : P.segs) {
+    SegLaunch s{};
+    shard(sg.base, sg.base + sg.count, rank, world, &s);
+    for (uint64_t q = 0; q < s.n_pos; ++q, ++n)
+      if (out && n < cap) out[n] = shard_index(q, s.n0, s.start0, s.first_chunk, s.world);
+  }
+  *n_out = n;
   return ADAPTIS_OK;
 }
 

@@ -56,6 +56,7 @@ struct SegLaunch {
   unsigned int overflow_cap;
   unsigned long long* n_invalid;// invalid decodes counted by this launch
   unsigned long long* n_tasks;  // simulated tasks counted by this launch
+  unsigned long long* n_rounds; // [0] warp rounds, [1] live device-lane rounds
   // fallback mode: positions index overflow_idx_in[] instead of [lo, hi)
   const uint64_t* list_idx;
   int ring_k;                   // ring slots (fast path: kRingK; fallback: >= m)
@@ -74,7 +75,7 @@ struct SegLaunch {
 // (split policies), the slots' cuts, and the fast-path rings
 // [2 directions][K slots][G*S stages].
 struct WarpLayout {
-  int rec_off, dmem_off, cuts_off, ring_off, per_warp;
+  int rec_off, dmem_off, cuts_off, cnt_off, ring_off, per_warp;
   ADAPTIS_LAYOUT_HD size_t prefix_bytes(int L) const {
     return ((size_t)kNumCols * (L + 1) * 8 + 15) & ~(size_t)15;
   }
@@ -86,6 +87,7 @@ ADAPTIS_LAYOUT_HD WarpLayout warp_layout(int S, int G, int V, int K, int tsz, in
   l.rec_off = off;  off += 3 * V * 32 * rsz;
   l.dmem_off = off; off += 3 * V * 32 * 8;
   l.cuts_off = off; off += align16(G * (S + 1) * 2);
+  l.cnt_off = off;  off += 32 * 4 * 4;  // GREEDY produced-count words [lane][chunk]
   l.ring_off = off; if (!gring) off += 2 * K * G * S * tsz;
   l.per_warp = align16(off);
   return l;

@@ -31,6 +31,7 @@ namespace adaptis {
 
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr int kQueueBlock = 64;  // positions claimed per warp atomic
+constexpr int kGreedyCommits = 1; // GREEDY tasks a lane may commit per round (more is slower)
 
 template <typename T> struct TT;
 template <> struct TT<int32_t> { static constexpr int32_t INF = INT32_MAX; };
@@ -122,15 +123,16 @@ __device__ int64_t megatron_peak(const int64_t (&a)[V], int p, int m, int w) {
 
 __device__ __forceinline__ uint64_t pos_to_index(const SegLaunch& sl, uint64_t pos) {
   if (sl.list_idx) return sl.list_idx[pos];
-  if (pos < sl.n0) return sl.start0 + pos;
-  const uint64_t q = pos - sl.n0;
-  const uint64_t t = q >> kChunkBits;
-  return ((sl.first_chunk + (t + 1) * (uint64_t)sl.world) << kChunkBits) +
-         (q & ((1ull << kChunkBits) - 1));
+  return shard_index(pos, sl.n0, sl.start0, sl.first_chunk, sl.world);
 }
 
+// register budget per policy (measured on B200, DESIGN.md §"Occupancy"): the
+// dataflow policies run best at <= 102 registers (5 CTAs/SM), GREEDY without a cap
+template <int POLICY> struct MinBlocks { static constexpr int value = 5; };
+template <> struct MinBlocks<ADAPTIS_GREEDY> { static constexpr int value = 1; };
+
 template <int POLICY, int V, typename T, bool GRING>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MinBlocks<POLICY>::value)
 seg_kernel(const DevTables tab, const SegLaunch sl) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr bool FUSED = (POLICY == ADAPTIS_GPIPE || POLICY == ADAPTIS_ONEF1B);
@@ -168,6 +170,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   Rec<T>* recs = reinterpret_cast<Rec<T>*>(wbase + lay.rec_off);
   int64_t* dmem = reinterpret_cast<int64_t*>(wbase + lay.dmem_off);
   int16_t* cuts_all = reinterpret_cast<int16_t*>(wbase + lay.cuts_off);
+  unsigned* cntw = reinterpret_cast<unsigned*>(wbase + lay.cnt_off);  // [lane][chunk]
   T* ring;
   if constexpr (GRING) {
     const size_t gw = (size_t)blockIdx.x * kWarpsPerCta + warp;
@@ -210,12 +213,20 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   // GREEDY per-chunk counters and F-gate bytes
   int gF[V], gB[V], gW[V];
   int64_t gA[V];
+  T pFc[V], pBc[V];   // cost of the cross-device predecessor of the F / B head (INF: none)
+  unsigned pleft = 0; // bit c: F-pred of chunk c on the left neighbour; bit V+c: B-pred
+  T hF[V], hB[V];     // cached arrival of the F / B head (-1: not yet produced)
+  int tF[V], tB[V];   // consumer (lane << 3 | chunk) of this chunk's F / B output, -1: none
 #pragma unroll
-  for (int c = 0; c < V; ++c) { gF[c] = gB[c] = gW[c] = 0; gA[c] = 0; }
+  for (int c = 0; c < V; ++c) {
+    gF[c] = gB[c] = gW[c] = 0; gA[c] = 0; pFc[c] = INF; pBc[c] = INF;
+    hF[c] = -1; hB[c] = -1; tF[c] = -1; tB[c] = -1;
+  }
   // queue (warp-uniform) and accumulators
   uint64_t qpos = 0, qend = 0;
   bool exhausted = false;
-  unsigned long long wkey = ~0ull >> 1, winvalid = 0, wtasks = 0;
+  unsigned long long wkey = ~0ull >> 1, winvalid = 0, wtasks = 0, wrounds = 0, wlive = 0;
+  unsigned ctasks = 0, clive = 0;  // this lane's tasks / live rounds since the last flush
 
   auto next_task = [&]() {
     if (nF < tot && (POLICY == ADAPTIS_GPIPE || nF - nB <= wup)) { tk = 0; tc = fp.c; tj = fp.mb(); }
@@ -226,6 +237,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
 
   // collective: write results of the slots with `fl` set (all lanes execute)
   auto finalize = [&](bool fl) {
+    if (fl) { wtasks += ctasks; wlive += clive; ctasks = 0; clive = 0; }
     const bool contrib = fl && dev_lane;
     const int64_t mk = seg_max(contrib ? (int64_t)free_t : (int64_t)0, p2);
     const int64_t sb = seg_sum(contrib ? busy : (int64_t)0, p2);
@@ -269,9 +281,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
     }
   };
 
+  bool maint = true;  // warp-uniform: some slot finished, or idle slots can be refilled
   for (;;) {
     // ================= maintenance: finalize finished slots, refill idle ones
-    {
+    if (maint) {
+      maint = false;
       const unsigned live_m = __ballot_sync(FULLMASK, active && !done);
       const bool fin = active && !(live_m & smask);
       const unsigned fin_m = __ballot_sync(FULLMASK, fin);
@@ -359,6 +373,31 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
                 DMEM(2, c) = -sta;
               }
               ac[c] = act + sta;
+              if constexpr (GREEDY) {
+                // Lemma 3 refinement: an unknown head F(s, j) waits for F(s-1, j) on the
+                // device of stage s-1, which lasts c_F(s-1) and then travels oF(s-1)
+                T pf = INF, pb = INF;
+                bool fl = true, bl = false;
+                if (s > 0 && dev_of(sl.placement, p, s - 1) != d) {
+                  const int a0 = cuts[s - 1];
+                  pf = (T)(pre[kColTF * (L + 1) + a] - pre[kColTF * (L + 1) + a0]) + (T)tab.comm[a - 1];
+                  fl = dev_of(sl.placement, p, s - 1) == (d == 0 ? p - 1 : d - 1);
+                }
+                if (s < S - 1 && dev_of(sl.placement, p, s + 1) != d) {
+                  const int b1 = cuts[s + 2];
+                  pb = (T)(pre[kColTB * (L + 1) + b1] - pre[kColTB * (L + 1) + b]) + (T)tab.comm[b - 1];
+                  bl = dev_of(sl.placement, p, s + 1) == (d == 0 ? p - 1 : d - 1);
+                }
+                pFc[c] = pf;
+                pBc[c] = pb;
+                tF[c] = s < S - 1 ? (((leader + dev_of(sl.placement, p, s + 1)) << 3) | ((s + 1) / p)) : -1;
+                tB[c] = s > 0 ? (((leader + dev_of(sl.placement, p, s - 1)) << 3) | ((s - 1) / p)) : -1;
+                hF[c] = s == 0 ? (T)0 : (T)-1;
+                hB[c] = s == S - 1 ? (T)0 : (T)-1;
+                cntw[lane * 4 + c] = 0;
+                pleft = (pleft & ~((1u << c) | (1u << (V + c)))) | ((fl ? 1u : 0u) << c) |
+                        ((bl ? 1u : 0u) << (V + c));
+              }
             }
           }
           // ---- a4 memory precheck of the fused fixed orders (R16)
@@ -386,7 +425,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             }
           }
           // ---- ring reset for the slots being set up
-          if (take && dev_lane) {
+          if (!GREEDY && take && dev_lane) {
             for (int s = d; s < S; s += p)
               for (int k = 0; k < 2 * sl.ring_k; ++k) ring[(size_t)k * RS + g * S + s] = EMPTY;
           }
@@ -406,15 +445,20 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           __syncwarp();
         }
       }
-      if (__ballot_sync(FULLMASK, active) == 0) {
+      const unsigned act_m = __ballot_sync(FULLMASK, active);
+      if (act_m == 0) {
         if (exhausted) break;
+        maint = true;
         continue;
       }
+      maint = (act_m != FULLMASK) && !exhausted;  // some slot is still idle
     }
 
     // ================= a5: one simulation round
     bool progressed = false, blocked = false;
     const bool live = active && !done;
+    ++wrounds;
+    clive += live ? 1u : 0u;
     if constexpr (!GREEDY) {
       T r = 0;
       int iaddr = -1, oaddr = -1;
@@ -439,7 +483,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             const int c = V - 1 - wp.c;
             free_t += REC(2, c).dur;
             dyn += DMEM(2, c);
-            ++nW; wp.next(p, V); ++wtasks;
+            ++nW; wp.next(p, V); ++ctasks;
             progressed = true;
           }
         }
@@ -459,33 +503,41 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             }
           }
           if (tk == 0) { ++nF; fp.next(p, V); } else { ++nB; bp.next(p, V); }
-          ++wtasks;
+          ++ctasks;
           progressed = true;
           next_task();
         }
         if (tk == 2 && (!ZB || nW == tot)) done = true;
       }
     } else {
-      // ---- GREEDY (R14) in bounded-lag rounds (Lemma 3 with neighbour bounds)
+      // ---- GREEDY (R14) in bounded-lag rounds (Lemma 3 with per-head bounds).
+      // Rings are >= m deep (every slot written once per candidate); producers
+      // bump the consumer's produced-count word, consumers read a slot once it
+      // exists and cache the head's arrival time.
       T at = INF;
       int ak = -1, acx = 0, aj = 0;
-      if (live) {
-        T rF[V], rB[V];
+      unsigned unkF = 0, unkB = 0;  // heads whose arrival is still unknown
+      auto decide = [&]() {
+        at = INF; ak = -1; unkF = 0; unkB = 0;
         bool cFv[V], cBv[V], cWv[V];
         T rmin = INF;
 #pragma unroll
         for (int c = 0; c < V; ++c) {
           const int s = stage_of(sl.placement, p, c, d);
           const int row = g * S + s;
+          const unsigned cw = ((volatile unsigned*)cntw)[lane * 4 + c];
+          if (hF[c] < 0 && gF[c] < (int)(cw & 0xffffu))
+            hF[c] = ((volatile T*)ring)[row + (gF[c] & KM) * RS];
+          if (hB[c] < 0 && gB[c] < (int)(cw >> 16))
+            hB[c] = ((volatile T*)ring)[BOFF + row + (gB[c] & KM) * RS];
           cFv[c] = false; cBv[c] = false; cWv[c] = gW[c] < gB[c];
-          rF[c] = 0; rB[c] = 0;
           if (gF[c] < m && stat + dyn + gA[c] <= sl.cap) {
-            const T r = s > 0 ? ring[row + (gF[c] & KM) * RS] : (T)0;
-            if (r >= 0) { cFv[c] = true; rF[c] = r; rmin = r < rmin ? r : rmin; }
+            if (hF[c] >= 0) { cFv[c] = true; rmin = hF[c] < rmin ? hF[c] : rmin; }
+            else unkF |= 1u << c;
           }
           if (gB[c] < gF[c]) {
-            const T r = s < S - 1 ? ring[BOFF + row + (gB[c] & KM) * RS] : (T)0;
-            if (r >= 0) { cBv[c] = true; rB[c] = r; rmin = r < rmin ? r : rmin; }
+            if (hB[c] >= 0) { cBv[c] = true; rmin = hB[c] < rmin ? hB[c] : rmin; }
+            else unkB |= 1u << c;
           }
           if (cWv[c]) rmin = 0;
         }
@@ -494,11 +546,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           int bj = INT_MAX;  // key (kind F < B < W, mb, stage); stage order == chunk order
 #pragma unroll
           for (int c = 0; c < V; ++c)
-            if (cFv[c] && rF[c] <= at && gF[c] < bj) { bj = gF[c]; ak = 0; acx = c; }
+            if (cFv[c] && hF[c] <= at && gF[c] < bj) { bj = gF[c]; ak = 0; acx = c; }
           if (ak < 0) {
 #pragma unroll
             for (int c = 0; c < V; ++c)
-              if (cBv[c] && rB[c] <= at && gB[c] < bj) { bj = gB[c]; ak = 1; acx = c; }
+              if (cBv[c] && hB[c] <= at && gB[c] < bj) { bj = gB[c]; ak = 1; acx = c; }
           }
           if (ak < 0) {
 #pragma unroll
@@ -507,65 +559,86 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           }
           aj = bj;
         }
-      }
-      // Every unscheduled task starts at >= t*; a neighbour n starts its next task
-      // at >= min(at_n, t* + window); so no new arrival reaches this lane before
-      // `bound` and its decision at `at` < bound is final.
+      };
+      if (live) decide();
+      // Every unscheduled task starts at >= t*, and a neighbour n starts every
+      // further task at >= min(at_n, t* + window) for the rest of this round. An
+      // unknown head therefore cannot become ready before that start plus its
+      // predecessor's duration and latency; decisions below every such bound are
+      // final (DESIGN.md Lemma 3').
       const T tstar = seg_min(at, p2);
       const T atl = __shfl_sync(FULLMASK, at, nleft);
       const T atr = __shfl_sync(FULLMASK, at, nright);
-      T lim = atl < atr ? atl : atr;
       const T tw = sat_add(tstar, window);
-      lim = lim < tw ? lim : tw;
-      const T bound = sat_add(lim, window);
-      int oaddr = -1, iaddr = -1;
-      bool go = false;
-      if (ak >= 0 && at < bound) {
-        const int s = stage_of(sl.placement, p, acx, d);
-        const int row = g * S + s;
-        if (ak == 0) {
-          iaddr = s > 0 ? row + (aj & KM) * RS : -1;
-          oaddr = s < S - 1 ? row + 1 + (aj & KM) * RS : -1;
-        } else if (ak == 1) {
-          iaddr = s < S - 1 ? BOFF + row + (aj & KM) * RS : -1;
-          oaddr = s > 0 ? BOFF + row - 1 + (aj & KM) * RS : -1;
+      const T nl = atl < tw ? atl : tw;
+      const T nr = atr < tw ? atr : tw;
+      T bound = INF;
+      auto tighten = [&]() {
+#pragma unroll
+        for (int c = 0; c < V; ++c) {
+          if (unkF & (1u << c)) {
+            const T x = sat_add((pleft >> c) & 1u ? nl : nr, pFc[c]);
+            bound = x < bound ? x : bound;
+          }
+          if (unkB & (1u << c)) {
+            const T x = sat_add((pleft >> (V + c)) & 1u ? nl : nr, pBc[c]);
+            bound = x < bound ? x : bound;
+          }
         }
-        const bool ofree = oaddr < 0 || ring[oaddr] == EMPTY;
-        go = ofree;
-        blocked = !ofree;
-      }
+      };
+      tighten();
       __syncwarp();
-      if (go) {
+      // commit while the decision stays below the bound (several tasks per round)
+      for (int k = 0; k < kGreedyCommits && live && !done && ak >= 0 && at < bound; ++k) {
         const Rec<T> rc = REC(ak, acx);
         const T fin = at + rc.dur;
         free_t = fin;
-        if (oaddr >= 0) ring[oaddr] = fin + rc.oc;
-        if (iaddr >= 0) ring[iaddr] = EMPTY;
         dyn += DMEM(ak, acx);
         if (ak == 0) peak = dyn > peak ? dyn : peak;
+        int tgt = -1, dir = 0;
 #pragma unroll
         for (int c = 0; c < V; ++c) {
-          gF[c] += (ak == 0 && c == acx);
-          gB[c] += (ak == 1 && c == acx);
-          gW[c] += (ak == 2 && c == acx);
+          if (c == acx) {
+            if (ak == 0) {
+              tgt = tF[c]; dir = 0; ++gF[c];
+              hF[c] = gF[c] < m && stage_of(sl.placement, p, c, d) == 0 ? (T)0 : (T)-1;
+            } else if (ak == 1) {
+              tgt = tB[c]; dir = 1; ++gB[c];
+              hB[c] = stage_of(sl.placement, p, c, d) == S - 1 ? (T)0 : (T)-1;
+            } else {
+              ++gW[c];
+            }
+          }
+        }
+        if (tgt >= 0) {  // publish the arrival, then count it for the consumer
+          ((volatile T*)ring)[rc.out_off + (aj & KM) * RS] = fin + rc.oc;
+          if (kGreedyCommits > 1) __threadfence_block();  // readers within this round
+          atomicAdd(&cntw[(tgt >> 3) * 4 + (tgt & 7)], dir ? 0x10000u : 1u);
         }
         bool all = true;
 #pragma unroll
         for (int c = 0; c < V; ++c) all = all && gW[c] == m;
         done = all;
-        ++wtasks;
+        ++ctasks;
         progressed = true;
+        if (!done && k + 1 < kGreedyCommits) { decide(); tighten(); }
       }
     }
     __syncwarp();
-    // ---- deadlock detection per slot (rare): no lane of a live slot progressed
+    // ---- per-slot bookkeeping: a slot whose lanes are all done finishes; a live
+    // slot in which no lane progressed is deadlocked (stuck, or rings too shallow)
     {
       const unsigned prog_m = __ballot_sync(FULLMASK, progressed);
       const unsigned live_m = __ballot_sync(FULLMASK, active && !done);
-      const unsigned blk_m = __ballot_sync(FULLMASK, blocked);
-      if (active && (live_m & smask) && !(prog_m & smask)) {
-        flags |= (blk_m & smask) ? F_OVERFLOW : F_STUCK;
-        done = true;
+      const bool slot_live = (live_m & smask) != 0;
+      const bool stall = active && slot_live && !(prog_m & smask);
+      if (__ballot_sync(FULLMASK, stall || (active && !slot_live))) {
+        const unsigned blk_m = __ballot_sync(FULLMASK, blocked);
+        if (stall) {
+          flags |= (blk_m & smask) ? F_OVERFLOW : F_STUCK;
+          done = true;
+        }
+        maint = true;
       }
     }
   }
@@ -573,16 +646,20 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
 #undef DMEM
 
   // ---- a7 argmin: warp min -> one atomicMin per warp; counters
+  wtasks += ctasks;
+  wlive += clive;
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long x = __shfl_xor_sync(FULLMASK, wkey, o);
     wkey = x < wkey ? x : wkey;
     winvalid += __shfl_xor_sync(FULLMASK, winvalid, o);
     wtasks += __shfl_xor_sync(FULLMASK, wtasks, o);
+    wlive += __shfl_xor_sync(FULLMASK, wlive, o);
   }
   if (lane == 0) {
     if (sl.key && wkey != (~0ull >> 1)) atomicMin(sl.key, wkey);
     if (winvalid) atomicAdd(sl.n_invalid, winvalid);
     if (wtasks) atomicAdd(sl.n_tasks, wtasks);
+    if (wrounds) { atomicAdd(&sl.n_rounds[0], wrounds); atomicAdd(&sl.n_rounds[1], wlive); }
   }
 }
 

@@ -39,18 +39,30 @@ for g in sp.groups:
             first = base + k * per
             prep.eval(first, min(n, 1024), device_out=True)  # warm this kernel
             fb0 = ctx.fallback_count
+            c0 = ctx.counters
             stream = torch.cuda.ExternalStream(ctx.stream)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record(stream)
-            r = prep.eval(first, n, device_out=True)
-            e1.record(stream)
-            e1.synchronize()
-            dt = e0.elapsed_time(e1) / 1e3
+            dts = []
+            for rep in range(2):  # best of two: the first launch of a kernel can be slow
+                if rep == 1:
+                    c0 = ctx.counters
+                torch.cuda.synchronize()
+                e0.record(stream)
+                r = prep.eval(first, n, device_out=True)
+                e1.record(stream)
+                e1.synchronize()
+                dts.append(e0.elapsed_time(e1) / 1e3)
+            dt = min(dts)
             st = torch.bincount(r["status"].long(), minlength=4).tolist()
+            c1 = ctx.counters
+            tk = c1["tasks"] - c0["tasks"]
+            rd = c1["rounds"] - c0["rounds"]
+            lv = c1["live_lane_rounds"] - c0["live_lane_rounds"]
             print(json.dumps({"seg": seg, "v": g.v, "combo": NAMES[(min(g.v, 2), combo)], "n": n,
                               "ms": round(dt * 1e3, 2), "Mcand_s": round(n / dt / 1e6, 2),
-                              "status": st, "fallback": ctx.fallback_count - fb0}), flush=True)
+                              "status": st, "fallback": ctx.fallback_count - fb0,
+                              "Gtask_s": round(tk / dt / 1e9, 2), "tasks_per_round": round(tk / max(rd, 1), 2),
+                              "lane_util": round(tk / max(lv, 1), 3)}), flush=True)
         k += 1
         seg += 1
     base += P
