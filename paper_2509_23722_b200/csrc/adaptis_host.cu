@@ -371,7 +371,7 @@ int ring_slots(int policy, int m) {
   return pw;
 }
 constexpr size_t kHdr = 8;  // [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds
-constexpr size_t kGreedySmemRing = 16384;  // per warp
+constexpr size_t kGreedySmemRing = 0;  // per warp: GREEDY rings live in global memory (L2)
 
 // global-memory ring scratch for a launch with s.ring_k slots; bounds the grid
 adaptis_status ensure_gring(adaptis_ctx* ctx, const adaptis_prepared* P, const SegLaunch& s,

@@ -126,10 +126,14 @@ __device__ __forceinline__ uint64_t pos_to_index(const SegLaunch& sl, uint64_t p
   return shard_index(pos, sl.n0, sl.start0, sl.first_chunk, sl.world);
 }
 
-// register budget per policy (measured on B200, DESIGN.md §"Occupancy"): the
-// dataflow policies run best at <= 102 registers (5 CTAs/SM), GREEDY without a cap
+// register budget (measured on B200, DESIGN.md §4 "Occupancy"): every policy
+// runs best at <= 102 registers (5 CTAs of 4 warps per SM); GREEDY with its
+// rings in global memory so that shared memory does not cap occupancy
 template <int POLICY> struct MinBlocks { static constexpr int value = 5; };
-template <> struct MinBlocks<ADAPTIS_GREEDY> { static constexpr int value = 1; };
+#ifndef ADAPTIS_GREEDY_MINB
+#define ADAPTIS_GREEDY_MINB 5
+#endif
+template <> struct MinBlocks<ADAPTIS_GREEDY> { static constexpr int value = ADAPTIS_GREEDY_MINB; };
 
 template <int POLICY, int V, typename T, bool GRING>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MinBlocks<POLICY>::value)
