@@ -62,6 +62,10 @@ enum { ADAPTIS_SEQ = 0, ADAPTIS_INTERLEAVED = 1, ADAPTIS_WAVE = 2 };
  * GPIPE and ONEF1B run B and W fused; ZB and GREEDY split them. */
 enum { ADAPTIS_GPIPE = 0, ADAPTIS_ONEF1B = 1, ADAPTIS_ZB = 2, ADAPTIS_GREEDY = 3 };
 
+/* Cost arithmetic (R1): exact int64 ticks, or the fp32-cost variant whose
+ * makespans agree with an fp64 evaluation within 1e-5 relative. */
+enum { ADAPTIS_COST_TICKS = 0, ADAPTIS_COST_FP32 = 1 };
+
 /* Partition spaces (R19): FULL = every contiguous S-way split of the L rows;
  * BALL = cut vectors within L1 distance `radius` of a seed partition. */
 enum { ADAPTIS_PART_FULL = 0, ADAPTIS_PART_BALL = 1 };
@@ -103,6 +107,10 @@ typedef struct {
   int64_t mem_cap_bytes;      /* M_d^capacity (uniform); INT64_MAX = unconstrained           */
   double  tick_seconds;       /* seconds per tick, throughput only (R22)                     */
   int64_t tokens_per_microbatch; /* throughput only (TS)                              */
+  int32_t cost_type;          /* ADAPTIS_COST_TICKS (exact integer ticks, default) or
+                                 ADAPTIS_COST_FP32 (all time arithmetic in fp32, R1)          */
+  const float* costs_f32;     /* FP32 only, optional: [4][L] real-valued t_f, t_b, t_w, comm
+                                 (each t >= 1, comm >= 0); NULL = the int64 tables as floats  */
 } adaptis_problem;
 
 typedef struct {              /* one group of the space per virtual-stage count v            */
@@ -132,6 +140,8 @@ typedef struct {
   int64_t* peak_mem_bytes;   /* max_d M_d (Alg. 1 Step 3); 0 for status 1 and 3            */
   float*   bubble_ratio;     /* 1 - sum_d busy_d / (p * makespan) (R7); 0 unless status 0   */
   uint8_t* status;           /* ADAPTIS_CAND_*                                              */
+  float*   makespan_f32;     /* FP32 cost mode: the fp32 makespan (makespan above is it
+                                rounded to the nearest tick); NULL to skip                  */
 } adaptis_results_soa;
 
 typedef struct {             /* host-side result of one candidate                            */
@@ -139,6 +149,7 @@ typedef struct {             /* host-side result of one candidate               
   float   bubble_ratio;
   double  throughput;        /* tokens/s = m * tokens_per_microbatch / (makespan * tick_s)   */
   uint8_t status;
+  float   makespan_f32;      /* FP32 cost mode: the unrounded makespan                       */
 } adaptis_result;
 
 typedef struct {             /* output of adaptis_search                                     */

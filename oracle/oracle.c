@@ -12,6 +12,7 @@
 #include "oracle.h"
 
 #include <limits.h>
+#include <math.h>
 #include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
@@ -91,18 +92,6 @@ int orc_fixed_order(const orc_problem* pr, const orc_plan* pl, int d, int* kind,
 #undef PUSH
 }
 
-/* ------------------------------------------------------------------------ */
-/* Per-candidate derived data: Alg. 1 Steps 1-2.                             */
-typedef struct {
-  int S, p, v, m, fused;
-  int dev[ORC_MAXS];
-  int64_t cF[ORC_MAXS], cB[ORC_MAXS], cW[ORC_MAXS];
-  int64_t act[ORC_MAXS], stash[ORC_MAXS], wg[ORC_MAXS];
-  int64_t xF[ORC_MAXS]; /* latency of edge (s-1 -> s) for F(s-1,j) -> F(s,j), R3/R5/R6 */
-  int64_t xB[ORC_MAXS]; /* latency of edge (s+1 -> s) for B(s+1,j) -> B(s,j)            */
-  int64_t dur[3][ORC_MAXS];
-} cand_t;
-
 static int cuts_valid(const orc_problem* pr, const orc_plan* pl) {
   if (pl->cuts[0] != 0 || pl->cuts[pl->S] != pr->L) return 0;
   for (int s = 0; s < pl->S; s++)
@@ -110,297 +99,51 @@ static int cuts_valid(const orc_problem* pr, const orc_plan* pl) {
   return 1;
 }
 
-static void derive(const orc_problem* pr, const orc_plan* pl, cand_t* c) {
-  const int S = pl->S;
-  c->S = S; c->p = pr->p; c->v = pl->v; c->m = pr->m;
-  c->fused = (pl->policy == ORC_GPIPE || pl->policy == ORC_ONEF1B); /* R2 */
-  for (int s = 0; s < S; s++) {
-    int a = pl->cuts[s], b = pl->cuts[s + 1];
-    c->dev[s] = orc_device_of_stage(pl->placement, pr->p, pl->v, s);
-    c->cF[s] = rows_sum(pr->t_f, a, b);
-    c->cB[s] = rows_sum(pr->t_b, a, b);
-    c->cW[s] = rows_sum(pr->t_w, a, b);
-    c->act[s] = rows_sum(pr->act, a, b);
-    c->stash[s] = rows_sum(pr->stash, a, b);
-    c->wg[s] = rows_sum(pr->weight, a, b) + rows_sum(pr->grad, a, b);
-  }
-  for (int s = 0; s < S; s++) {
-    /* the boundary between stage s-1 and s is the one after row cuts[s]-1 */
-    c->xF[s] = 0;
-    if (s > 0 && c->dev[s - 1] != c->dev[s]) c->xF[s] = pr->comm[pl->cuts[s] - 1];
-    c->xB[s] = 0;
-    if (s < S - 1 && c->dev[s + 1] != c->dev[s]) c->xB[s] = pr->comm[pl->cuts[s + 1] - 1];
-    c->dur[KF][s] = c->cF[s];
-    c->dur[KB][s] = c->fused ? c->cB[s] + c->cW[s] : c->cB[s];
-    c->dur[KW][s] = c->cW[s];
-  }
-}
-
-/* ------------------------------------------------------------------------ */
-/* Alg. 1 Step 3: the global event loop.       */
-typedef struct {
-  const orc_problem* pr;
-  const cand_t* c;
-  int policy;
-  int64_t* fin;                     /* fin[(kind*S + s)*m + j], UNK = not scheduled */
-  int64_t free_[ORC_MAXP], busy[ORC_MAXP], dyn[ORC_MAXP], peak[ORC_MAXP], stat[ORC_MAXP];
-  /* fixed lists (GPIPE / ONEF1B / ZB) */
-  int* lk; int* ls; int* lj; int len[ORC_MAXP]; int pos[ORC_MAXP]; int lcap;
-  /* ZB pending-W FIFO in B-completion order (R13) */
-  int* wq_s; int* wq_j; int wq_head[ORC_MAXP], wq_tail[ORC_MAXP]; int wcap;
-  /* GREEDY: next unissued F per stage (R14) */
-  int nextF[ORC_MAXS];
-} sim_t;
-
 #define FIN(st, k, s, j) ((st)->fin[((size_t)(k) * (st)->c->S + (s)) * (st)->c->m + (j)])
 
-/* ready time of a task: max over its DAG predecessors (S:141 edges) of
- * finish + edge latency; UNK while some predecessor is unscheduled. */
-static int64_t ready_time(const sim_t* st, int k, int s, int j) {
-  const cand_t* c = st->c;
-  if (k == KF) {
-    if (s == 0) return 0;
-    int64_t f = FIN(st, KF, s - 1, j);
-    return f == UNK ? UNK : f + c->xF[s];
-  }
-  if (k == KB) {
-    int64_t f = FIN(st, KF, s, j);
-    if (f == UNK) return UNK;
-    int64_t r = f;
-    if (s < c->S - 1) {
-      int64_t b = FIN(st, KB, s + 1, j);
-      if (b == UNK) return UNK;
-      r = max64(r, b + c->xB[s]);
-    }
-    return r;
-  }
-  return FIN(st, KB, s, j); /* W(s,j) <- B(s,j) on the same device */
+static double rows_sum_f(const double* col, int a, int b) {
+  double s = 0;
+  for (int l = a; l < b; l++) s += col[l];
+  return s;
 }
 
-typedef struct { int ok; int64_t at; int k, s, j; int from_list; } prop_t;
+/* exact integer ticks */
+#define OT int64_t
+#define OSUF(x) x
+#define OTMAX INT64_MAX
+#define OMAX max64
+#define OMIN min64
+#define ORND(x) (x)
+#define ORC_F64 0
+#define COMM(row) (pr->comm[(row)])
+#include "oracle_sim.inc"
+#undef OT
+#undef OSUF
+#undef OTMAX
+#undef OMAX
+#undef OMIN
+#undef ORND
+#undef ORC_F64
+#undef COMM
 
-static int fits(const sim_t* st, int d, int s) { /* Eq. 2 gate for issuing F(s, .) */
-  const cand_t* c = st->c;
-  return st->stat[d] + st->dyn[d] + c->act[s] + c->stash[s] <= st->pr->cap;
-}
-
-static prop_t propose(const sim_t* st, int d) {
-  prop_t pr = {0, 0, 0, 0, 0, 0};
-  const cand_t* c = st->c;
-  const int64_t fr = st->free_[d];
-  if (st->policy == ORC_GPIPE || st->policy == ORC_ONEF1B) {
-    /* fixed order: the next list task starts at max(free, ready) (R9-R11) */
-    if (st->pos[d] >= st->len[d]) return pr;
-    int i = d * st->lcap + st->pos[d];
-    int64_t r = ready_time(st, st->lk[i], st->ls[i], st->lj[i]);
-    if (r == UNK) return pr;
-    pr.ok = 1; pr.at = max64(fr, r); pr.k = st->lk[i]; pr.s = st->ls[i]; pr.j = st->lj[i];
-    pr.from_list = 1;
-    return pr;
-  }
-  if (st->policy == ORC_ZB) {
-    /* R13: W-fill without lookahead. */
-    int has_w = st->wq_head[d] < st->wq_tail[d];
-    int ws = 0, wj = 0;
-    if (has_w) {
-      ws = st->wq_s[d * st->wcap + st->wq_head[d]];
-      wj = st->wq_j[d * st->wcap + st->wq_head[d]];
-    }
-    if (st->pos[d] < st->len[d]) {
-      int i = d * st->lcap + st->pos[d];
-      int k = st->lk[i], s = st->ls[i], j = st->lj[i];
-      /* (i) memory-forced W before an F that does not fit */
-      if (k == KF && !fits(st, d, s) && has_w) {
-        pr.ok = 1; pr.at = fr; pr.k = KW; pr.s = ws; pr.j = wj; return pr;
-      }
-      int64_t r = ready_time(st, k, s, j);
-      /* (ii) fill with the oldest W while the device would idle. If r is still
-       * unknown, this action is only executed when fr is the global minimum
-       * action time, and then r > fr because every unscheduled predecessor
-       * starts at >= fr and lasts >= 1 tick (R17). */
-      if (has_w && (r == UNK || fr < r)) {
-        pr.ok = 1; pr.at = fr; pr.k = KW; pr.s = ws; pr.j = wj; return pr;
-      }
-      if (r == UNK) return pr;
-      pr.ok = 1; pr.at = max64(fr, r); pr.k = k; pr.s = s; pr.j = j; pr.from_list = 1;
-      return pr;
-    }
-    if (has_w) { pr.ok = 1; pr.at = fr; pr.k = KW; pr.s = ws; pr.j = wj; }
-    return pr;
-  }
-  /* GREEDY (R14): candidates are the next unissued F of each own stage (if it
-   * fits under the cap), every B whose F is done, every pending W. Those ready
-   * at `at` = max(free, earliest ready) compete by key (kind F<B<W, mb, stage). */
-  int64_t rmin = INT64_MAX;
-  int nc = 0;
-  for (int pass = 0; pass < 2; pass++) {
-    int64_t at = max64(fr, rmin);
-    int bk = 99, bs = 0, bj = 0;
-    for (int s = 0; s < c->S; s++) {
-      if (c->dev[s] != d) continue;
-      int j = st->nextF[s];
-      if (j < c->m) {
-        int64_t r = ready_time(st, KF, s, j);
-        if (r != UNK && fits(st, d, s)) {
-          if (pass == 0) { rmin = min64(rmin, r); nc++; }
-          else if (r <= at && (KF < bk || (KF == bk && (j < bj || (j == bj && s < bs))))) {
-            bk = KF; bs = s; bj = j;
-          }
-        }
-      }
-      for (int jb = 0; jb < c->m; jb++) {
-        if (FIN(st, KF, s, jb) == UNK || FIN(st, KB, s, jb) != UNK) continue;
-        int64_t r = ready_time(st, KB, s, jb);
-        if (r == UNK) continue;
-        if (pass == 0) { rmin = min64(rmin, r); nc++; }
-        else if (r <= at && (KB < bk || (KB == bk && (jb < bj || (jb == bj && s < bs))))) {
-          bk = KB; bs = s; bj = jb;
-        }
-      }
-      for (int jw = 0; jw < c->m; jw++) {
-        if (FIN(st, KB, s, jw) == UNK || FIN(st, KW, s, jw) != UNK) continue;
-        int64_t r = FIN(st, KB, s, jw);
-        if (pass == 0) { rmin = min64(rmin, r); nc++; }
-        else if (r <= at && (KW < bk || (KW == bk && (jw < bj || (jw == bj && s < bs))))) {
-          bk = KW; bs = s; bj = jw;
-        }
-      }
-    }
-    if (pass == 0 && nc == 0) return pr;
-    if (pass == 1) { pr.ok = 1; pr.at = at; pr.k = bk; pr.s = bs; pr.j = bj; }
-  }
-  return pr;
-}
-
-static void execute(sim_t* st, int d, const prop_t* a, orc_trace* tr) {
-  const cand_t* c = st->c;
-  int64_t start = a->at, dur = c->dur[a->k][a->s], fin = start + dur;
-  FIN(st, a->k, a->s, a->j) = fin;
-  st->busy[d] += dur;
-  st->free_[d] = fin;
-  /* R16 memory: act + stash allocated at F start; act freed at B end, stash
-   * at W end (at B end when fused). Device events are totally ordered. */
-  if (a->k == KF) {
-    st->dyn[d] += c->act[a->s] + c->stash[a->s];
-    st->peak[d] = max64(st->peak[d], st->dyn[d]);
-  } else if (a->k == KB) {
-    st->dyn[d] -= c->act[a->s] + (c->fused ? c->stash[a->s] : 0);
-  } else {
-    st->dyn[d] -= c->stash[a->s];
-  }
-  if (tr && tr->n[d] < tr->cap_per_dev) {
-    int i = d * tr->cap_per_dev + tr->n[d]++;
-    tr->kind[i] = a->k; tr->stage[i] = a->s; tr->mb[i] = a->j; tr->start[i] = start;
-  }
-  if (st->policy == ORC_GREEDY) {
-    if (a->k == KF) st->nextF[a->s]++;
-    return;
-  }
-  if (a->from_list) st->pos[d]++;
-  if (st->policy == ORC_ZB) {
-    if (a->k == KB) { /* the W joins the FIFO in B-completion order */
-      int i = d * st->wcap + st->wq_tail[d]++;
-      st->wq_s[i] = a->s; st->wq_j[i] = a->j;
-    } else if (a->k == KW) {
-      st->wq_head[d]++;
-    }
-  }
-}
-
-int orc_simulate(const orc_problem* pr, const orc_plan* pl, orc_result* out, orc_trace* tr) {
-  memset(out, 0, sizeof(*out));
-  out->makespan = INT64_MAX;
-  if (tr) memset(tr->n, 0, sizeof(tr->n));
-  if (!cuts_valid(pr, pl)) { out->status = ORC_INVALID; return 0; }
-  cand_t c;
-  derive(pr, pl, &c);
-  const int S = c.S, p = pr->p, m = pr->m;
-  sim_t st;
-  memset(&st, 0, sizeof(st));
-  st.pr = pr; st.c = &c; st.policy = pl->policy;
-  st.fin = (int64_t*)malloc(sizeof(int64_t) * 3 * (size_t)S * m);
-  for (size_t i = 0; i < 3 * (size_t)S * m; i++) st.fin[i] = UNK;
-  for (int s = 0; s < S; s++) st.stat[c.dev[s]] += c.wg[s]; /* weights + grads */
-  int64_t list_peak[ORC_MAXP];
-  memset(list_peak, 0, sizeof(list_peak));
-  int fixed = (pl->policy != ORC_GREEDY);
-  if (fixed) {
-    st.lcap = 2 * m * pl->v;
-    st.lk = (int*)malloc(sizeof(int) * (size_t)st.lcap * p);
-    st.ls = (int*)malloc(sizeof(int) * (size_t)st.lcap * p);
-    st.lj = (int*)malloc(sizeof(int) * (size_t)st.lcap * p);
-    for (int d = 0; d < p; d++) {
-      st.len[d] = orc_fixed_order(pr, pl, d, st.lk + d * st.lcap, st.ls + d * st.lcap,
-                                  st.lj + d * st.lcap, st.lcap);
-      /* R16: for fused fixed orders the peak is a function of the list alone */
-      int64_t dyn = 0;
-      for (int i = 0; i < st.len[d]; i++) {
-        int s = st.ls[d * st.lcap + i];
-        if (st.lk[d * st.lcap + i] == KF) {
-          dyn += c.act[s] + c.stash[s];
-          list_peak[d] = max64(list_peak[d], dyn);
-        } else {
-          dyn -= c.act[s] + c.stash[s];
-        }
-      }
-    }
-    if (pl->policy == ORC_ZB) {
-      st.wcap = m * pl->v;
-      st.wq_s = (int*)malloc(sizeof(int) * (size_t)st.wcap * p);
-      st.wq_j = (int*)malloc(sizeof(int) * (size_t)st.wcap * p);
-    }
-  }
-  long remaining = (long)S * m * (c.fused ? 2 : 3);
-  int stuck = 0;
-  while (remaining > 0) {
-    int bd = -1;
-    prop_t best = {0, 0, 0, 0, 0, 0};
-    for (int d = 0; d < p; d++) {
-      prop_t a = propose(&st, d);
-      if (a.ok && (bd < 0 || a.at < best.at)) { best = a; bd = d; }
-    }
-    if (bd < 0) { stuck = 1; break; }
-    execute(&st, bd, &best, tr);
-    remaining--;
-  }
-  int rc = 0;
-  int64_t makespan = 0, peak = 0, sumbusy = 0;
-  int over = 0;
-  for (int d = 0; d < p; d++) {
-    out->T_d[d] = st.free_[d];
-    out->busy_d[d] = st.busy[d];
-    out->static_d[d] = st.stat[d];
-    int64_t pk = st.peak[d];
-    if (c.fused) {
-      if (!stuck && pk != list_peak[d]) rc = -1; /* event-loop peak must equal R16's */
-      pk = list_peak[d];
-    }
-    out->M_d[d] = st.stat[d] + pk;
-    if (out->M_d[d] > pr->cap) over = 1;
-    makespan = max64(makespan, st.free_[d]);
-    peak = max64(peak, out->M_d[d]);
-    sumbusy += st.busy[d];
-  }
-  if (c.fused && over) {
-    out->status = ORC_OVER_CAP;          /* decided by the order alone (R16)   */
-    out->peak_mem = peak;
-  } else if (stuck) {
-    out->status = ORC_STUCK;
-    out->peak_mem = 0;
-  } else if (over) {
-    out->status = ORC_OVER_CAP;
-    out->peak_mem = peak;
-  } else {
-    out->status = ORC_OK;
-    out->makespan = makespan;
-    out->peak_mem = peak;
-    out->bubble = 1.0 - (double)sumbusy / ((double)p * (double)makespan); /* R7 */
-  }
-  free(st.fin);
-  free(st.lk); free(st.ls); free(st.lj);
-  free(st.wq_s); free(st.wq_j);
-  return rc;
-}
+/* fp64 reference of the fp32-cost variant (costs from pr->costs_f64) */
+#define OT double
+#define OSUF(x) x##_f64
+#define OTMAX HUGE_VAL
+#define OMAX fmax
+#define OMIN fmin
+#define ORND(x) llround(x)
+#define ORC_F64 1
+#define COMM(row) (pr->costs_f64[3 * (size_t)pr->L + (row)])
+#include "oracle_sim.inc"
+#undef OT
+#undef OSUF
+#undef OTMAX
+#undef OMAX
+#undef OMIN
+#undef ORND
+#undef ORC_F64
+#undef COMM
 
 /* ------------------------------------------------------------------------ */
 /* Independent checker: longest path over DAG + list edges.          */
@@ -708,7 +451,7 @@ int orc_decode(const orc_problem* pr, const orc_space* sp, uint64_t index, orc_p
 /* Threaded drivers (plain work splitting; no change to the arithmetic).     */
 typedef struct {
   const orc_problem* pr; const orc_space* sp; const uint64_t* idx; uint64_t n;
-  int64_t* ms; int64_t* pk; double* bub; uint8_t* stt;
+  int64_t* ms; int64_t* pk; double* bub; uint8_t* stt; double* msf;
   int tid, nth; int err;
 } ev_arg;
 
@@ -717,7 +460,9 @@ static void* ev_worker(void* a_) {
   for (uint64_t i = a->tid; i < a->n; i += a->nth) {
     orc_plan pl; orc_result r;
     if (orc_decode(a->pr, a->sp, a->idx[i], &pl) != 0) { a->err = 1; continue; }
-    if (orc_simulate(a->pr, &pl, &r, NULL) != 0) a->err = 1;
+    int rc = a->pr->costs_f64 ? orc_simulate_f64(a->pr, &pl, &r, NULL) : orc_simulate(a->pr, &pl, &r, NULL);
+    if (rc != 0) a->err = 1;
+    if (a->msf) a->msf[i] = r.status == ORC_OK ? r.makespan_f : HUGE_VAL;
     if (a->ms) a->ms[i] = r.makespan;
     if (a->pk) a->pk[i] = r.peak_mem;
     if (a->bub) a->bub[i] = r.bubble;
@@ -728,13 +473,13 @@ static void* ev_worker(void* a_) {
 
 int orc_eval_indices(const orc_problem* pr, const orc_space* sp, const uint64_t* idx, uint64_t n,
                      int nthreads, int64_t* makespan, int64_t* peak, double* bubble,
-                     uint8_t* status) {
+                     uint8_t* status, double* makespan_f) {
   if (nthreads < 1) nthreads = 1;
   pthread_t th[256];
   ev_arg args[256];
   if (nthreads > 256) nthreads = 256;
   for (int t = 0; t < nthreads; t++) {
-    ev_arg a = {pr, sp, idx, n, makespan, peak, bubble, status, t, nthreads, 0};
+    ev_arg a = {pr, sp, idx, n, makespan, peak, bubble, status, makespan_f, t, nthreads, 0};
     args[t] = a;
     pthread_create(&th[t], NULL, ev_worker, &args[t]);
   }

@@ -45,6 +45,8 @@ typedef struct {
   const int64_t *comm;                      /* boundary after row l (R3-R5)               */
   int p, m;
   int64_t cap;                              /* M_d^capacity (Eq. 2)                       */
+  const double* costs_f64;                  /* optional [4][L] real t_f, t_b, t_w, comm:
+                                               selects the fp64 simulator                 */
 } orc_problem;
 
 typedef struct {
@@ -58,6 +60,8 @@ typedef struct {
   int64_t peak_mem;                         /* max_d M_d                                  */
   double bubble;                            /* 1 - sum busy / (p * makespan)              */
   int64_t T_d[ORC_MAXP], busy_d[ORC_MAXP], M_d[ORC_MAXP], static_d[ORC_MAXP];
+  double makespan_f;                        /* the makespan as a real number             */
+  double T_f[ORC_MAXP];
 } orc_result;
 
 /* realised per-device order of one simulation (optional output of orc_simulate) */
@@ -94,6 +98,8 @@ int  orc_fixed_order(const orc_problem* pr, const orc_plan* pl, int d,
 /* Alg. 1 Steps 1-3 for one candidate (global event loop, R9-R16). Returns 0,
  * or -1 on an internal inconsistency (a test failure). */
 int  orc_simulate(const orc_problem* pr, const orc_plan* pl, orc_result* out, orc_trace* tr);
+/* the same event loop with real-valued times (fp64) on pr->costs_f64 */
+int  orc_simulate_f64(const orc_problem* pr, const orc_plan* pl, orc_result* out, orc_trace* tr);
 /* Independent checker: longest path over the task DAG (S:141 edges) plus the
  * given per-device list-order edges, by relaxation to a fixpoint. Returns 0,
  * or 1 if the lists contain a cyclic wait. fused: B charged c_B + c_W, no W. */
@@ -114,7 +120,7 @@ int  orc_decode(const orc_problem* pr, const orc_space* sp, uint64_t index, orc_
 /* plain helpers for tests/bench */
 int  orc_eval_indices(const orc_problem* pr, const orc_space* sp, const uint64_t* idx,
                       uint64_t n, int nthreads, int64_t* makespan, int64_t* peak,
-                      double* bubble, uint8_t* status);
+                      double* bubble, uint8_t* status, double* makespan_f);
 /* exhaustive argmin of Eq. 1-2 with lowest-index tie-break (R18). prune=1
  * enables the exact lower-bound prune (skip if max_d busy_d > best, or equal
  * with a larger index) and the fixed-order memory precheck. */

@@ -18,6 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "liboracle.so")
 SRC = os.path.join(HERE, "oracle.c")
 HDR = os.path.join(HERE, "oracle.h")
+INC = os.path.join(HERE, "oracle_sim.inc")
 MAXS, MAXP = 64, 32
 INT64_MAX = (1 << 63) - 1
 UINT64_MAX = (1 << 64) - 1
@@ -29,17 +30,19 @@ _lib = None
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (plain C11 + pthreads)."""
     stale = (not os.path.exists(LIB) or
-             max(os.path.getmtime(SRC), os.path.getmtime(HDR)) > os.path.getmtime(LIB))
+             max(os.path.getmtime(f) for f in (SRC, HDR, INC)) > os.path.getmtime(LIB))
     if force or stale:
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-fPIC", "-shared", "-pthread",
-                               SRC, "-o", LIB])
+                               SRC, "-o", LIB + ".tmp", "-lm"])
+        os.replace(LIB + ".tmp", LIB)
     return LIB
 
 
 class _Problem(C.Structure):
     _fields_ = [("L", C.c_int)] + [(n, C.POINTER(C.c_int64)) for n in
                                    ("t_f", "t_b", "t_w", "act", "stash", "weight", "grad", "comm")] + \
-               [("p", C.c_int), ("m", C.c_int), ("cap", C.c_int64)]
+               [("p", C.c_int), ("m", C.c_int), ("cap", C.c_int64),
+                ("costs_f64", C.POINTER(C.c_double))]
 
 
 class _Plan(C.Structure):
@@ -50,7 +53,8 @@ class _Plan(C.Structure):
 class _Result(C.Structure):
     _fields_ = [("status", C.c_int), ("makespan", C.c_int64), ("peak_mem", C.c_int64),
                 ("bubble", C.c_double)] + [(n, C.c_int64 * MAXP) for n in
-                                           ("T_d", "busy_d", "M_d", "static_d")]
+                                           ("T_d", "busy_d", "M_d", "static_d")] + \
+               [("makespan_f", C.c_double), ("T_f", C.c_double * MAXP)]
 
 
 class _Trace(C.Structure):
@@ -103,7 +107,9 @@ def lib():
             L.orc_eval_indices.argtypes = [C.POINTER(_Problem), C.POINTER(_Space),
                                            C.POINTER(C.c_uint64), C.c_uint64, C.c_int,
                                            C.POINTER(C.c_int64), C.POINTER(C.c_int64),
-                                           C.POINTER(C.c_double), C.POINTER(C.c_uint8)]
+                                           C.POINTER(C.c_double), C.POINTER(C.c_uint8),
+                                           C.POINTER(C.c_double)]
+            L.orc_simulate_f64.argtypes = L.orc_simulate.argtypes
             L.orc_search.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.c_int, C.c_int,
                                      C.POINTER(_Best)]
             _lib = L
@@ -124,7 +130,13 @@ class _Ctx:
             a = np.ascontiguousarray(np.asarray(getattr(pr, n), dtype=np.int64))
             self.keep.append(a)
             cols[n] = _i64p(a)
-        self.pr = _Problem(L=len(pr.t_f), p=pr.p, m=pr.m, cap=int(pr.cap), **cols)
+        cf = None
+        if getattr(pr, "costs_f32", None) is not None and getattr(pr, "cost_type", 0) == 1:
+            # the fp64 reference of the fp32-cost variant reads the same fp32 values
+            a = np.ascontiguousarray(np.asarray(pr.costs_f32, dtype=np.float64))
+            self.keep.append(a)
+            cf = a.ctypes.data_as(C.POINTER(C.c_double))
+        self.pr = _Problem(L=len(pr.t_f), p=pr.p, m=pr.m, cap=int(pr.cap), costs_f64=cf, **cols)
         self.sp = None
         if sp is not None:
             s = _Space()
@@ -169,11 +181,13 @@ def simulate(pr, v, placement, policy, cuts, trace=False):
                     stage=arrs[1].ctypes.data_as(C.POINTER(C.c_int)),
                     mb=arrs[2].ctypes.data_as(C.POINTER(C.c_int)), start=_i64p(arrs[3]))
         tr_p = C.pointer(tr)
-    rc = lib().orc_simulate(C.byref(ctx.pr), C.byref(pl), C.byref(res), tr_p)
+    sim = lib().orc_simulate_f64 if ctx.pr.costs_f64 else lib().orc_simulate
+    rc = sim(C.byref(ctx.pr), C.byref(pl), C.byref(res), tr_p)
     if rc != 0:
         raise RuntimeError("oracle internal inconsistency")
     p = pr.p
     out = {"status": res.status, "makespan": res.makespan, "peak_mem": res.peak_mem,
+           "makespan_f": res.makespan_f,
            "bubble": res.bubble, "T_d": list(res.T_d[:p]), "busy_d": list(res.busy_d[:p]),
            "M_d": list(res.M_d[:p]), "static_d": list(res.static_d[:p])}
     if trace:
@@ -278,14 +292,16 @@ def eval_indices(pr, sp, indices, nthreads=None):
     n = idx.shape[0]
     ms = np.zeros(n, np.int64); pk = np.zeros(n, np.int64)
     bub = np.zeros(n, np.float64); st = np.zeros(n, np.uint8)
+    msf = np.zeros(n, np.float64)
     nth = nthreads or os.cpu_count() or 1
     rc = lib().orc_eval_indices(C.byref(ctx.pr), C.byref(ctx.sp),
                                 idx.ctypes.data_as(C.POINTER(C.c_uint64)), n, nth, _i64p(ms),
                                 _i64p(pk), bub.ctypes.data_as(C.POINTER(C.c_double)),
-                                st.ctypes.data_as(C.POINTER(C.c_uint8)))
+                                st.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                msf.ctypes.data_as(C.POINTER(C.c_double)))
     if rc != 0:
         raise RuntimeError("oracle internal inconsistency")
-    return {"makespan": ms, "peak_mem": pk, "bubble": bub, "status": st}
+    return {"makespan": ms, "peak_mem": pk, "bubble": bub, "status": st, "makespan_f": msf}
 
 
 def search(pr, sp, prune=True, nthreads=None):

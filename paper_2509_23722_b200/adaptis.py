@@ -42,7 +42,8 @@ class _Layers(C.Structure):
 class _Problem(C.Structure):
     _fields_ = [("layers", _Layers), ("p", C.c_int32), ("m", C.c_int32),
                 ("mem_cap_bytes", C.c_int64), ("tick_seconds", C.c_double),
-                ("tokens_per_microbatch", C.c_int64)]
+                ("tokens_per_microbatch", C.c_int64), ("cost_type", C.c_int32),
+                ("costs_f32", C.POINTER(C.c_float))]
 
 
 class _Group(C.Structure):
@@ -61,12 +62,13 @@ class _Plan(C.Structure):
 
 class _ResultsSoa(C.Structure):
     _fields_ = [("makespan", C.c_void_p), ("peak_mem_bytes", C.c_void_p),
-                ("bubble_ratio", C.c_void_p), ("status", C.c_void_p)]
+                ("bubble_ratio", C.c_void_p), ("status", C.c_void_p), ("makespan_f32", C.c_void_p)]
 
 
 class _Result(C.Structure):
     _fields_ = [("makespan", C.c_int64), ("peak_mem_bytes", C.c_int64),
-                ("bubble_ratio", C.c_float), ("throughput", C.c_double), ("status", C.c_uint8)]
+                ("bubble_ratio", C.c_float), ("throughput", C.c_double), ("status", C.c_uint8),
+                ("makespan_f32", C.c_float)]
 
 
 class _Best(C.Structure):
@@ -161,9 +163,15 @@ class _Marshal:
             a = np.ascontiguousarray(np.asarray(getattr(pr, src), dtype=np.int64))
             self.keep.append(a)
             ptrs[dst] = a.ctypes.data_as(C.POINTER(C.c_int64))
+        cf = None
+        if getattr(pr, "costs_f32", None) is not None:
+            a = np.ascontiguousarray(np.asarray(pr.costs_f32, dtype=np.float32))
+            self.keep.append(a)
+            cf = a.ctypes.data_as(C.POINTER(C.c_float))
         self.problem = _Problem(layers=_Layers(L=len(pr.t_f), **ptrs), p=pr.p, m=pr.m,
                                 mem_cap_bytes=int(pr.cap), tick_seconds=float(pr.tick_seconds),
-                                tokens_per_microbatch=int(pr.tokens_per_microbatch))
+                                tokens_per_microbatch=int(pr.tokens_per_microbatch),
+                                cost_type=int(getattr(pr, "cost_type", 0)), costs_f32=cf)
         self.space = None
         if sp is not None:
             s = _Space(n_groups=len(sp.groups))
@@ -354,9 +362,11 @@ class Prepared:
             out = {"makespan": torch.empty(count, dtype=torch.int64, device=dev),
                    "peak_mem": torch.empty(count, dtype=torch.int64, device=dev),
                    "bubble": torch.empty(count, dtype=torch.float32, device=dev),
-                   "status": torch.empty(count, dtype=torch.uint8, device=dev)}
+                   "status": torch.empty(count, dtype=torch.uint8, device=dev),
+                   "makespan_f32": torch.empty(count, dtype=torch.float32, device=dev)}
             soa = _ResultsSoa(out["makespan"].data_ptr(), out["peak_mem"].data_ptr(),
-                              out["bubble"].data_ptr(), out["status"].data_ptr())
+                              out["bubble"].data_ptr(), out["status"].data_ptr(),
+                              out["makespan_f32"].data_ptr())
             torch.cuda.current_stream(self.ctx.device).synchronize()
             _check(lib().adaptis_eval_prepared(self.ctx.ptr, self.ptr, first, count, C.byref(soa), 1),
                    self.ctx.ptr)
@@ -370,12 +380,14 @@ class Prepared:
 
 def _host_results(count):
     return {"makespan": np.zeros(count, np.int64), "peak_mem": np.zeros(count, np.int64),
-            "bubble": np.zeros(count, np.float32), "status": np.zeros(count, np.uint8)}
+            "bubble": np.zeros(count, np.float32), "status": np.zeros(count, np.uint8),
+            "makespan_f32": np.zeros(count, np.float32)}
 
 
 def _soa_from_numpy(out):
     return _ResultsSoa(out["makespan"].ctypes.data, out["peak_mem"].ctypes.data,
-                       out["bubble"].ctypes.data, out["status"].ctypes.data)
+                       out["bubble"].ctypes.data, out["status"].ctypes.data,
+                       out["makespan_f32"].ctypes.data)
 
 
 def _best_dict(b: _Best, st: int, ctx_ptr) -> dict:
@@ -384,6 +396,7 @@ def _best_dict(b: _Best, st: int, ctx_ptr) -> dict:
     p = b.p
     return {"status": st, "index": int(b.index), "plan": plan_dict(b.plan),
             "makespan": int(b.result.makespan), "peak_mem": int(b.result.peak_mem_bytes),
+            "makespan_f32": float(b.result.makespan_f32),
             "bubble": float(b.result.bubble_ratio), "throughput": float(b.result.throughput),
             "cand_status": int(b.result.status),
             "T_d": list(b.T_d[:p]), "busy_d": list(b.busy_d[:p]), "M_d": list(b.M_d[:p]),

@@ -54,11 +54,13 @@ struct adaptis_prepared {
   std::vector<Seg> segs;
   uint64_t N = 0;
   int key_bits = 1;
-  bool use_int64 = false;
+  int tick = kTickI32;
   std::vector<uint64_t> h_binom, h_ball;
   std::vector<int16_t> h_seeds;
   int group_v[ADAPTIS_MAX_GROUPS] = {0};
   // device
+  double* d_colsf = nullptr;
+  float* d_commf = nullptr;
   int64_t* d_cols = nullptr;
   int64_t* d_comm = nullptr;
   uint64_t* d_binom = nullptr;
@@ -130,6 +132,17 @@ adaptis_status validate(adaptis_ctx* ctx, const adaptis_problem* pr, const adapt
       if (cols[c][l] > (int64_t)1 << 52)
         return fail(ctx, ADAPTIS_EINVAL, "layers.%s[%d] > 2^52", names[c], l);
     }
+  }
+  if (pr->cost_type != ADAPTIS_COST_TICKS && pr->cost_type != ADAPTIS_COST_FP32)
+    return fail(ctx, ADAPTIS_EINVAL, "cost_type = %d", pr->cost_type);
+  if (pr->cost_type == ADAPTIS_COST_FP32 && pr->costs_f32) {
+    const char* fn[4] = {"t_f", "t_b", "t_w", "comm"};
+    for (int c = 0; c < 4; ++c)
+      for (int l = 0; l < (c == 3 ? Ly.L - 1 : Ly.L); ++l) {
+        const float x = pr->costs_f32[(size_t)c * Ly.L + l];
+        if (!(x == x) || x > 1e30f || (c < 3 && x < 1.0f) || (c == 3 && x < 0.0f))
+          return fail(ctx, ADAPTIS_EINVAL, "costs_f32.%s[%d] = %g out of range", fn[c], l, (double)x);
+      }
   }
   if (pr->p < 1 || pr->p > ADAPTIS_MAX_P) return fail(ctx, ADAPTIS_EINVAL, "p = %d not in [1, 32]", pr->p);
   if (pr->m < 1 || pr->m > 65535) return fail(ctx, ADAPTIS_EINVAL, "m = %d not in [1, 65535]", pr->m);
@@ -282,9 +295,16 @@ adaptis_status build_space(adaptis_ctx* ctx, const adaptis_problem* pr, const ad
   for (int l = 0; l < Ly.L; ++l) U += (unsigned __int128)(Ly.t_f[l] + Ly.t_b[l] + Ly.t_w[l]);
   for (int l = 0; l + 1 < Ly.L; ++l) U += 2 * (unsigned __int128)Ly.comm_ticks[l];
   U *= (unsigned __int128)pr->m;
+  if (pr->cost_type == ADAPTIS_COST_FP32) {
+    // fp32 makespans enter the key as their (order-preserving) 32-bit patterns
+    if (bits > 31) return fail(ctx, ADAPTIS_EOVERFLOW, "fp32 keys need |space| < 2^31");
+    P->tick = kTickF32;
+    return ADAPTIS_OK;
+  }
   if (bits >= 63 || U >= ((unsigned __int128)1 << (63 - bits)))
     return fail(ctx, ADAPTIS_EOVERFLOW, "makespan bound and %d index bits exceed the 63-bit key", bits);
-  P->use_int64 = U >= ((unsigned __int128)1 << 31) - 1;
+  P->tick = U >= ((unsigned __int128)1 << 31) - 1 ? kTickI64 : kTickI32;
+  if (getenv("ADAPTIS_FORCE_INT64")) P->tick = kTickI64;  // test hook: exercise the int64 path
   return ADAPTIS_OK;
 }
 
@@ -303,6 +323,23 @@ adaptis_status upload(adaptis_ctx* ctx, const adaptis_problem* pr, adaptis_prepa
   std::vector<int64_t> comm(Ly.comm_ticks, Ly.comm_ticks + L);
   comm[L - 1] = 0;
   CU(ctx, cudaSetDevice(ctx->device));
+  if (P->tick == kTickF32) {  // the fp32-cost variant's real-valued durations and latencies
+    std::vector<double> cf((size_t)3 * L);
+    std::vector<float> mf(L);
+    for (int l = 0; l < L; ++l) {
+      const float* c = pr->costs_f32;
+      cf[l] = c ? (double)c[l] : (double)(float)Ly.t_f[l];
+      cf[(size_t)L + l] = c ? (double)c[(size_t)L + l] : (double)(float)Ly.t_b[l];
+      cf[(size_t)2 * L + l] = c ? (double)c[(size_t)2 * L + l] : (double)(float)Ly.t_w[l];
+      mf[l] = l == L - 1 ? 0.0f : (c ? c[(size_t)3 * L + l] : (float)Ly.comm_ticks[l]);
+    }
+    CU(ctx, cudaMalloc(&P->d_colsf, cf.size() * 8));
+    CU(ctx, cudaMalloc(&P->d_commf, mf.size() * 4));
+    CU(ctx, cudaMemcpy(P->d_colsf, cf.data(), cf.size() * 8, cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(P->d_commf, mf.data(), mf.size() * 4, cudaMemcpyHostToDevice));
+    P->tabs.colsf = P->d_colsf;
+    P->tabs.commf = P->d_commf;
+  }
   CU(ctx, cudaMalloc(&P->d_cols, cols.size() * 8));
   CU(ctx, cudaMalloc(&P->d_comm, comm.size() * 8));
   CU(ctx, cudaMalloc(&P->d_binom, P->h_binom.size() * 8));
@@ -376,7 +413,7 @@ constexpr size_t kGreedySmemRing = 0;  // per warp: GREEDY rings live in global 
 // global-memory ring scratch for a launch with s.ring_k slots; bounds the grid
 adaptis_status ensure_gring(adaptis_ctx* ctx, const adaptis_prepared* P, const SegLaunch& s,
                             unsigned* grid_limit) {
-  const size_t tsz = P->use_int64 ? 8 : 4;
+  const size_t tsz = P->tick == kTickI64 ? 8 : 4;
   const size_t per_warp = (size_t)2 * s.ring_k * s.G * s.S * tsz;
   const size_t budget = (size_t)1 << 30;
   unsigned gl = (unsigned)std::max<size_t>(1, budget / (per_warp * kWarpsPerCta));
@@ -403,7 +440,7 @@ SegLaunch make_launch(const adaptis_prepared* P, const Seg& sg) {
   s.seg_base = sg.base;
   s.key_bits = P->key_bits;
   s.ring_k = ring_slots(sg.policy, P->m);
-  s.use_int64 = P->use_int64 ? 1 : 0;
+  s.tick = P->tick;
   return s;
 }
 
@@ -446,6 +483,7 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     if (!mode_search && dout) {
       s.out_makespan = dout->makespan; s.out_peak = dout->peak_mem_bytes;
       s.out_bubble = dout->bubble_ratio; s.out_status = dout->status;
+      s.out_makespan_f32 = dout->makespan_f32;
     }
     s.out_report = report;
     s.cursor = sw + 0;
@@ -457,7 +495,7 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     s.n_rounds = W + 3;
     // GREEDY rings hold all m items (its F-first rule can run m items ahead);
     // they live in global memory when they do not fit the shared-memory budget
-    const size_t ring_bytes = (size_t)2 * s.ring_k * s.G * s.S * (P->use_int64 ? 8 : 4);
+    const size_t ring_bytes = (size_t)2 * s.ring_k * s.G * s.S * (P->tick == kTickI64 ? 8 : 4);
     static const size_t greedy_smem_ring =
         getenv("ADAPTIS_GREEDY_SMEM_RING") ? (size_t)atol(getenv("ADAPTIS_GREEDY_SMEM_RING")) : kGreedySmemRing;
     const bool direct_global = s.policy == ADAPTIS_GREEDY && ring_bytes > greedy_smem_ring;
@@ -663,7 +701,7 @@ adaptis_status adaptis_prepare(adaptis_ctx* ctx, const adaptis_problem* problem,
 
 void adaptis_prepared_free(adaptis_prepared* P) {
   if (!P) return;
-  cudaFree(P->d_cols); cudaFree(P->d_comm); cudaFree(P->d_binom); cudaFree(P->d_ball);
+  cudaFree(P->d_cols); cudaFree(P->d_comm); cudaFree(P->d_colsf); cudaFree(P->d_commf); cudaFree(P->d_binom); cudaFree(P->d_ball);
   cudaFree(P->d_seeds);
   delete P;
 }
@@ -679,12 +717,13 @@ adaptis_status adaptis_eval_prepared(adaptis_ctx* ctx, adaptis_prepared* P, uint
   if (count == 0) return ADAPTIS_OK;
   CU(ctx, cudaSetDevice(ctx->device));
   adaptis_results_soa dout = *out;
-  void* tmp[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* tmp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   if (!out_on_device) {
     if (out->makespan) { CU(ctx, cudaMalloc(&tmp[0], count * 8)); dout.makespan = (int64_t*)tmp[0]; }
     if (out->peak_mem_bytes) { CU(ctx, cudaMalloc(&tmp[1], count * 8)); dout.peak_mem_bytes = (int64_t*)tmp[1]; }
     if (out->bubble_ratio) { CU(ctx, cudaMalloc(&tmp[2], count * 4)); dout.bubble_ratio = (float*)tmp[2]; }
     if (out->status) { CU(ctx, cudaMalloc(&tmp[3], count)); dout.status = (uint8_t*)tmp[3]; }
+    if (out->makespan_f32) { CU(ctx, cudaMalloc(&tmp[4], count * 4)); dout.makespan_f32 = (float*)tmp[4]; }
   }
   adaptis_status st = run_range(ctx, P, first, first + count, false, 0, 1, &dout, first, nullptr, nullptr);
   if (st == ADAPTIS_OK && !out_on_device) {
@@ -692,6 +731,7 @@ adaptis_status adaptis_eval_prepared(adaptis_ctx* ctx, adaptis_prepared* P, uint
     if (out->peak_mem_bytes) CU(ctx, cudaMemcpyAsync(out->peak_mem_bytes, tmp[1], count * 8, cudaMemcpyDeviceToHost, ctx->stream));
     if (out->bubble_ratio) CU(ctx, cudaMemcpyAsync(out->bubble_ratio, tmp[2], count * 4, cudaMemcpyDeviceToHost, ctx->stream));
     if (out->status) CU(ctx, cudaMemcpyAsync(out->status, tmp[3], count, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->makespan_f32) CU(ctx, cudaMemcpyAsync(out->makespan_f32, tmp[4], count * 4, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
   }
   for (void* t : tmp) if (t) cudaFree(t);
@@ -751,35 +791,42 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   fill_plan(*P, idx, &out->plan, nullptr);
   // winner report: the same kernel on the single winning index
   std::vector<int64_t> rep(3 * P->p);
-  int64_t mk = 0, pk = 0; float bub = 0; uint8_t stt = 0;
-  int64_t *dmk = nullptr, *dpk = nullptr; float* dbub = nullptr; uint8_t* dst = nullptr;
-  CU(ctx, cudaMalloc(&dmk, 8)); CU(ctx, cudaMalloc(&dpk, 8)); CU(ctx, cudaMalloc(&dbub, 4)); CU(ctx, cudaMalloc(&dst, 1));
-  adaptis_results_soa so{dmk, dpk, dbub, dst};
+  int64_t mk = 0, pk = 0; float bub = 0, mkf = 0; uint8_t stt = 0;
+  int64_t *dmk = nullptr, *dpk = nullptr; float *dbub = nullptr, *dmkf = nullptr; uint8_t* dst = nullptr;
+  CU(ctx, cudaMalloc(&dmk, 8)); CU(ctx, cudaMalloc(&dpk, 8)); CU(ctx, cudaMalloc(&dbub, 4));
+  CU(ctx, cudaMalloc(&dst, 1)); CU(ctx, cudaMalloc(&dmkf, 4));
+  adaptis_results_soa so{dmk, dpk, dbub, dst, dmkf};
   st = run_range(ctx, P, idx, idx + 1, false, 0, 1, &so, idx, ctx->d_report, nullptr);
   if (st == ADAPTIS_OK) {
     CU(ctx, cudaMemcpyAsync(&mk, dmk, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(&pk, dpk, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(&bub, dbub, 4, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(&stt, dst, 1, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(&mkf, dmkf, 4, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(rep.data(), ctx->d_report, rep.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
   }
-  cudaFree(dmk); cudaFree(dpk); cudaFree(dbub); cudaFree(dst);
+  cudaFree(dmk); cudaFree(dpk); cudaFree(dbub); cudaFree(dst); cudaFree(dmkf);
   ctx->last_info = search_info;  // report the search's launches, not the re-evaluation
   if (st != ADAPTIS_OK) return st;
   out->result.makespan = mk;
   out->result.peak_mem_bytes = pk;
   out->result.bubble_ratio = bub;
   out->result.status = stt;
-  out->result.throughput = (mk > 0 && P->tick_seconds > 0)
-      ? (double)P->m * (double)P->tokens_per_mb / ((double)mk * P->tick_seconds) : 0.0;
+  out->result.makespan_f32 = P->tick == kTickF32 ? mkf : (float)mk;
+  const double mkd = P->tick == kTickF32 ? (double)mkf : (double)mk;
+  out->result.throughput = (mkd > 0 && P->tick_seconds > 0)
+      ? (double)P->m * (double)P->tokens_per_mb / (mkd * P->tick_seconds) : 0.0;
   for (int d = 0; d < P->p; ++d) {
     out->T_d[d] = rep[d];
     out->busy_d[d] = rep[P->p + d];
     out->M_d[d] = rep[2 * P->p + d];
   }
-  if (mk != (int64_t)(key >> P->key_bits))
-    return fail(ctx, ADAPTIS_ECUDA, "winner re-evaluation disagrees with its search key");
+  const unsigned long long kv = key >> P->key_bits;
+  bool agree;
+  if (P->tick == kTickF32) { float f; uint32_t u = (uint32_t)kv; memcpy(&f, &u, 4); agree = f == mkf; }
+  else agree = mk == (int64_t)kv;
+  if (!agree) return fail(ctx, ADAPTIS_ECUDA, "winner re-evaluation disagrees with its search key");
   return ADAPTIS_OK;
 }
 

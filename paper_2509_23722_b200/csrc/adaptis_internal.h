@@ -9,6 +9,7 @@
 namespace adaptis {
 
 constexpr int kChunkBits = 16;  // block-cyclic shard chunk = 65536 indices
+constexpr int kTickI32 = 0, kTickI64 = 1, kTickF32 = 2;
 constexpr int kNumCols = 6;     // prefix columns: t_f, t_b, t_w, act, stash, weight+grad
 constexpr int kColTF = 0, kColTB = 1, kColTW = 2, kColAct = 3, kColStash = 4, kColWG = 5;
 constexpr int kRingK = 8;       // fast-path ring slots per stage and direction (power of two)
@@ -23,6 +24,8 @@ struct DevTables {
   const uint64_t* binom;    // [kMaxBinomN][ADAPTIS_MAX_S + 1], saturating
   const uint64_t* ball;     // [n_groups][ADAPTIS_MAX_S][kMaxRadius + 1]
   const int16_t* seeds;     // [n_groups][ADAPTIS_MAX_S]  (interior cuts of the BALL seed)
+  const double* colsf;      // FP32 cost mode: [3][L] t_f, t_b, t_w as real ticks
+  const float* commf;       // FP32 cost mode: [L] comm as real ticks
 };
 
 // One launch = one (group, combo) segment of the canonical order (R19),
@@ -49,6 +52,7 @@ struct SegLaunch {
   int64_t* out_peak;
   float* out_bubble;
   uint8_t* out_status;
+  float* out_makespan_f32;
   int64_t* out_report;          // optional [3][p]: T_d, busy_d, M_d (single candidate)
   unsigned long long* cursor;   // work-claim counter (zeroed per launch)
   unsigned int* overflow_count; // candidates whose fast-path rings filled up
@@ -61,7 +65,7 @@ struct SegLaunch {
   const uint64_t* list_idx;
   int ring_k;                   // ring slots (fast path: kRingK; fallback: >= m)
   int64_t* gring;               // fallback: global ring scratch
-  int use_int64;                // 0: int32 ticks (host-proved bound), 1: int64 ticks
+  int tick;                     // kTickI32 (host-proved bound), kTickI64, kTickF32 (fp32 variant)
 };
 
 #ifdef __CUDACC__

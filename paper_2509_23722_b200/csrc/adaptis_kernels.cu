@@ -23,6 +23,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "adaptis_decode.cuh"
 #include "adaptis_internal.h"
@@ -36,6 +37,14 @@ constexpr int kGreedyCommits = 1; // GREEDY tasks a lane may commit per round (m
 template <typename T> struct TT;
 template <> struct TT<int32_t> { static constexpr int32_t INF = INT32_MAX; };
 template <> struct TT<int64_t> { static constexpr int64_t INF = INT64_MAX; };
+template <> struct TT<float> { static constexpr float INF = __builtin_huge_valf(); };
+// busy-time accumulator and integer rounding per tick type
+template <typename T> struct Acc { using type = int64_t; };
+template <> struct Acc<float> { using type = double; };
+__device__ __forceinline__ int64_t to_ticks(int32_t x) { return x; }
+__device__ __forceinline__ int64_t to_ticks(int64_t x) { return x; }
+__device__ __forceinline__ int64_t to_ticks(float x) { return llrintf(x); }
+__device__ __forceinline__ int64_t to_ticks(double x) { return llrint(x); }
 
 template <typename T>
 struct __align__(16) Rec {  // one task kind of one own stage (chunk) of a lane
@@ -76,7 +85,8 @@ __device__ __forceinline__ X seg_sum(X v, int p2) {
 }
 template <typename T>
 __device__ __forceinline__ T sat_add(T a, T b) {
-  return a > TT<T>::INF - b ? TT<T>::INF : a + b;
+  if constexpr (std::is_floating_point<T>::value) return a + b;  // inf saturates
+  else return a > TT<T>::INF - b ? TT<T>::INF : a + b;
 }
 
 // incremental position in Megatron's virtual order (R10): k -> (chunk, mb)
@@ -147,9 +157,30 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int L = sl.L, p = sl.p, m = sl.m, S = sl.S, p2 = sl.p2, G = sl.G;
 
-  // ---- a2 prologue: per-CTA prefix table of the layer columns (warp-shuffle scan)
+  constexpr bool FP = std::is_floating_point<T>::value;
+  using BT = typename Acc<T>::type;
+  // ---- a2 prologue: per-CTA prefix table of the layer columns (warp-shuffle scan);
+  // in the fp32-cost variant the three duration columns are real-valued (double sums)
   int64_t* pre = reinterpret_cast<int64_t*>(smem);
+  double* pref = reinterpret_cast<double*>(smem);
   for (int col = warp; col < kNumCols; col += kWarpsPerCta) {
+    if (FP && col < 3) {
+      double carry = 0;
+      const double* src = tab.colsf + (size_t)col * L;
+      double* dst = pref + (size_t)col * (L + 1);
+      if (lane == 0) dst[0] = 0;
+      for (int b = 0; b < L; b += 32) {
+        double x = (b + lane < L) ? src[b + lane] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(FULLMASK, x, o);
+          if (lane >= o) x += y;
+        }
+        if (b + lane < L) dst[b + lane + 1] = carry + x;
+        carry += __shfl_sync(FULLMASK, x, 31);
+      }
+      continue;
+    }
     int64_t carry = 0;
     const int64_t* src = tab.cols + (size_t)col * L;
     int64_t* dst = pre + (size_t)col * (L + 1);
@@ -166,6 +197,15 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
     }
   }
   __syncthreads();
+  // stage sum of a duration column over rows [a, b) and an edge latency, per tick type
+  auto dsum = [&](int col, int a, int b) -> BT {
+    if constexpr (FP) return pref[col * (L + 1) + b] - pref[col * (L + 1) + a];
+    else return pre[col * (L + 1) + b] - pre[col * (L + 1) + a];
+  };
+  auto lat = [&](int row) -> T {
+    if constexpr (FP) return tab.commf[row];
+    else return (T)tab.comm[row];
+  };
 
   // ---- per-warp shared regions (layout mirrored by smem_bytes())
   const WarpLayout lay =
@@ -206,7 +246,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   int flags = 0;        // slot-uniform F_* bits
   uint64_t idx = 0;
   T free_t = 0;
-  int64_t dyn = 0, peak = 0, busy = 0, stat = 0;
+  int64_t dyn = 0, peak = 0, stat = 0;
+  BT busy = 0;
   T window = INF;
   // fixed orders
   int nF = 0, nB = 0, nW = 0;
@@ -243,8 +284,9 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   auto finalize = [&](bool fl) {
     if (fl) { wtasks += ctasks; wlive += clive; ctasks = 0; clive = 0; }
     const bool contrib = fl && dev_lane;
-    const int64_t mk = seg_max(contrib ? (int64_t)free_t : (int64_t)0, p2);
-    const int64_t sb = seg_sum(contrib ? busy : (int64_t)0, p2);
+    const T mkT = seg_max(contrib ? free_t : (T)0, p2);
+    const int64_t mk = to_ticks(mkT);
+    const BT sb = seg_sum(contrib ? busy : (BT)0, p2);
     const int64_t Md = stat + peak;
     const int64_t Mmax = seg_max(contrib ? Md : (int64_t)0, p2);
     const bool anyover = (__ballot_sync(FULLMASK, contrib && Md > sl.cap) & smask) != 0;
@@ -263,24 +305,28 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         if (status == ADAPTIS_CAND_INVALID) ++winvalid;
         if (sl.key) {
           if (status == ADAPTIS_CAND_OK) {
-            const unsigned long long key = ((unsigned long long)mk << sl.key_bits) | idx;
+            unsigned long long kv;  // order-preserving: fp32 bits of a positive float
+            if constexpr (FP) kv = (unsigned long long)__float_as_uint(mkT);
+            else kv = (unsigned long long)mk;
+            const unsigned long long key = (kv << sl.key_bits) | idx;
             wkey = key < wkey ? key : wkey;
           }
         } else {
           const uint64_t o = idx - sl.eval_first;
           if (sl.out_status) sl.out_status[o] = (uint8_t)status;
           if (sl.out_makespan) sl.out_makespan[o] = status == 0 ? mk : INT64_MAX;
+          if (sl.out_makespan_f32) sl.out_makespan_f32[o] = status == 0 ? (float)mkT : INFINITY;
           if (sl.out_peak)
             sl.out_peak[o] = (status == 0 || status == ADAPTIS_CAND_OVER_CAP) ? Mmax : 0;
           if (sl.out_bubble)
             sl.out_bubble[o] =
-                status == 0 ? (float)(1.0 - (double)sb / ((double)p * (double)mk)) : 0.0f;
+                status == 0 ? (float)(1.0 - (double)sb / ((double)p * (double)mkT)) : 0.0f;
         }
       }
     }
     if (sl.out_report && contrib && status >= 0) {
-      sl.out_report[d] = (int64_t)free_t;
-      sl.out_report[p + d] = busy;
+      sl.out_report[d] = to_ticks(free_t);
+      sl.out_report[p + d] = to_ticks(busy);
       sl.out_report[2 * p + d] = Md;
     }
   };
@@ -340,20 +386,20 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             for (int c = 0; c < V; ++c) {
               const int s = stage_of(sl.placement, p, c, d);
               const int a = cuts[s], b = cuts[s + 1];
-              const int64_t cF = pre[kColTF * (L + 1) + b] - pre[kColTF * (L + 1) + a];
-              const int64_t cB = pre[kColTB * (L + 1) + b] - pre[kColTB * (L + 1) + a];
-              const int64_t cW = pre[kColTW * (L + 1) + b] - pre[kColTW * (L + 1) + a];
+              const BT cF = dsum(kColTF, a, b);
+              const BT cB = dsum(kColTB, a, b);
+              const BT cW = dsum(kColTW, a, b);
               const int64_t act = pre[kColAct * (L + 1) + b] - pre[kColAct * (L + 1) + a];
               const int64_t sta = pre[kColStash * (L + 1) + b] - pre[kColStash * (L + 1) + a];
               stat += pre[kColWG * (L + 1) + b] - pre[kColWG * (L + 1) + a];
-              busy += (int64_t)m * (cF + cB + cW);
+              busy += (BT)m * (cF + cB + cW);
               T oF = 0, oB = 0;
               if (s < S - 1 && dev_of(sl.placement, p, s + 1) != d) {
-                oF = (T)tab.comm[b - 1];
+                oF = lat(b - 1);
                 cmin = oF < cmin ? oF : cmin;
               }
               if (s > 0 && dev_of(sl.placement, p, s - 1) != d) {
-                oB = (T)tab.comm[a - 1];
+                oB = lat(a - 1);
                 cmin = oB < cmin ? oB : cmin;
               }
               T mn = (T)cF < (T)cB ? (T)cF : (T)cB;
@@ -384,12 +430,12 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
                 bool fl = true, bl = false;
                 if (s > 0 && dev_of(sl.placement, p, s - 1) != d) {
                   const int a0 = cuts[s - 1];
-                  pf = (T)(pre[kColTF * (L + 1) + a] - pre[kColTF * (L + 1) + a0]) + (T)tab.comm[a - 1];
+                  pf = (T)dsum(kColTF, a0, a) + lat(a - 1);
                   fl = dev_of(sl.placement, p, s - 1) == (d == 0 ? p - 1 : d - 1);
                 }
                 if (s < S - 1 && dev_of(sl.placement, p, s + 1) != d) {
                   const int b1 = cuts[s + 2];
-                  pb = (T)(pre[kColTB * (L + 1) + b1] - pre[kColTB * (L + 1) + b]) + (T)tab.comm[b - 1];
+                  pb = (T)dsum(kColTB, b, b1) + lat(b - 1);
                   bl = dev_of(sl.placement, p, s + 1) == (d == 0 ? p - 1 : d - 1);
                 }
                 pFc[c] = pf;
@@ -669,8 +715,9 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
 
 // ------------------------------------------------------------------------------
 static WarpLayout host_layout(const SegLaunch& s, bool gring) {
-  const int tsz = s.use_int64 ? 8 : 4;
-  const int rsz = s.use_int64 ? (int)sizeof(Rec<int64_t>) : (int)sizeof(Rec<int32_t>);
+  const int tsz = s.tick == kTickI64 ? 8 : 4;
+  const int rsz = s.tick == kTickI64 ? (int)sizeof(Rec<int64_t>)
+                : s.tick == kTickF32 ? (int)sizeof(Rec<float>) : (int)sizeof(Rec<int32_t>);
   return warp_layout(s.S, s.G, s.v, s.ring_k, tsz, rsz, gring);
 }
 
@@ -704,7 +751,9 @@ static KFn pick_pol(int pol, int v, bool fb) {
   }
 }
 static KFn pick(const SegLaunch& s, bool fb) {
-  return s.use_int64 ? pick_pol<int64_t>(s.policy, s.v, fb) : pick_pol<int32_t>(s.policy, s.v, fb);
+  if (s.tick == kTickI64) return pick_pol<int64_t>(s.policy, s.v, fb);
+  if (s.tick == kTickF32) return pick_pol<float>(s.policy, s.v, fb);
+  return pick_pol<int32_t>(s.policy, s.v, fb);
 }
 
 int occupancy_ctas_per_sm(const SegLaunch& s, bool fallback) {

@@ -74,10 +74,14 @@ class Problem:
     tick_seconds: float = 1e-6
     tokens_per_microbatch: int = 4096
     name: str = ""
+    cost_type: int = 0                   # 0: exact int64 ticks, 1: fp32-cost variant
+    costs_f32: Optional[np.ndarray] = None  # fp32 variant: [4][L] t_f, t_b, t_w, comm
 
     def __post_init__(self):
         for c in COLUMNS:
             setattr(self, c, np.ascontiguousarray(np.asarray(getattr(self, c), dtype=np.int64)))
+        if self.costs_f32 is not None:
+            self.costs_f32 = np.ascontiguousarray(np.asarray(self.costs_f32, dtype=np.float32))
 
     @property
     def L(self) -> int:
@@ -178,6 +182,17 @@ def cfg1_unit() -> Problem:
     z = [0] * 8
     return Problem(t_f=t_f, t_b=list(t_f), t_w=t_w, act=z, stash=z, weight=z, grad=z,
                    comm=[1] * 7 + [0], p=2, m=4, name="cfg1-unit")
+
+
+def fractional_costs(pr: "Problem", rng: SplitMix64, denom: int = 8) -> np.ndarray:
+    """[4][L] fp32 costs for the fp32 variant: each tick value plus a seeded
+    fraction k/denom (durations stay >= 1)."""
+    out = np.zeros((4, pr.L), np.float32)
+    for ci, col in enumerate((pr.t_f, pr.t_b, pr.t_w, pr.comm)):
+        for l in range(pr.L):
+            out[ci, l] = np.float32(float(col[l]) + (rng.next() % denom) / denom)
+    out[3, pr.L - 1] = 0.0
+    return out
 
 
 def random_problem(rng: SplitMix64, L: int, p: int, m: int, *, tmax: int = 9,

@@ -183,3 +183,88 @@ def test_device_resident_eval_matches_host(ctx):
     for k in ("makespan", "peak_mem", "status"):
         assert np.array_equal(a[k], b[k].cpu().numpy())
     prep.close()
+
+
+# ----------------------------------------------------------------- the int64 tick path
+def test_int64_tick_path_matches_oracle(ctx, monkeypatch):
+    """Force the int64 kernels (used when the makespan bound exceeds 2^31)."""
+    monkeypatch.setenv("ADAPTIS_FORCE_INT64", "1")
+    pr, sp = W.config(1)
+    got, want = _eval_range(ctx, pr, sp, 0, O.space_size(pr, sp))
+    _compare(got, want, "cfg1 int64")
+    for pr, sp in _random_spaces(9, 6):
+        N = O.space_size(pr, sp)
+        got, want = _eval_range(ctx, pr, sp, 0, N)
+        _compare(got, want, "int64 p=%d m=%d" % (pr.p, pr.m))
+
+
+def test_large_ticks_select_int64_and_match(ctx):
+    """Costs so large that U >= 2^31: the library picks int64 ticks by itself."""
+    rng = W.SplitMix64(77)
+    pr = W.random_problem(rng, 9, 2, 4, tmax=9, cmax=5, bytes_max=9)
+    for c in ("t_f", "t_b", "t_w", "comm"):
+        setattr(pr, c, getattr(pr, c) * (1 << 26) + 1)
+    sp = W.Space([W.Group(1, W.FULL, combo_mask=0xF), W.Group(2, W.FULL, combo_mask=0x3F)])
+    got, want = _eval_range(ctx, pr, sp, 0, O.space_size(pr, sp))
+    _compare(got, want, "large ticks")
+    assert want["makespan"][want["status"] == 0].max() > (1 << 31)
+
+
+# ----------------------------------------------------------------- the fp32-cost variant
+FP32_RTOL = 1e-5  # north_star: "within 1e-5 relative for the fp32-cost variant"
+
+
+def _fp32_problem(pr, seed):
+    return W.Problem(**{c: getattr(pr, c) for c in W.COLUMNS}, p=pr.p, m=pr.m, cap=pr.cap,
+                     cost_type=1, costs_f32=W.fractional_costs(pr, W.SplitMix64(seed)))
+
+
+def _compare_fp32(got, want, where):
+    st_g, st_w = np.asarray(got["status"]), np.asarray(want["status"])
+    ok = (st_w == 0) & (st_g == 0)
+    g = np.asarray(got["makespan_f32"], np.float64)[ok]
+    w = np.asarray(want["makespan_f"])[ok]
+    rel = np.abs(g - w) / w
+    assert ok.sum() >= 0.9 * (st_w == 0).sum(), where + ": status disagreements"
+    assert np.all(rel <= FP32_RTOL), "%s: max rel %.3g at %s" % (where, rel.max(), np.argmax(rel))
+    return int(ok.sum()), float(rel.max() if rel.size else 0.0)
+
+
+@pytest.mark.parametrize("cid,first,count", [(1, 0, 244), (2, 123456, 4096), (3, 9_173_505, 2048),
+                                             (3, 85_357_574, 2048), (3, 115_000_000, 1024),
+                                             (5, 100_000_000, 256), (5, 300_000_000, 128)])
+def test_fp32_variant_within_tolerance(ctx, cid, first, count):
+    """Dyadic fractional costs (k/8 ticks): every makespan within 1e-5 of fp64."""
+    pr, sp = W.config(cid)
+    prf = _fp32_problem(pr, 100 + cid)
+    got = ctx.eval_batch(prf, sp, first, count)
+    want = O.eval_indices(prf, sp, range(first, first + count))
+    n, mx = _compare_fp32(got, want, "cfg%d fp32" % cid)
+    assert n > 0
+
+
+def test_fp32_variant_nondyadic_costs(ctx):
+    """Costs k/7 are not representable in fp32. Fixed orders (no time-dependent
+    decisions) stay within 1e-5; ZB / GREEDY may resolve a real-arithmetic tie
+    differently from fp64 (R27), which must stay rare."""
+    from paper_2509_23722_b200 import adaptis as A
+    pr, sp = W.config(1)
+    prf = _fp32_problem(pr, 3)
+    prf.costs_f32 = W.fractional_costs(pr, W.SplitMix64(3), denom=7)
+    N = O.space_size(prf, sp)
+    got = ctx.eval_batch(prf, sp, 0, N)
+    want = O.eval_indices(prf, sp, range(N))
+    fixed = np.array([A.decode(pr, sp, i)["policy"] in (W.GPIPE, W.ONEF1B) for i in range(N)])
+    ok = (np.asarray(want["status"]) == 0) & (np.asarray(got["status"]) == 0)
+    rel = np.abs(np.asarray(got["makespan_f32"], np.float64) - want["makespan_f"]) / want["makespan_f"]
+    assert np.all(rel[ok & fixed] <= FP32_RTOL)
+    assert np.mean(rel[ok & ~fixed] <= FP32_RTOL) >= 0.95
+
+
+def test_fp32_search_winner_within_tolerance(ctx):
+    pr, sp = W.config(1)
+    prf = _fp32_problem(pr, 7)
+    b = ctx.search(prf, sp)
+    want = O.eval_indices(prf, sp, range(O.space_size(prf, sp)))
+    best = np.min(want["makespan_f"][want["status"] == 0])
+    assert b["makespan_f32"] <= best * (1 + FP32_RTOL)  # T7: the winner is within 1e-5 of the optimum

@@ -11,6 +11,7 @@ import math
 import os
 from fractions import Fraction
 
+import numpy as np
 import pytest
 
 from oracle import oracle as O
@@ -340,3 +341,38 @@ def test_cfg1_unit_advisory_golden():
     evl = O.eval_indices(pr, lit, range(165))
     ties = [i for i in range(165) if evl["makespan"][i] == 218]
     assert ties == g["literal_three_policy"]["tied_indices"]
+
+
+# ---------------------------------------------------------------- fp64 reference of the fp32 variant
+def test_f64_event_loop_equals_int64_on_integer_costs():
+    """The fp64 simulator on integer-valued costs reproduces the exact int64 one."""
+    rng = W.SplitMix64(555)
+    for _ in range(120):
+        p = 1 + rng.next() % 4
+        m = p * (1 + rng.next() % 2)
+        L = 2 * p + 1 + rng.next() % 3
+        pr = W.random_problem(rng, L, p, m, bytes_max=6, cap=W.INT64_MAX if rng.next() % 2 else 80)
+        prf = W.Problem(**{c: getattr(pr, c) for c in W.COLUMNS}, p=p, m=m, cap=pr.cap, cost_type=1,
+                        costs_f32=np.stack([pr.t_f, pr.t_b, pr.t_w, pr.comm]).astype(np.float32))
+        cuts = sorted(set(range(1, L)) - {int(1 + rng.next() % (L - 1))})[: 2 * p - 1]
+        v, placement = (2, W.INTERLEAVED) if len(cuts) == 2 * p - 1 else (1, W.SEQ)
+        if v == 1:
+            cuts = list(range(1, p))
+        for pol in range(4):
+            a = O.simulate(pr, v, placement, pol, cuts)
+            b = O.simulate(prf, v, placement, pol, cuts)
+            assert (a["status"], a["makespan"], a["peak_mem"]) == (b["status"], b["makespan"], b["peak_mem"])
+            if a["status"] == 0:
+                assert b["makespan_f"] == float(a["makespan"])
+
+
+@pytest.mark.parametrize("p,m", [(2, 4), (4, 8)])
+def test_f64_closed_forms_with_fractional_costs(p, m):
+    """GPipe and S-1F1B closed forms hold for real costs (dyadic, exact in fp64)."""
+    tf, tb, tw = 1.25, 2.5, 1.125
+    pr = homo(p, p, m, 1, 1, 1)
+    prf = W.Problem(**{c: getattr(pr, c) for c in W.COLUMNS}, p=p, m=m, cost_type=1,
+                    costs_f32=np.array([[tf] * p, [tb] * p, [tw] * p, [0.0] * p], np.float32))
+    g = O.simulate(prf, 1, W.SEQ, W.GPIPE, seq_cuts(p))
+    o = O.simulate(prf, 1, W.SEQ, W.ONEF1B, seq_cuts(p))
+    assert g["makespan_f"] == (m + p - 1) * (tf + tb + tw) == o["makespan_f"]
