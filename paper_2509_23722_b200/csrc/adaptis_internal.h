@@ -79,19 +79,21 @@ struct SegLaunch {
 // (split policies), the slots' cuts, and the fast-path rings
 // [2 directions][K slots][G*S stages].
 struct WarpLayout {
-  int rec_off, dmem_off, cuts_off, cnt_off, ring_off, per_warp;
+  int rec_off, dmem_off, cuts_off, cnt_off, gaux_off, ring_off, per_warp;
   ADAPTIS_LAYOUT_HD size_t prefix_bytes(int L) const {
     return ((size_t)kNumCols * (L + 1) * 8 + 15) & ~(size_t)15;
   }
 };
 ADAPTIS_LAYOUT_HD int align16(int x) { return (x + 15) & ~15; }
-ADAPTIS_LAYOUT_HD WarpLayout warp_layout(int S, int G, int V, int K, int tsz, int rsz, bool gring) {
+ADAPTIS_LAYOUT_HD WarpLayout warp_layout(int S, int G, int V, int K, int tsz, int rsz, bool gring,
+                                         int gaux_sz = 0) {
   WarpLayout l;
   int off = 0;
   l.rec_off = off;  off += 3 * V * 32 * rsz;
   l.dmem_off = off; off += 3 * V * 32 * 8;
   l.cuts_off = off; off += align16(G * (S + 1) * 2);
   l.cnt_off = off;  off += 32 * 4 * 4;  // GREEDY produced-count words [lane][chunk]
+  l.gaux_off = off; off += align16(V * 32 * gaux_sz);  // GREEDY per-chunk statics
   l.ring_off = off; if (!gring) off += 2 * K * G * S * tsz;
   l.per_warp = align16(off);
   return l;

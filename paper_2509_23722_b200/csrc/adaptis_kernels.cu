@@ -32,7 +32,7 @@ namespace adaptis {
 
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr int kQueueBlock = 64;  // positions claimed per warp atomic
-constexpr int kGreedyCommits = 1; // GREEDY tasks a lane may commit per round (more is slower)
+constexpr unsigned kTstarEvery = 1; // GREEDY t* refresh period (a stale t* costs more commits than it saves)
 
 template <typename T> struct TT;
 template <> struct TT<int32_t> { static constexpr int32_t INF = INT32_MAX; };
@@ -54,6 +54,13 @@ struct __align__(16) Rec {  // one task kind of one own stage (chunk) of a lane
   int out_off;  // ring offset of the output slot row, -1 = no successor
 };
 
+template <typename T>
+struct GAux {      // GREEDY statics of one (lane, chunk), read off the critical path
+  int64_t gate;    // F of the chunk fits under Eq. 2 iff dyn <= gate (R14)
+  int32_t tF, tB;  // consumer (lane << 3 | chunk) of the F / B output, -1: none
+  T pF, pB;        // cost of the cross-device predecessor of an unknown F / B head
+};
+
 enum : int { F_INVALID = 1, F_PREOVER = 2, F_STUCK = 4, F_OVERFLOW = 8 };
 
 __device__ __forceinline__ int stage_of(int placement, int p, int c, int d) {
@@ -68,25 +75,38 @@ __device__ __forceinline__ int dev_of(int placement, int p, int s) {
   return (c & 1) ? p - 1 - j : j;
 }
 
+// segmented reductions over aligned groups of p2 lanes (p2 is warp-uniform, so
+// the unrolled steps are uniform predicates, not a runtime loop)
 template <typename X>
 __device__ __forceinline__ X seg_max(X v, int p2) {
-  for (int o = 1; o < p2; o <<= 1) { X w = __shfl_xor_sync(FULLMASK, v, o); v = w > v ? w : v; }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+    if (o < p2) { X w = __shfl_xor_sync(FULLMASK, v, o); v = w > v ? w : v; }
   return v;
 }
 template <typename X>
 __device__ __forceinline__ X seg_min(X v, int p2) {
-  for (int o = 1; o < p2; o <<= 1) { X w = __shfl_xor_sync(FULLMASK, v, o); v = w < v ? w : v; }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+    if (o < p2) { X w = __shfl_xor_sync(FULLMASK, v, o); v = w < v ? w : v; }
   return v;
 }
 template <typename X>
 __device__ __forceinline__ X seg_sum(X v, int p2) {
-  for (int o = 1; o < p2; o <<= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+    if (o < p2) v += __shfl_xor_sync(FULLMASK, v, o);
   return v;
 }
 template <typename T>
 __device__ __forceinline__ T sat_add(T a, T b) {
-  if constexpr (std::is_floating_point<T>::value) return a + b;  // inf saturates
-  else return a > TT<T>::INF - b ? TT<T>::INF : a + b;
+  if constexpr (std::is_floating_point<T>::value) {
+    return a + b;  // inf saturates
+  } else {  // a, b in [0, INF]: the unsigned sum cannot wrap
+    using U = typename std::make_unsigned<T>::type;
+    const U x = (U)a + (U)b;
+    return x < (U)TT<T>::INF ? (T)x : TT<T>::INF;
+  }
 }
 
 // incremental position in Megatron's virtual order (R10): k -> (chunk, mb)
@@ -208,13 +228,14 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   };
 
   // ---- per-warp shared regions (layout mirrored by smem_bytes())
-  const WarpLayout lay =
-      warp_layout(S, G, V, sl.ring_k, (int)sizeof(T), (int)sizeof(Rec<T>), GRING);
+  const WarpLayout lay = warp_layout(S, G, V, sl.ring_k, (int)sizeof(T), (int)sizeof(Rec<T>), GRING,
+                                     GREEDY ? (int)sizeof(GAux<T>) : 0);
   unsigned char* wbase = smem + lay.prefix_bytes(L) + (size_t)lay.per_warp * warp;
   Rec<T>* recs = reinterpret_cast<Rec<T>*>(wbase + lay.rec_off);
   int64_t* dmem = reinterpret_cast<int64_t*>(wbase + lay.dmem_off);
   int16_t* cuts_all = reinterpret_cast<int16_t*>(wbase + lay.cuts_off);
   unsigned* cntw = reinterpret_cast<unsigned*>(wbase + lay.cnt_off);  // [lane][chunk]
+  GAux<T>* gaux = reinterpret_cast<GAux<T>*>(wbase + lay.gaux_off);    // [chunk][lane]
   T* ring;
   if constexpr (GRING) {
     const size_t gw = (size_t)blockIdx.x * kWarpsPerCta + warp;
@@ -257,15 +278,20 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   Rec<T> tr{};
   // GREEDY per-chunk counters and F-gate bytes
   int gF[V], gB[V], gW[V];
-  int64_t gA[V];
-  T pFc[V], pBc[V];   // cost of the cross-device predecessor of the F / B head (INF: none)
   unsigned pleft = 0; // bit c: F-pred of chunk c on the left neighbour; bit V+c: B-pred
+  unsigned fitmask = 0, s0mask = 0, lastmask = 0;  // bit c: F fits / stage 0 / stage S-1
+  T tstar = 0;        // t* of the slot (non-decreasing, refreshed every 4 rounds)
+  bool ts_fresh = true, force_ts = false;  // warp-uniform
   T hF[V], hB[V];     // cached arrival of the F / B head (-1: not yet produced)
-  int tF[V], tB[V];   // consumer (lane << 3 | chunk) of this chunk's F / B output, -1: none
+  unsigned seen[V];   // produced-count words seen at the last decision
+  bool gdirty = true; // the lane's decision must be recomputed
+  T g_at = INF;       // cached GREEDY decision: time, kind, chunk, mb, unknown heads
+  int g_ak = -1, g_acx = 0, g_aj = 0;
+  unsigned g_unk = 0;
 #pragma unroll
   for (int c = 0; c < V; ++c) {
-    gF[c] = gB[c] = gW[c] = 0; gA[c] = 0; pFc[c] = INF; pBc[c] = INF;
-    hF[c] = -1; hB[c] = -1; tF[c] = -1; tB[c] = -1;
+    gF[c] = gB[c] = gW[c] = 0;
+    hF[c] = -1; hB[c] = -1; seen[c] = 0;
   }
   // queue (warp-uniform) and accumulators
   uint64_t qpos = 0, qend = 0;
@@ -438,10 +464,15 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
                   pb = (T)dsum(kColTB, b, b1) + lat(b - 1);
                   bl = dev_of(sl.placement, p, s + 1) == (d == 0 ? p - 1 : d - 1);
                 }
-                pFc[c] = pf;
-                pBc[c] = pb;
-                tF[c] = s < S - 1 ? (((leader + dev_of(sl.placement, p, s + 1)) << 3) | ((s + 1) / p)) : -1;
-                tB[c] = s > 0 ? (((leader + dev_of(sl.placement, p, s - 1)) << 3) | ((s - 1) / p)) : -1;
+                GAux<T> ga;
+                ga.gate = 0;  // set below, once stat is complete
+                ga.pF = pf;
+                ga.pB = pb;
+                ga.tF = s < S - 1 ? (((leader + dev_of(sl.placement, p, s + 1)) << 3) | ((s + 1) / p)) : -1;
+                ga.tB = s > 0 ? (((leader + dev_of(sl.placement, p, s - 1)) << 3) | ((s - 1) / p)) : -1;
+                gaux[c * 32 + lane] = ga;
+                s0mask = (s0mask & ~(1u << c)) | ((s == 0 ? 1u : 0u) << c);
+                lastmask = (lastmask & ~(1u << c)) | ((s == S - 1 ? 1u : 0u) << c);
                 hF[c] = s == 0 ? (T)0 : (T)-1;
                 hB[c] = s == S - 1 ? (T)0 : (T)-1;
                 cntw[lane * 4 + c] = 0;
@@ -470,8 +501,18 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             const T dm = seg_min(dmin, p2), cm = seg_min(cmin, p2);
             if (take) {
               window = (cm == INF) ? INF : dm + cm;
+              gdirty = true;
 #pragma unroll
-              for (int c = 0; c < V; ++c) gA[c] = ac[c];
+              tstar = 0;
+              fitmask = 0;
+              for (int c = 0; c < V; ++c) {
+                seen[c] = 0xffffffffu;
+                if (lane_on) {
+                  const int64_t gate = sl.cap - stat - ac[c];  // cap - stat cannot overflow
+                  gaux[c * 32 + lane].gate = gate;
+                  fitmask |= (0 <= gate ? 1u : 0u) << c;
+                }
+              }
             }
           }
           // ---- ring reset for the slots being set up
@@ -563,115 +604,131 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       // ---- GREEDY (R14) in bounded-lag rounds (Lemma 3 with per-head bounds).
       // Rings are >= m deep (every slot written once per candidate); producers
       // bump the consumer's produced-count word, consumers read a slot once it
-      // exists and cache the head's arrival time.
-      T at = INF;
-      int ak = -1, acx = 0, aj = 0;
-      unsigned unkF = 0, unkB = 0;  // heads whose arrival is still unknown
-      auto decide = [&]() {
-        at = INF; ak = -1; unkF = 0; unkB = 0;
-        bool cFv[V], cBv[V], cWv[V];
-        T rmin = INF;
+      // exists and cache the head's arrival time. A lane's decision only changes
+      // after its own commit or a new arrival, so it is cached otherwise.
+      T& at = g_at;
+      int& ak = g_ak;
+      if (live) {
+        unsigned cw[V];
+        bool dirty = gdirty;
 #pragma unroll
         for (int c = 0; c < V; ++c) {
-          const int s = stage_of(sl.placement, p, c, d);
-          const int row = g * S + s;
-          const unsigned cw = ((volatile unsigned*)cntw)[lane * 4 + c];
-          if (hF[c] < 0 && gF[c] < (int)(cw & 0xffffu))
-            hF[c] = ((volatile T*)ring)[row + (gF[c] & KM) * RS];
-          if (hB[c] < 0 && gB[c] < (int)(cw >> 16))
-            hB[c] = ((volatile T*)ring)[BOFF + row + (gB[c] & KM) * RS];
-          cFv[c] = false; cBv[c] = false; cWv[c] = gW[c] < gB[c];
-          if (gF[c] < m && stat + dyn + gA[c] <= sl.cap) {
-            if (hF[c] >= 0) { cFv[c] = true; rmin = hF[c] < rmin ? hF[c] : rmin; }
-            else unkF |= 1u << c;
-          }
-          if (gB[c] < gF[c]) {
-            if (hB[c] >= 0) { cBv[c] = true; rmin = hB[c] < rmin ? hB[c] : rmin; }
-            else unkB |= 1u << c;
-          }
-          if (cWv[c]) rmin = 0;
+          cw[c] = ((volatile unsigned*)cntw)[lane * 4 + c];
+          dirty = dirty || cw[c] != seen[c];
         }
-        if (rmin != INF) {
-          at = free_t > rmin ? free_t : rmin;
-          int bj = INT_MAX;  // key (kind F < B < W, mb, stage); stage order == chunk order
+        if (dirty) {
+          gdirty = false;
+          at = INF; ak = -1; g_unk = 0;
+          unsigned okF = 0, okB = 0, okW = 0;
+          T rmin = INF;
 #pragma unroll
-          for (int c = 0; c < V; ++c)
-            if (cFv[c] && hF[c] <= at && gF[c] < bj) { bj = gF[c]; ak = 0; acx = c; }
-          if (ak < 0) {
-#pragma unroll
-            for (int c = 0; c < V; ++c)
-              if (cBv[c] && hB[c] <= at && gB[c] < bj) { bj = gB[c]; ak = 1; acx = c; }
+          for (int c = 0; c < V; ++c) {
+            seen[c] = cw[c];
+            if (hF[c] < 0 && gF[c] < (int)(cw[c] & 0xffffu))
+              hF[c] = ((volatile T*)ring)[REC(0, c).in_off + (gF[c] & KM) * RS];
+            if (hB[c] < 0 && gB[c] < (int)(cw[c] >> 16))
+              hB[c] = ((volatile T*)ring)[REC(1, c).in_off + (gB[c] & KM) * RS];
+            if (gF[c] < m && ((fitmask >> c) & 1u)) {
+              if (hF[c] >= 0) { okF |= 1u << c; rmin = hF[c] < rmin ? hF[c] : rmin; }
+              else g_unk |= 1u << c;
+            }
+            if (gB[c] < gF[c]) {
+              if (hB[c] >= 0) { okB |= 1u << c; rmin = hB[c] < rmin ? hB[c] : rmin; }
+              else g_unk |= 1u << (V + c);
+            }
+            if (gW[c] < gB[c]) { okW |= 1u << c; rmin = 0; }
           }
-          if (ak < 0) {
+          if (rmin != INF) {
+            at = free_t > rmin ? free_t : rmin;
+            // key (kind F < B < W, mb, stage); stage order == chunk order
+            unsigned kF = 0xffffffffu, kB = 0xffffffffu, kW = 0xffffffffu;
 #pragma unroll
-            for (int c = 0; c < V; ++c)
-              if (cWv[c] && gW[c] < bj) { bj = gW[c]; ak = 2; acx = c; }
+            for (int c = 0; c < V; ++c) {
+              const unsigned xf = ((unsigned)gF[c] << 2) | c, xb = ((unsigned)gB[c] << 2) | c,
+                             xw = ((unsigned)gW[c] << 2) | c;
+              if (((okF >> c) & 1u) && hF[c] <= at) kF = xf < kF ? xf : kF;
+              if (((okB >> c) & 1u) && hB[c] <= at) kB = xb < kB ? xb : kB;
+              if ((okW >> c) & 1u) kW = xw < kW ? xw : kW;
+            }
+            const unsigned k = kF != 0xffffffffu ? kF : (kB != 0xffffffffu ? kB : kW);
+            ak = kF != 0xffffffffu ? 0 : (kB != 0xffffffffu ? 1 : 2);
+            g_acx = (int)(k & 3u);
+            g_aj = (int)(k >> 2);
           }
-          aj = bj;
         }
-      };
-      if (live) decide();
+      } else {
+        at = INF; ak = -1;
+      }
+      const int acx = g_acx, aj = g_aj;
       // Every unscheduled task starts at >= t*, and a neighbour n starts every
       // further task at >= min(at_n, t* + window) for the rest of this round. An
       // unknown head therefore cannot become ready before that start plus its
-      // predecessor's duration and latency; decisions below every such bound are
+      // predecessor's duration and latency; a decision below every such bound is
       // final (DESIGN.md Lemma 3').
-      const T tstar = seg_min(at, p2);
+      ts_fresh = kTstarEvery == 1 || (wrounds % kTstarEvery) == 0 || force_ts;
+      if (ts_fresh) {  // t* is non-decreasing, so a stale value stays a valid (looser) bound
+        const T ts = seg_min(at, p2);
+        if (active) tstar = ts > tstar ? ts : tstar;
+        force_ts = false;
+      }
       const T atl = __shfl_sync(FULLMASK, at, nleft);
       const T atr = __shfl_sync(FULLMASK, at, nright);
-      const T tw = sat_add(tstar, window);
-      const T nl = atl < tw ? atl : tw;
-      const T nr = atr < tw ? atr : tw;
       T bound = INF;
-      auto tighten = [&]() {
+      if (g_unk) {
+        const T tw = sat_add(tstar, window);
+        const T nl = atl < tw ? atl : tw;
+        const T nr = atr < tw ? atr : tw;
 #pragma unroll
         for (int c = 0; c < V; ++c) {
-          if (unkF & (1u << c)) {
-            const T x = sat_add((pleft >> c) & 1u ? nl : nr, pFc[c]);
+          if (g_unk & (1u << c)) {
+            const T x = sat_add((pleft >> c) & 1u ? nl : nr, gaux[c * 32 + lane].pF);
             bound = x < bound ? x : bound;
           }
-          if (unkB & (1u << c)) {
-            const T x = sat_add((pleft >> (V + c)) & 1u ? nl : nr, pBc[c]);
+          if (g_unk & (1u << (V + c))) {
+            const T x = sat_add((pleft >> (V + c)) & 1u ? nl : nr, gaux[c * 32 + lane].pB);
             bound = x < bound ? x : bound;
           }
         }
-      };
-      tighten();
+      }
       __syncwarp();
-      // commit while the decision stays below the bound (several tasks per round)
-      for (int k = 0; k < kGreedyCommits && live && !done && ak >= 0 && at < bound; ++k) {
+      if (live && ak >= 0 && at < bound) {
         const Rec<T> rc = REC(ak, acx);
         const T fin = at + rc.dur;
         free_t = fin;
         dyn += DMEM(ak, acx);
         if (ak == 0) peak = dyn > peak ? dyn : peak;
-        int tgt = -1, dir = 0;
+        int tgt = -1;
+        const int dir = ak;
+        if (ak == 0) tgt = gaux[acx * 32 + lane].tF;
+        else if (ak == 1) tgt = gaux[acx * 32 + lane].tB;
 #pragma unroll
         for (int c = 0; c < V; ++c) {
           if (c == acx) {
             if (ak == 0) {
-              tgt = tF[c]; dir = 0; ++gF[c];
-              hF[c] = gF[c] < m && stage_of(sl.placement, p, c, d) == 0 ? (T)0 : (T)-1;
+              ++gF[c];
+              hF[c] = gF[c] < m && ((s0mask >> c) & 1u) ? (T)0 : (T)-1;
             } else if (ak == 1) {
-              tgt = tB[c]; dir = 1; ++gB[c];
-              hB[c] = stage_of(sl.placement, p, c, d) == S - 1 ? (T)0 : (T)-1;
+              ++gB[c];
+              hB[c] = ((lastmask >> c) & 1u) ? (T)0 : (T)-1;
             } else {
               ++gW[c];
             }
           }
         }
+        fitmask = 0;  // dyn changed: refresh the Eq. 2 gates
+#pragma unroll
+        for (int c = 0; c < V; ++c) fitmask |= (dyn <= gaux[c * 32 + lane].gate ? 1u : 0u) << c;
         if (tgt >= 0) {  // publish the arrival, then count it for the consumer
           ((volatile T*)ring)[rc.out_off + (aj & KM) * RS] = fin + rc.oc;
-          if (kGreedyCommits > 1) __threadfence_block();  // readers within this round
-          atomicAdd(&cntw[(tgt >> 3) * 4 + (tgt & 7)], dir ? 0x10000u : 1u);
+          atomicAdd(&cntw[(tgt >> 3) * 4 + (tgt & 7)], dir == 1 ? 0x10000u : 1u);
         }
         bool all = true;
 #pragma unroll
         for (int c = 0; c < V; ++c) all = all && gW[c] == m;
         done = all;
+        gdirty = true;
         ++ctasks;
         progressed = true;
-        if (!done && k + 1 < kGreedyCommits) { decide(); tighten(); }
       }
     }
     __syncwarp();
@@ -684,7 +741,9 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       const bool stall = active && slot_live && !(prog_m & smask);
       if (__ballot_sync(FULLMASK, stall || (active && !slot_live))) {
         const unsigned blk_m = __ballot_sync(FULLMASK, blocked);
-        if (stall) {
+        if (GREEDY && !ts_fresh && __ballot_sync(FULLMASK, stall)) {
+          force_ts = true;  // progress is only guaranteed with a fresh t*: retry once
+        } else if (stall) {
           flags |= (blk_m & smask) ? F_OVERFLOW : F_STUCK;
           done = true;
         }
@@ -718,7 +777,10 @@ static WarpLayout host_layout(const SegLaunch& s, bool gring) {
   const int tsz = s.tick == kTickI64 ? 8 : 4;
   const int rsz = s.tick == kTickI64 ? (int)sizeof(Rec<int64_t>)
                 : s.tick == kTickF32 ? (int)sizeof(Rec<float>) : (int)sizeof(Rec<int32_t>);
-  return warp_layout(s.S, s.G, s.v, s.ring_k, tsz, rsz, gring);
+  const int gsz = s.policy != ADAPTIS_GREEDY ? 0
+                : s.tick == kTickI64 ? (int)sizeof(GAux<int64_t>)
+                : s.tick == kTickF32 ? (int)sizeof(GAux<float>) : (int)sizeof(GAux<int32_t>);
+  return warp_layout(s.S, s.G, s.v, s.ring_k, tsz, rsz, gring, gsz);
 }
 
 size_t smem_bytes(const SegLaunch& s, bool fallback) {
