@@ -220,6 +220,27 @@ def main():
     total_ms, total_kern_ms = float(tot[0]), float(tot[1])
     valid = N - int(inv.item())
 
+    # ---- time-to-best-plan with the exact lower-bound prune (same winner; the
+    # simulated/s metric above keeps pruning off)
+    ctx.set_prune(True)
+    prep.search()
+    pr_ms = []
+    for _ in range(max(1, min(args.steps, 3))):
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        bp = prep.search()
+        e1.record(stream)
+        e1.synchronize()
+        pr_ms.append(e0.elapsed_time(e1))
+        assert bp["index"] == best["index"]
+    ctx.set_prune(False)
+    tp = torch.tensor([sum(pr_ms) / len(pr_ms)], dtype=torch.float64, device="cuda:%d" % local)
+    if world > 1:
+        dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+    pruned_ms = float(tp.item())
+
     # ---- e2e through the public call with host inputs (validation + H2D + D2H)
     e2e_ms = []
     for _ in range(max(1, min(args.steps, 3))):
@@ -244,7 +265,10 @@ def main():
                 "dtype": "int32" if not _int64(pr) else "int64", "data": "synthetic",
                 "config": {"workload": CONFIG_NAMES[args.config], "config_id": args.config,
                            "candidates": N, "valid_candidates": valid,
-                           "time_to_best_plan_ms": ms_step, "parallelism": "candidates%d" % world,
+                           "time_to_best_plan_ms": ms_step,
+                           "time_to_best_plan_pruned_ms": pruned_ms,
+                           "pruned_candidates": bp["n_pruned"],
+                           "parallelism": "candidates%d" % world,
                            "l2": "flushed (256 MiB write) between timed steps"},
                 "best": {"index": best["index"], "makespan_ticks": best["makespan"],
                          "plan": best["plan"], "bubble": best["bubble"],

@@ -164,6 +164,7 @@ typedef struct {             /* output of adaptis_search                        
   uint64_t n_evaluated;      /* candidates this rank evaluated                               */
   uint64_t n_invalid;        /* of those, invalid decodes (status 1)                         */
   uint64_t n_tasks;          /* F/B/W tasks this rank simulated (work counter for the roofline) */
+  uint64_t n_pruned;         /* candidates skipped by the exact lower-bound prune (0 if off)  */
   float    kernel_ms;        /* device time of this rank's evaluation kernels                */
 } adaptis_best;
 
@@ -184,6 +185,12 @@ typedef int (*adaptis_allreduce_min_fn)(int64_t* dev_key, void* cuda_stream, voi
 ADAPTIS_API adaptis_status adaptis_ctx_create(int cuda_device, int rank, int world, adaptis_ctx** out);
 ADAPTIS_API void           adaptis_ctx_destroy(adaptis_ctx* ctx);
 ADAPTIS_API adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_allreduce_min_fn fn, void* user);
+/* Exact lower-bound pruning for adaptis_search (default off; SURVEY §8d
+ * "time-to-best-plan with and without LB pruning"): a candidate is skipped when
+ * (max_d busy_d << bits | index) exceeds the best key found so far; since
+ * makespan >= max_d busy_d it cannot win, so the winner is unchanged. Skipped
+ * candidates are counted in adaptis_best.n_pruned. Ignored in FP32 cost mode. */
+ADAPTIS_API adaptis_status adaptis_ctx_set_prune(adaptis_ctx* ctx, int enable);
 /* The CUDA stream (cudaStream_t) every kernel of this context is queued on. */
 ADAPTIS_API void*          adaptis_ctx_stream(adaptis_ctx* ctx);
 /* Number of kernel launches this context has issued since creation. */

@@ -76,7 +76,7 @@ class _Best(C.Structure):
                 ("T_d", C.c_int64 * MAX_P), ("busy_d", C.c_int64 * MAX_P),
                 ("M_d", C.c_int64 * MAX_P), ("n_candidates", C.c_uint64),
                 ("n_evaluated", C.c_uint64), ("n_invalid", C.c_uint64), ("n_tasks", C.c_uint64),
-                ("kernel_ms", C.c_float)]
+                ("n_pruned", C.c_uint64), ("kernel_ms", C.c_float)]
 
 
 class _LaunchInfo(C.Structure):
@@ -111,6 +111,8 @@ def lib():
             L.adaptis_ctx_create.restype = st
             L.adaptis_ctx_create.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
             L.adaptis_ctx_destroy.argtypes = [C.c_void_p]
+            L.adaptis_ctx_set_prune.restype = st
+            L.adaptis_ctx_set_prune.argtypes = [C.c_void_p, C.c_int]
             L.adaptis_ctx_set_allreduce.restype = st
             L.adaptis_ctx_set_allreduce.argtypes = [C.c_void_p, ALLREDUCE_FN, C.c_void_p]
             L.adaptis_ctx_stream.restype = C.c_void_p
@@ -271,6 +273,10 @@ class Context:
         self._cb = ALLREDUCE_FN(_allreduce)
         _check(lib().adaptis_ctx_set_allreduce(self.ptr, self._cb, None), self.ptr)
 
+    def set_prune(self, enable: bool = True):
+        """Exact lower-bound pruning for search (winner unchanged; see adaptis.h)."""
+        _check(lib().adaptis_ctx_set_prune(self.ptr, int(bool(enable))), self.ptr)
+
     @property
     def stream(self) -> int:
         return lib().adaptis_ctx_stream(self.ptr)
@@ -401,7 +407,7 @@ def _best_dict(b: _Best, st: int, ctx_ptr) -> dict:
             "cand_status": int(b.result.status),
             "T_d": list(b.T_d[:p]), "busy_d": list(b.busy_d[:p]), "M_d": list(b.M_d[:p]),
             "n_candidates": int(b.n_candidates), "n_evaluated": int(b.n_evaluated),
-            "n_invalid": int(b.n_invalid), "n_tasks": int(b.n_tasks),
+            "n_invalid": int(b.n_invalid), "n_tasks": int(b.n_tasks), "n_pruned": int(b.n_pruned),
             "kernel_ms": float(b.kernel_ms)}
 
 

@@ -79,6 +79,7 @@ struct adaptis_ctx {
   std::string err;
   uint64_t launches = 0;
   uint64_t fallback_cands = 0;
+  int prune = 0;
   uint64_t counters[3] = {0, 0, 0};
   uint64_t last_tasks = 0;
   std::vector<cudaEvent_t> seg_events;
@@ -493,6 +494,8 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     s.n_invalid = W + 1;
     s.n_tasks = sw + 2;
     s.n_rounds = W + 3;
+    s.n_pruned = W + 5;
+    s.prune = (mode_search && ctx->prune && P->tick != kTickF32) ? 1 : 0;
     // GREEDY rings hold all m items (its F-first rule can run m items ahead);
     // they live in global memory when they do not fit the shared-memory budget
     const size_t ring_bytes = (size_t)2 * s.ring_k * s.G * s.S * (P->tick == kTickI64 ? 8 : 4);
@@ -632,6 +635,12 @@ void adaptis_ctx_destroy(adaptis_ctx* c) {
   delete c;
 }
 
+adaptis_status adaptis_ctx_set_prune(adaptis_ctx* ctx, int enable) {
+  if (!ctx) return fail(nullptr, ADAPTIS_EINVAL, "ctx is NULL");
+  ctx->prune = enable ? 1 : 0;
+  return ADAPTIS_OK;
+}
+
 adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_allreduce_min_fn fn, void* user) {
   if (!ctx) return fail(nullptr, ADAPTIS_EINVAL, "ctx is NULL");
   ctx->allreduce = fn; ctx->allreduce_user = user;
@@ -759,11 +768,12 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   float ms = 0;
   adaptis_status st = run_range(ctx, P, 0, P->N, true, ctx->rank, ctx->world, nullptr, 0, nullptr, &ms);
   if (st != ADAPTIS_OK) return st;
-  unsigned long long words[3] = {0, 0, 0};
-  CU(ctx, cudaMemcpyAsync(words, ctx->d_scratch, 24, cudaMemcpyDeviceToHost, ctx->stream));
+  unsigned long long words[6] = {0, 0, 0, 0, 0, 0};
+  CU(ctx, cudaMemcpyAsync(words, ctx->d_scratch, 48, cudaMemcpyDeviceToHost, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   out->n_invalid = words[1];
   out->n_tasks = ctx->last_tasks;
+  out->n_pruned = words[5];
   const std::vector<adaptis_launch_info> search_info = ctx->last_info;
   out->kernel_ms = ms;
   out->n_candidates = P->N;

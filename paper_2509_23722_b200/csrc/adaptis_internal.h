@@ -61,6 +61,8 @@ struct SegLaunch {
   unsigned long long* n_invalid;// invalid decodes counted by this launch
   unsigned long long* n_tasks;  // simulated tasks counted by this launch
   unsigned long long* n_rounds; // [0] warp rounds, [1] live device-lane rounds
+  unsigned long long* n_pruned; // candidates skipped by the exact lower-bound prune
+  int prune;                    // search: skip candidates whose LB key exceeds the incumbent
   // fallback mode: positions index overflow_idx_in[] instead of [lo, hi)
   const uint64_t* list_idx;
   int ring_k;                   // ring slots (fast path: kRingK; fallback: >= m)
@@ -79,7 +81,7 @@ struct SegLaunch {
 // (split policies), the slots' cuts, and the fast-path rings
 // [2 directions][K slots][G*S stages].
 struct WarpLayout {
-  int rec_off, dmem_off, cuts_off, cnt_off, gaux_off, ring_off, per_warp;
+  int rec_off, dmem_off, cuts_off, cnt_off, gaux_off, cold_off, ring_off, per_warp;
   ADAPTIS_LAYOUT_HD size_t prefix_bytes(int L) const {
     return ((size_t)kNumCols * (L + 1) * 8 + 15) & ~(size_t)15;
   }
@@ -94,6 +96,7 @@ ADAPTIS_LAYOUT_HD WarpLayout warp_layout(int S, int G, int V, int K, int tsz, in
   l.cuts_off = off; off += align16(G * (S + 1) * 2);
   l.cnt_off = off;  off += 32 * 4 * 4;  // GREEDY produced-count words [lane][chunk]
   l.gaux_off = off; off += align16(V * 32 * gaux_sz);  // GREEDY per-chunk statics
+  l.cold_off = off; off += 32 * 56;                    // per-lane cold state (LaneCold)
   l.ring_off = off; if (!gring) off += 2 * K * G * S * tsz;
   l.per_warp = align16(off);
   return l;

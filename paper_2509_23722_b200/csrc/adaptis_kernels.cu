@@ -32,6 +32,10 @@ namespace adaptis {
 
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr int kQueueBlock = 64;  // positions claimed per warp atomic
+#ifndef ADAPTIS_GREEDY_COMMITS
+#define ADAPTIS_GREEDY_COMMITS 1
+#endif
+constexpr int kGreedyCommits = ADAPTIS_GREEDY_COMMITS;  // GREEDY tasks a lane may commit per round
 constexpr unsigned kTstarEvery = 1; // GREEDY t* refresh period (a stale t* costs more commits than it saves)
 
 template <typename T> struct TT;
@@ -61,7 +65,18 @@ struct GAux {      // GREEDY statics of one (lane, chunk), read off the critical
   T pF, pB;        // cost of the cross-device predecessor of an unknown F / B head
 };
 
-enum : int { F_INVALID = 1, F_PREOVER = 2, F_STUCK = 4, F_OVERFLOW = 8 };
+// per-lane state touched only at candidate setup / finalize and at kernel exit,
+// kept in shared memory so that the round loop keeps its registers (48 bytes)
+struct LaneCold {
+  uint64_t idx;                   // global index of the slot's candidate
+  int64_t busy;                   // busy time (int64, or double bits in the fp32 variant)
+  unsigned long long key;         // running minimum of the packed argmin key
+  unsigned long long invalid, tasks, live;  // counters flushed at kernel exit
+  unsigned long long pruned;
+};
+static_assert(sizeof(LaneCold) == 56, "LaneCold layout");
+
+enum : int { F_INVALID = 1, F_PREOVER = 2, F_STUCK = 4, F_OVERFLOW = 8, F_PRUNED = 16 };
 
 __device__ __forceinline__ int stage_of(int placement, int p, int c, int d) {
   if (placement == ADAPTIS_SEQ) return d;
@@ -236,6 +251,9 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   int16_t* cuts_all = reinterpret_cast<int16_t*>(wbase + lay.cuts_off);
   unsigned* cntw = reinterpret_cast<unsigned*>(wbase + lay.cnt_off);  // [lane][chunk]
   GAux<T>* gaux = reinterpret_cast<GAux<T>*>(wbase + lay.gaux_off);    // [chunk][lane]
+  LaneCold& cold = reinterpret_cast<LaneCold*>(wbase + lay.cold_off)[threadIdx.x & 31];
+  cold.idx = 0; cold.busy = 0; cold.key = ~0ull >> 1; cold.invalid = 0; cold.tasks = 0; cold.live = 0;
+  cold.pruned = 0;
   T* ring;
   if constexpr (GRING) {
     const size_t gw = (size_t)blockIdx.x * kWarpsPerCta + warp;
@@ -265,10 +283,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   bool active = false;  // slot simulates a candidate (uniform within the slot)
   bool done = true;     // this lane has no task left
   int flags = 0;        // slot-uniform F_* bits
-  uint64_t idx = 0;
   T free_t = 0;
   int64_t dyn = 0, peak = 0, stat = 0;
-  BT busy = 0;
   T window = INF;
   // fixed orders
   int nF = 0, nB = 0, nW = 0;
@@ -296,7 +312,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   // queue (warp-uniform) and accumulators
   uint64_t qpos = 0, qend = 0;
   bool exhausted = false;
-  unsigned long long wkey = ~0ull >> 1, winvalid = 0, wtasks = 0, wrounds = 0, wlive = 0;
+  unsigned wrounds = 0;
   unsigned ctasks = 0, clive = 0;  // this lane's tasks / live rounds since the last flush
 
   auto next_task = [&]() {
@@ -308,7 +324,10 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
 
   // collective: write results of the slots with `fl` set (all lanes execute)
   auto finalize = [&](bool fl) {
-    if (fl) { wtasks += ctasks; wlive += clive; ctasks = 0; clive = 0; }
+    if (fl) { cold.tasks += ctasks; cold.live += clive; ctasks = 0; clive = 0; }
+    BT busy;
+    if constexpr (FP) busy = __longlong_as_double(cold.busy); else busy = cold.busy;
+    const uint64_t idx = cold.idx;
     const bool contrib = fl && dev_lane;
     const T mkT = seg_max(contrib ? free_t : (T)0, p2);
     const int64_t mk = to_ticks(mkT);
@@ -317,7 +336,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
     const int64_t Mmax = seg_max(contrib ? Md : (int64_t)0, p2);
     const bool anyover = (__ballot_sync(FULLMASK, contrib && Md > sl.cap) & smask) != 0;
     int status;
-    if (flags & F_INVALID) status = ADAPTIS_CAND_INVALID;
+    if (flags & F_PRUNED) status = -3;  // search: cannot beat the incumbent key (exact LB prune)
+    else if (flags & F_INVALID) status = ADAPTIS_CAND_INVALID;
     else if (flags & F_OVERFLOW) status = -2;
     else if (FUSED && ((flags & F_PREOVER) || anyover)) status = ADAPTIS_CAND_OVER_CAP;
     else if (flags & F_STUCK) status = ADAPTIS_CAND_STUCK;
@@ -328,14 +348,18 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         const unsigned k = atomicAdd(sl.overflow_count, 1u);
         if (k < sl.overflow_cap) sl.overflow_idx[k] = idx;
       } else {
-        if (status == ADAPTIS_CAND_INVALID) ++winvalid;
+        if (status == ADAPTIS_CAND_INVALID) ++cold.invalid;
+        if (status == -3) ++cold.pruned;
         if (sl.key) {
           if (status == ADAPTIS_CAND_OK) {
             unsigned long long kv;  // order-preserving: fp32 bits of a positive float
             if constexpr (FP) kv = (unsigned long long)__float_as_uint(mkT);
             else kv = (unsigned long long)mk;
             const unsigned long long key = (kv << sl.key_bits) | idx;
-            wkey = key < wkey ? key : wkey;
+            if (key < cold.key) {
+              cold.key = key;
+              if (sl.prune) atomicMin(sl.key, key);  // share the incumbent at once
+            }
           }
         } else {
           const uint64_t o = idx - sl.eval_first;
@@ -391,7 +415,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
 
           // ---- a1 decode
           bool valid = false;
-          if (take) idx = pos_to_index(sl, mypos);
+          uint64_t idx = 0;
+          if (take) { idx = pos_to_index(sl, mypos); cold.idx = idx; }
           if (take && d == 0)
             valid = decode_cuts(tab.binom, tab.ball, tab.seeds, sl.group, sl.part_mode, sl.radius,
                                 S, L, idx - sl.seg_base, cuts);
@@ -400,10 +425,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           const bool lane_on = take && valid && dev_lane;
           if (take) {
             flags = valid ? 0 : F_INVALID;
-            free_t = 0; dyn = 0; peak = 0; busy = 0; stat = 0;
+            free_t = 0; dyn = 0; peak = 0; stat = 0;
           }
           // ---- a2/a3 aggregation into task records
           T dmin = INF, cmin = INF;
+          BT busy = 0;
           int64_t ac[V];
 #pragma unroll
           for (int c = 0; c < V; ++c) ac[c] = 0;
@@ -449,6 +475,9 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
                 DMEM(2, c) = -sta;
               }
               ac[c] = act + sta;
+              if (c == V - 1) {
+                if constexpr (FP) cold.busy = __double_as_longlong(busy); else cold.busy = busy;
+              }
               if constexpr (GREEDY) {
                 // Lemma 3 refinement: an unknown head F(s, j) waits for F(s-1, j) on the
                 // device of stage s-1, which lasts c_F(s-1) and then travels oF(s-1)
@@ -521,7 +550,18 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
               for (int k = 0; k < 2 * sl.ring_k; ++k) ring[(size_t)k * RS + g * S + s] = EMPTY;
           }
           __syncwarp();
-          const bool survivor = take && valid && !(flags & F_PREOVER);
+          // exact lower-bound prune (search only): makespan >= max_d busy_d, so a
+          // candidate whose (LB << bits | index) exceeds the incumbent key cannot win
+          if constexpr (!FP) {
+            if (sl.prune) {
+              const int64_t lb = seg_max(lane_on ? (int64_t)busy : (int64_t)0, p2);
+              const unsigned long long inc = *(volatile unsigned long long*)sl.key;
+              if (take && valid && !(flags & F_PREOVER) &
+                  ((((unsigned long long)lb << sl.key_bits) | idx) > inc))
+                flags |= F_PRUNED;
+            }
+          }
+          const bool survivor = take && valid && !(flags & (F_PREOVER | F_PRUNED));
           const unsigned nonsurv_m = __ballot_sync(FULLMASK, take && !survivor);
           if (nonsurv_m) finalize(take && !survivor);
           if (survivor) {
@@ -608,58 +648,59 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       // after its own commit or a new arrival, so it is cached otherwise.
       T& at = g_at;
       int& ak = g_ak;
-      if (live) {
+      auto decide = [&](bool force) {
         unsigned cw[V];
-        bool dirty = gdirty;
+        bool dirty = gdirty || force;
 #pragma unroll
         for (int c = 0; c < V; ++c) {
           cw[c] = ((volatile unsigned*)cntw)[lane * 4 + c];
           dirty = dirty || cw[c] != seen[c];
         }
-        if (dirty) {
-          gdirty = false;
-          at = INF; ak = -1; g_unk = 0;
-          unsigned okF = 0, okB = 0, okW = 0;
-          T rmin = INF;
+        if (!dirty) return;
+        gdirty = false;
+        at = INF; ak = -1; g_unk = 0;
+        unsigned okF = 0, okB = 0, okW = 0;
+        T rmin = INF;
+#pragma unroll
+        for (int c = 0; c < V; ++c) {
+          seen[c] = cw[c];
+          if (hF[c] < 0 && gF[c] < (int)(cw[c] & 0xffffu))
+            hF[c] = ((volatile T*)ring)[REC(0, c).in_off + (gF[c] & KM) * RS];
+          if (hB[c] < 0 && gB[c] < (int)(cw[c] >> 16))
+            hB[c] = ((volatile T*)ring)[REC(1, c).in_off + (gB[c] & KM) * RS];
+          if (gF[c] < m && ((fitmask >> c) & 1u)) {
+            if (hF[c] >= 0) { okF |= 1u << c; rmin = hF[c] < rmin ? hF[c] : rmin; }
+            else g_unk |= 1u << c;
+          }
+          if (gB[c] < gF[c]) {
+            if (hB[c] >= 0) { okB |= 1u << c; rmin = hB[c] < rmin ? hB[c] : rmin; }
+            else g_unk |= 1u << (V + c);
+          }
+          if (gW[c] < gB[c]) { okW |= 1u << c; rmin = 0; }
+        }
+        if (rmin != INF) {
+          at = free_t > rmin ? free_t : rmin;
+          // key (kind F < B < W, mb, stage); stage order == chunk order
+          unsigned kF = 0xffffffffu, kB = 0xffffffffu, kW = 0xffffffffu;
 #pragma unroll
           for (int c = 0; c < V; ++c) {
-            seen[c] = cw[c];
-            if (hF[c] < 0 && gF[c] < (int)(cw[c] & 0xffffu))
-              hF[c] = ((volatile T*)ring)[REC(0, c).in_off + (gF[c] & KM) * RS];
-            if (hB[c] < 0 && gB[c] < (int)(cw[c] >> 16))
-              hB[c] = ((volatile T*)ring)[REC(1, c).in_off + (gB[c] & KM) * RS];
-            if (gF[c] < m && ((fitmask >> c) & 1u)) {
-              if (hF[c] >= 0) { okF |= 1u << c; rmin = hF[c] < rmin ? hF[c] : rmin; }
-              else g_unk |= 1u << c;
-            }
-            if (gB[c] < gF[c]) {
-              if (hB[c] >= 0) { okB |= 1u << c; rmin = hB[c] < rmin ? hB[c] : rmin; }
-              else g_unk |= 1u << (V + c);
-            }
-            if (gW[c] < gB[c]) { okW |= 1u << c; rmin = 0; }
+            const unsigned xf = ((unsigned)gF[c] << 2) | c, xb = ((unsigned)gB[c] << 2) | c,
+                           xw = ((unsigned)gW[c] << 2) | c;
+            if (((okF >> c) & 1u) && hF[c] <= at) kF = xf < kF ? xf : kF;
+            if (((okB >> c) & 1u) && hB[c] <= at) kB = xb < kB ? xb : kB;
+            if ((okW >> c) & 1u) kW = xw < kW ? xw : kW;
           }
-          if (rmin != INF) {
-            at = free_t > rmin ? free_t : rmin;
-            // key (kind F < B < W, mb, stage); stage order == chunk order
-            unsigned kF = 0xffffffffu, kB = 0xffffffffu, kW = 0xffffffffu;
-#pragma unroll
-            for (int c = 0; c < V; ++c) {
-              const unsigned xf = ((unsigned)gF[c] << 2) | c, xb = ((unsigned)gB[c] << 2) | c,
-                             xw = ((unsigned)gW[c] << 2) | c;
-              if (((okF >> c) & 1u) && hF[c] <= at) kF = xf < kF ? xf : kF;
-              if (((okB >> c) & 1u) && hB[c] <= at) kB = xb < kB ? xb : kB;
-              if ((okW >> c) & 1u) kW = xw < kW ? xw : kW;
-            }
-            const unsigned k = kF != 0xffffffffu ? kF : (kB != 0xffffffffu ? kB : kW);
-            ak = kF != 0xffffffffu ? 0 : (kB != 0xffffffffu ? 1 : 2);
-            g_acx = (int)(k & 3u);
-            g_aj = (int)(k >> 2);
-          }
+          const unsigned k = kF != 0xffffffffu ? kF : (kB != 0xffffffffu ? kB : kW);
+          ak = kF != 0xffffffffu ? 0 : (kB != 0xffffffffu ? 1 : 2);
+          g_acx = (int)(k & 3u);
+          g_aj = (int)(k >> 2);
         }
+      };
+      if (live) {
+        decide(false);
       } else {
         at = INF; ak = -1;
       }
-      const int acx = g_acx, aj = g_aj;
       // Every unscheduled task starts at >= t*, and a neighbour n starts every
       // further task at >= min(at_n, t* + window) for the rest of this round. An
       // unknown head therefore cannot become ready before that start plus its
@@ -674,10 +715,10 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       const T atl = __shfl_sync(FULLMASK, at, nleft);
       const T atr = __shfl_sync(FULLMASK, at, nright);
       T bound = INF;
-      if (g_unk) {
-        const T tw = sat_add(tstar, window);
-        const T nl = atl < tw ? atl : tw;
-        const T nr = atr < tw ? atr : tw;
+      const T tw = sat_add(tstar, window);
+      const T nl = atl < tw ? atl : tw;
+      const T nr = atr < tw ? atr : tw;
+      auto tighten = [&]() {
 #pragma unroll
         for (int c = 0; c < V; ++c) {
           if (g_unk & (1u << c)) {
@@ -689,9 +730,14 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             bound = x < bound ? x : bound;
           }
         }
-      }
+      };
+      if (g_unk) tighten();
       __syncwarp();
-      if (live && ak >= 0 && at < bound) {
+      // commit while the decision stays below the bound: the bound stays a lower
+      // bound on every new arrival for the rest of the round once the terms of
+      // newly unknown heads are added (DESIGN.md Lemma 3')
+      for (int kc = 0; kc < kGreedyCommits && live && !done && ak >= 0 && at < bound; ++kc) {
+        const int acx = g_acx, aj = g_aj;
         const Rec<T> rc = REC(ak, acx);
         const T fin = at + rc.dur;
         free_t = fin;
@@ -720,6 +766,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         for (int c = 0; c < V; ++c) fitmask |= (dyn <= gaux[c * 32 + lane].gate ? 1u : 0u) << c;
         if (tgt >= 0) {  // publish the arrival, then count it for the consumer
           ((volatile T*)ring)[rc.out_off + (aj & KM) * RS] = fin + rc.oc;
+          if (kGreedyCommits > 1) __threadfence_block();  // readers within this round
           atomicAdd(&cntw[(tgt >> 3) * 4 + (tgt & 7)], dir == 1 ? 0x10000u : 1u);
         }
         bool all = true;
@@ -729,6 +776,10 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         gdirty = true;
         ++ctasks;
         progressed = true;
+        if (kGreedyCommits > 1 && !done && kc + 1 < kGreedyCommits) {
+          decide(true);
+          if (g_unk) tighten();
+        }
       }
     }
     __syncwarp();
@@ -755,20 +806,22 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
 #undef DMEM
 
   // ---- a7 argmin: warp min -> one atomicMin per warp; counters
-  wtasks += ctasks;
-  wlive += clive;
+  unsigned long long wkey = cold.key, winvalid = cold.invalid, wtasks = cold.tasks + ctasks,
+                     wlive = cold.live + clive, wpruned = cold.pruned;
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long x = __shfl_xor_sync(FULLMASK, wkey, o);
     wkey = x < wkey ? x : wkey;
     winvalid += __shfl_xor_sync(FULLMASK, winvalid, o);
     wtasks += __shfl_xor_sync(FULLMASK, wtasks, o);
     wlive += __shfl_xor_sync(FULLMASK, wlive, o);
+    wpruned += __shfl_xor_sync(FULLMASK, wpruned, o);
   }
   if (lane == 0) {
     if (sl.key && wkey != (~0ull >> 1)) atomicMin(sl.key, wkey);
     if (winvalid) atomicAdd(sl.n_invalid, winvalid);
     if (wtasks) atomicAdd(sl.n_tasks, wtasks);
-    if (wrounds) { atomicAdd(&sl.n_rounds[0], wrounds); atomicAdd(&sl.n_rounds[1], wlive); }
+    if (wpruned) atomicAdd(sl.n_pruned, wpruned);
+    if (wrounds) { atomicAdd(&sl.n_rounds[0], (unsigned long long)wrounds); atomicAdd(&sl.n_rounds[1], wlive); }
   }
 }
 

@@ -268,3 +268,19 @@ def test_fp32_search_winner_within_tolerance(ctx):
     want = O.eval_indices(prf, sp, range(O.space_size(prf, sp)))
     best = np.min(want["makespan_f"][want["status"] == 0])
     assert b["makespan_f32"] <= best * (1 + FP32_RTOL)  # T7: the winner is within 1e-5 of the optimum
+
+
+# ----------------------------------------------------------------- exact lower-bound pruning
+def test_pruned_search_same_winner(ctx):
+    from paper_2509_23722_b200 import adaptis as A
+    c = A.Context(0)
+    c.set_prune(True)
+    cases = [W.config(1), W.config(2)] + _random_spaces(21, 6)
+    for pr, sp in cases:
+        a = ctx.search(pr, sp)
+        b = c.search(pr, sp)
+        assert (a["index"], a["makespan"], a["status"]) == (b["index"], b["makespan"], b["status"])
+    pr, sp = W.config(2)
+    b = c.search(pr, sp)
+    assert b["n_pruned"] > 0.5 * b["n_candidates"]  # the LB prune removes most of cfg2
+    c.close()
