@@ -408,6 +408,7 @@ int ring_slots(int policy, int m) {
   while (pw < k) pw <<= 1;
   return pw;
 }
+constexpr uint64_t kSeedPass = 4096;  // indices per segment in the pruned search's seed pass
 constexpr size_t kHdr = 8;  // [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds
 constexpr size_t kGreedySmemRing = 0;  // per warp: GREEDY rings live in global memory (L2)
 
@@ -454,7 +455,8 @@ SegLaunch make_launch(const adaptis_prepared* P, const Seg& sg) {
 constexpr size_t kSegWords = 6;
 adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uint64_t hi,
                          bool mode_search, int rank, int world, const adaptis_results_soa* dout,
-                         uint64_t eval_first, int64_t* report, float* kernel_ms) {
+                         uint64_t eval_first, int64_t* report, float* kernel_ms,
+                         bool keep_key = false) {
   const size_t nseg = P->segs.size();
   const size_t nwords = kHdr + kSegWords * nseg;
   adaptis_status st = ensure_scratch(ctx, nwords, kOverflowPerSeg * nseg);
@@ -467,7 +469,10 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
   unsigned long long* W = ctx->d_scratch;
   std::vector<unsigned long long> init(nwords, 0);
   init[0] = (~0ull) >> 1;
-  CU(ctx, cudaMemcpyAsync(W, init.data(), nwords * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (keep_key)  // continue from the incumbent of a previous pass
+    CU(ctx, cudaMemcpyAsync(W + 1, init.data() + 1, (nwords - 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  else
+    CU(ctx, cudaMemcpyAsync(W, init.data(), nwords * 8, cudaMemcpyHostToDevice, ctx->stream));
   CU(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   std::vector<SegLaunch> launched(nseg);
   std::vector<char> active(nseg, 0);
@@ -477,6 +482,7 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     if (a >= b) continue;
     SegLaunch s = make_launch(P, sg);
     shard(a, b, rank, world, &s);
+    s.lo = a; s.hi = b;
     if (s.n_pos == 0) continue;
     unsigned long long* sw = W + kHdr + kSegWords * i;
     s.key = mode_search ? W : nullptr;
@@ -766,7 +772,26 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   CU(ctx, cudaSetDevice(ctx->device));
   memset(out, 0, sizeof(*out));
   float ms = 0;
-  adaptis_status st = run_range(ctx, P, 0, P->N, true, ctx->rank, ctx->world, nullptr, 0, nullptr, &ms);
+  adaptis_status st;
+  bool seeded = false;
+  if (ctx->prune && P->tick != kTickF32) {
+    // seed pass: the first indices of every segment (the seed neighbourhood of
+    // BALL spaces) give the lower-bound prune a good incumbent early; every rank
+    // runs it, duplicates do not change the minimum
+    for (const Seg& sg : P->segs) {
+      const uint64_t n = std::min<uint64_t>(sg.count, kSeedPass);
+      float t = 0;
+      st = run_range(ctx, P, sg.base, sg.base + n, true, 0, 1, nullptr, 0, nullptr, &t, seeded);
+      if (st != ADAPTIS_OK) return st;
+      ms += t;
+      seeded = true;
+    }
+  }
+  {
+    float t = 0;
+    st = run_range(ctx, P, 0, P->N, true, ctx->rank, ctx->world, nullptr, 0, nullptr, &t, seeded);
+    ms += t;
+  }
   if (st != ADAPTIS_OK) return st;
   unsigned long long words[6] = {0, 0, 0, 0, 0, 0};
   CU(ctx, cudaMemcpyAsync(words, ctx->d_scratch, 48, cudaMemcpyDeviceToHost, ctx->stream));

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdio>
 #include <cstdint>
 #include <type_traits>
 
@@ -30,8 +31,21 @@
 
 namespace adaptis {
 
+#ifdef ADAPTIS_DEBUG
+#define DCHECK(cond, what, val)                                                          \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      printf("DCHECK %s failed: %s = %lld (block %d lane %d)\n", #cond, what,          \
+             (long long)(val), blockIdx.x, threadIdx.x);                                 \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define DCHECK(cond, what, val) do { } while (0)
+#endif
+
 constexpr unsigned FULLMASK = 0xffffffffu;
-constexpr int kQueueBlock = 64;  // positions claimed per warp atomic
+constexpr int kRun = 32;         // consecutive positions a slot claims (incremental decode)
 #ifndef ADAPTIS_GREEDY_COMMITS
 #define ADAPTIS_GREEDY_COMMITS 1
 #endif
@@ -164,6 +178,31 @@ __device__ int64_t megatron_peak(const int64_t (&a)[V], int p, int m, int w) {
     best = x > best ? x : best;
   }
   return best;
+}
+
+// successors in the canonical order (R19), for consecutive indices of one slot:
+// L1 ball: odometer over delta_n (fastest) .. delta_1 with digit order
+// 0, -1, +1, -2, +2, ... and the remaining radius `rem`
+__device__ __forceinline__ void ball_next(int16_t* cuts, const int16_t* seed, int n, int& rem) {
+  for (int i = n; i >= 1; --i) {
+    const int di = cuts[i] - seed[i - 1];
+    const int ai = di < 0 ? -di : di;
+    const int nd = di == 0 ? -1 : (di < 0 ? -di : -di - 1);
+    const int cost = (nd < 0 ? -nd : nd) - ai;
+    if (cost <= rem) { cuts[i] = (int16_t)(seed[i - 1] + nd); rem -= cost; return; }
+    rem += ai;
+    cuts[i] = seed[i - 1];  // digit back to 0, carry into delta_{i-1}
+  }
+}
+// FULL: colex successor of c_1 < ... < c_{S-1} < cuts[S] = L
+__device__ __forceinline__ void colex_next(int16_t* cuts, int S) {
+  for (int i = 1; i <= S - 1; ++i) {
+    if (cuts[i] + 1 < cuts[i + 1]) {
+      cuts[i] = (int16_t)(cuts[i] + 1);
+      for (int k = 1; k < i; ++k) cuts[k] = (int16_t)k;
+      return;
+    }
+  }
 }
 
 __device__ __forceinline__ uint64_t pos_to_index(const SegLaunch& sl, uint64_t pos) {
@@ -309,9 +348,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
     gF[c] = gB[c] = gW[c] = 0;
     hF[c] = -1; hB[c] = -1; seen[c] = 0;
   }
-  // queue (warp-uniform) and accumulators
-  uint64_t qpos = 0, qend = 0;
-  bool exhausted = false;
+  // work queue: every slot works through runs of consecutive positions
+  uint64_t rpos = 0, rend = 0;  // slot-uniform current run
+  uint64_t prev_idx = ~0ull - 1; // slot leader: index whose cuts are in smem (none yet)
+  int brem = 0;                 // slot leader: remaining L1 radius of that decode
+  bool exhausted = false;       // warp-uniform: the launch's positions are all claimed
   unsigned wrounds = 0;
   unsigned ctasks = 0, clive = 0;  // this lane's tasks / live rounds since the last flush
 
@@ -394,33 +435,68 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         if (fin) active = false;
       }
       const unsigned idle_m = __ballot_sync(FULLMASK, !active);
-      if (idle_m && !exhausted) {
+      const bool runs_left = __any_sync(FULLMASK, rpos < rend);
+      if (idle_m && (!exhausted || runs_left)) {
         for (int it = 0; it < 4; ++it) {
-          const unsigned want_m = __ballot_sync(FULLMASK, !active && d == 0);
-          if (want_m == 0) break;
-          if (qpos >= qend) {
+          // idle slots without positions claim runs of kRun consecutive positions
+          const bool want = !active;
+          const unsigned need_m = __ballot_sync(FULLMASK, want && rpos >= rend && d == 0);
+          if (need_m && !exhausted) {
+            const unsigned nw = __popc(need_m);
+            const unsigned rank = __popc(need_m & ((1u << leader) - 1u));
             unsigned long long b = 0;
-            if (lane == 0) b = atomicAdd(sl.cursor, (unsigned long long)kQueueBlock);
+            if (lane == 0) b = atomicAdd(sl.cursor, (unsigned long long)nw * kRun);
             b = __shfl_sync(FULLMASK, b, 0);
-            if (b >= sl.n_pos) { exhausted = true; break; }
-            qpos = b;
-            qend = b + kQueueBlock < sl.n_pos ? b + kQueueBlock : sl.n_pos;
+            if (b + (unsigned long long)nw * kRun >= sl.n_pos) exhausted = true;
+            if (want && rpos >= rend) {
+              const uint64_t st = b + (uint64_t)rank * kRun;
+              rpos = st < sl.n_pos ? st : sl.n_pos;
+              rend = st + kRun < sl.n_pos ? st + kRun : sl.n_pos;
+            }
           }
-          const unsigned nw = __popc(want_m);
-          const unsigned rank = __popc(want_m & ((1u << leader) - 1u));
-          const uint64_t avail = qend - qpos;
-          const bool take = !active && (uint64_t)rank < avail;
-          const uint64_t mypos = qpos + rank;
-          qpos += (uint64_t)nw < avail ? (uint64_t)nw : avail;
+          const bool take = want && rpos < rend;
+          if (__ballot_sync(FULLMASK, take) == 0) break;
+          const uint64_t mypos = rpos;
+          if (take) ++rpos;
+          DCHECK(!take || mypos < sl.n_pos, "mypos", mypos);
 
-          // ---- a1 decode
-          bool valid = false;
+          // ---- a1 decode: the successor of the previous candidate when the slot
+          // moves to the next index, else unranking from scratch
           uint64_t idx = 0;
           if (take) { idx = pos_to_index(sl, mypos); cold.idx = idx; }
-          if (take && d == 0)
-            valid = decode_cuts(tab.binom, tab.ball, tab.seeds, sl.group, sl.part_mode, sl.radius,
-                                S, L, idx - sl.seg_base, cuts);
-          valid = __shfl_sync(FULLMASK, valid, leader);
+          DCHECK(!take || (idx >= sl.seg_base && idx < sl.hi), "idx", (long long)idx);
+          if (take && d == 0) {
+            const int16_t* seed = tab.seeds + sl.group * ADAPTIS_MAX_S;
+            if (idx == prev_idx + 1 && S > 1) {
+              if (sl.part_mode == ADAPTIS_PART_FULL) colex_next(cuts, S);
+              else ball_next(cuts, seed, S - 1, brem);
+            } else {
+              decode_cuts(tab.binom, tab.ball, tab.seeds, sl.group, sl.part_mode, sl.radius, S, L,
+                          idx - sl.seg_base, cuts);
+              if (sl.part_mode == ADAPTIS_PART_BALL) {
+                int used = 0;
+                for (int i = 1; i < S; ++i) {
+                  const int di = cuts[i] - seed[i - 1];
+                  used += di < 0 ? -di : di;
+                }
+                brem = sl.radius - used;
+              }
+            }
+            prev_idx = idx;
+          }
+          __syncwarp();
+          // validity (strictly increasing cuts, R19), checked by the slot's lanes.
+          // The ballot runs on all lanes: a short-circuited collective diverges the warp.
+          bool viol = false;
+          if (take && dev_lane) {
+#pragma unroll
+            for (int c = 0; c < V; ++c) {
+              const int s = stage_of(sl.placement, p, c, d);
+              viol = viol || cuts[s] >= cuts[s + 1];
+            }
+          }
+          const unsigned viol_m = __ballot_sync(FULLMASK, viol);
+          const bool valid = take && !(viol_m & smask);
           __syncwarp();
           const bool lane_on = take && valid && dev_lane;
           if (take) {
@@ -438,6 +514,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             for (int c = 0; c < V; ++c) {
               const int s = stage_of(sl.placement, p, c, d);
               const int a = cuts[s], b = cuts[s + 1];
+              DCHECK(s >= 0 && s < S, "stage", s);
+              DCHECK(a >= 0 && b <= L && a < b, "cut", a * 100000 + b);
               const BT cF = dsum(kColTF, a, b);
               const BT cB = dsum(kColTB, a, b);
               const BT cW = dsum(kColTW, a, b);
@@ -577,12 +655,14 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         }
       }
       const unsigned act_m = __ballot_sync(FULLMASK, active);
+      const bool runs_any = __any_sync(FULLMASK, rpos < rend);
+      const bool more = !exhausted || runs_any;
       if (act_m == 0) {
-        if (exhausted) break;
+        if (!more) break;
         maint = true;
         continue;
       }
-      maint = (act_m != FULLMASK) && !exhausted;  // some slot is still idle
+      maint = (act_m != FULLMASK) && more;  // some slot is still idle
     }
 
     // ================= a5: one simulation round
@@ -597,6 +677,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       if (live && tk < 2) {  // phase A: read the input arrival and the output slot
         iaddr = tr.in_off >= 0 ? tr.in_off + (tj & KM) * RS : -1;
         oaddr = tr.out_off >= 0 ? tr.out_off + (tj & KM) * RS : -1;
+        DCHECK(iaddr < 2 * sl.ring_k * RS && oaddr < 2 * sl.ring_k * RS, "ring addr", iaddr * 100000 + oaddr);
+        DCHECK(tc >= 0 && tc < V && tk >= 0 && tk < 2, "task", tk * 100 + tc);
         r = iaddr >= 0 ? ring[iaddr] : (T)0;
         ofree = oaddr < 0 || ring[oaddr] == EMPTY;
       }
