@@ -119,9 +119,17 @@ def cpu_oracle_rate(pr, sp, seconds, seed=2025):
     ev = O.eval_indices(pr, sp, idx, nthreads=nth)
     dt = time.perf_counter() - t
     valid = int((ev["status"] != 1).sum())
+    # single-thread rate of the same oracle on a quarter-length prefix of the sample
+    n1 = max(8, int(n / nth / 4))
+    t = time.perf_counter()
+    ev1 = O.eval_indices(pr, sp, idx[:n1], nthreads=1)
+    dt1 = time.perf_counter() - t
+    valid1 = int((ev1["status"] != 1).sum())
     return {"value": valid / dt, "unit": UNIT, "cores": nth, "kind": "oracle",
-            "sample": "%d uniformly random candidates of %s (%d valid), event-loop oracle, %.1f s"
-                      % (n, pr.name, valid, dt)}, n, dt
+            "value_1thread": valid1 / dt1,
+            "sample": "%d uniformly random candidates of %s (%d valid), event-loop oracle, %.1f s on "
+                      "%d threads; 1-thread rate on the first %d of them (%.1f s)"
+                      % (n, pr.name, valid, dt, nth, n1, dt1)}, n, dt
 
 
 def run_reference(args, rank, world):

@@ -45,7 +45,10 @@ namespace adaptis {
 #endif
 
 constexpr unsigned FULLMASK = 0xffffffffu;
-constexpr int kRun = 32;         // consecutive positions a slot claims (incremental decode)
+#ifndef ADAPTIS_KRUN
+#define ADAPTIS_KRUN 32
+#endif
+constexpr int kRun = ADAPTIS_KRUN;  // consecutive positions a slot claims (incremental decode)
 #ifndef ADAPTIS_GREEDY_COMMITS
 #define ADAPTIS_GREEDY_COMMITS 1
 #endif
@@ -316,6 +319,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   const int nleft = leader + (d == 0 ? p - 1 : d - 1);  // neighbour devices (wrap)
   const int nright = leader + (d + 1 >= p ? 0 : d + 1);
 #define REC(kind, c) recs[((kind) * V + (c)) * 32 + lane]
+
 #define DMEM(kind, c) dmem[((kind) * V + (c)) * 32 + lane]
 
   // ---- lane / slot state
@@ -444,14 +448,24 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           if (need_m && !exhausted) {
             const unsigned nw = __popc(need_m);
             const unsigned rank = __popc(need_m & ((1u << leader) - 1u));
-            unsigned long long b = 0;
-            if (lane == 0) b = atomicAdd(sl.cursor, (unsigned long long)nw * kRun);
+            // run length: kRun, shortened near the end of the launch so that the
+            // last runs spread over all slots (tail balance)
+            unsigned long long b = 0, run = kRun;
+            if (lane == 0) {
+              const unsigned long long cur = *(volatile unsigned long long*)sl.cursor;
+              const unsigned long long rem = cur < sl.n_pos ? sl.n_pos - cur : 0;
+              const unsigned long long fair =
+                  rem / ((unsigned long long)gridDim.x * kWarpsPerCta * G * 4);
+              run = fair >= (unsigned long long)kRun ? kRun : (fair < 1 ? 1 : fair);
+              b = atomicAdd(sl.cursor, (unsigned long long)nw * run);
+            }
             b = __shfl_sync(FULLMASK, b, 0);
-            if (b + (unsigned long long)nw * kRun >= sl.n_pos) exhausted = true;
+            run = __shfl_sync(FULLMASK, run, 0);
+            if (b + (unsigned long long)nw * run >= sl.n_pos) exhausted = true;
             if (want && rpos >= rend) {
-              const uint64_t st = b + (uint64_t)rank * kRun;
+              const uint64_t st = b + (uint64_t)rank * run;
               rpos = st < sl.n_pos ? st : sl.n_pos;
-              rend = st + kRun < sl.n_pos ? st + kRun : sl.n_pos;
+              rend = st + run < sl.n_pos ? st + run : sl.n_pos;
             }
           }
           const bool take = want && rpos < rend;
@@ -747,9 +761,9 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         for (int c = 0; c < V; ++c) {
           seen[c] = cw[c];
           if (hF[c] < 0 && gF[c] < (int)(cw[c] & 0xffffu))
-            hF[c] = ((volatile T*)ring)[REC(0, c).in_off + (gF[c] & KM) * RS];
+            hF[c] = ring[REC(0, c).in_off + (gF[c] & KM) * RS];  // plain load: __syncwarp orders it
           if (hB[c] < 0 && gB[c] < (int)(cw[c] >> 16))
-            hB[c] = ((volatile T*)ring)[REC(1, c).in_off + (gB[c] & KM) * RS];
+            hB[c] = ring[REC(1, c).in_off + (gB[c] & KM) * RS];
           if (gF[c] < m && ((fitmask >> c) & 1u)) {
             if (hF[c] >= 0) { okF |= 1u << c; rmin = hF[c] < rmin ? hF[c] : rmin; }
             else g_unk |= 1u << c;
@@ -847,7 +861,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
 #pragma unroll
         for (int c = 0; c < V; ++c) fitmask |= (dyn <= gaux[c * 32 + lane].gate ? 1u : 0u) << c;
         if (tgt >= 0) {  // publish the arrival, then count it for the consumer
-          ((volatile T*)ring)[rc.out_off + (aj & KM) * RS] = fin + rc.oc;
+          ring[rc.out_off + (aj & KM) * RS] = fin + rc.oc;
           if (kGreedyCommits > 1) __threadfence_block();  // readers within this round
           atomicAdd(&cntw[(tgt >> 3) * 4 + (tgt & 7)], dir == 1 ? 0x10000u : 1u);
         }
