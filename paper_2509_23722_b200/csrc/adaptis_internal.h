@@ -94,7 +94,7 @@ ADAPTIS_LAYOUT_HD WarpLayout warp_layout(int S, int G, int V, int K, int tsz, in
   l.rec_off = off;  off += 3 * V * 32 * rsz;
   l.dmem_off = off; off += 3 * V * 32 * 8;
   l.cuts_off = off; off += align16(G * (S + 1) * 2);
-  l.cnt_off = off;  off += 32 * 4 * 4;  // GREEDY produced-count words [lane][chunk]
+  l.cnt_off = off;  off += 32 * 4 * 4;  // GREEDY produced-count words [chunk][lane]
   l.gaux_off = off; off += align16(V * 32 * gaux_sz);  // GREEDY per-chunk statics
   l.cold_off = off; off += 32 * 56;                    // per-lane cold state (LaneCold)
   l.ring_off = off; if (!gring) off += 2 * K * G * S * tsz;

@@ -76,7 +76,7 @@ struct __align__(16) Rec {  // one task kind of one own stage (chunk) of a lane
 };
 
 template <typename T>
-struct GAux {      // GREEDY statics of one (lane, chunk), read off the critical path
+struct GAux {      // GREEDY statics of one (lane, chunk); stored as SoA, this fixes the size
   int64_t gate;    // F of the chunk fits under Eq. 2 iff dyn <= gate (R14)
   int32_t tF, tB;  // consumer (lane << 3 | chunk) of the F / B output, -1: none
   T pF, pB;        // cost of the cross-device predecessor of an unknown F / B head
@@ -216,14 +216,23 @@ __device__ __forceinline__ uint64_t pos_to_index(const SegLaunch& sl, uint64_t p
 // register budget (measured on B200, DESIGN.md §4 "Occupancy"): every policy
 // runs best at <= 102 registers (5 CTAs of 4 warps per SM); GREEDY with its
 // rings in global memory so that shared memory does not cap occupancy
-template <int POLICY> struct MinBlocks { static constexpr int value = 5; };
 #ifndef ADAPTIS_GREEDY_MINB
 #define ADAPTIS_GREEDY_MINB 5
 #endif
-template <> struct MinBlocks<ADAPTIS_GREEDY> { static constexpr int value = ADAPTIS_GREEDY_MINB; };
+#ifndef ADAPTIS_GREEDY_V4_MINB
+#define ADAPTIS_GREEDY_V4_MINB 4
+#endif
+#ifndef ADAPTIS_FIXED_V4_MINB
+#define ADAPTIS_FIXED_V4_MINB 4
+#endif
+template <int POLICY, int V> struct MinBlocks {
+  static constexpr int value = POLICY != ADAPTIS_GREEDY
+                                   ? (V >= 3 ? ADAPTIS_FIXED_V4_MINB : 5)
+                                   : (V >= 3 ? ADAPTIS_GREEDY_V4_MINB : ADAPTIS_GREEDY_MINB);
+};
 
 template <int POLICY, int V, typename T, bool GRING>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, MinBlocks<POLICY>::value)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MinBlocks<POLICY, V>::value)
 seg_kernel(const DevTables tab, const SegLaunch sl) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr bool FUSED = (POLICY == ADAPTIS_GPIPE || POLICY == ADAPTIS_ONEF1B);
@@ -291,8 +300,14 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   Rec<T>* recs = reinterpret_cast<Rec<T>*>(wbase + lay.rec_off);
   int64_t* dmem = reinterpret_cast<int64_t*>(wbase + lay.dmem_off);
   int16_t* cuts_all = reinterpret_cast<int16_t*>(wbase + lay.cuts_off);
-  unsigned* cntw = reinterpret_cast<unsigned*>(wbase + lay.cnt_off);  // [lane][chunk]
-  GAux<T>* gaux = reinterpret_cast<GAux<T>*>(wbase + lay.gaux_off);    // [chunk][lane]
+  unsigned* cntw = reinterpret_cast<unsigned*>(wbase + lay.cnt_off);  // [chunk][lane]
+  // GREEDY statics, structure of arrays [field][chunk][lane] (conflict-free; the
+  // GAux struct only fixes the region size)
+  int64_t* ga_gate = reinterpret_cast<int64_t*>(wbase + lay.gaux_off);
+  int32_t* ga_tF = reinterpret_cast<int32_t*>(ga_gate + V * 32);
+  int32_t* ga_tB = ga_tF + V * 32;
+  T* ga_pF = reinterpret_cast<T*>(ga_tB + V * 32);
+  T* ga_pB = ga_pF + V * 32;
   LaneCold& cold = reinterpret_cast<LaneCold*>(wbase + lay.cold_off)[threadIdx.x & 31];
   cold.idx = 0; cold.busy = 0; cold.key = ~0ull >> 1; cold.invalid = 0; cold.tasks = 0; cold.live = 0;
   cold.pruned = 0;
@@ -585,18 +600,18 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
                   pb = (T)dsum(kColTB, b, b1) + lat(b - 1);
                   bl = dev_of(sl.placement, p, s + 1) == (d == 0 ? p - 1 : d - 1);
                 }
-                GAux<T> ga;
-                ga.gate = 0;  // set below, once stat is complete
-                ga.pF = pf;
-                ga.pB = pb;
-                ga.tF = s < S - 1 ? (((leader + dev_of(sl.placement, p, s + 1)) << 3) | ((s + 1) / p)) : -1;
-                ga.tB = s > 0 ? (((leader + dev_of(sl.placement, p, s - 1)) << 3) | ((s - 1) / p)) : -1;
-                gaux[c * 32 + lane] = ga;
+                // gate is set below, once stat is complete
+                ga_pF[c * 32 + lane] = pf;
+                ga_pB[c * 32 + lane] = pb;
+                ga_tF[c * 32 + lane] =
+                    s < S - 1 ? (((leader + dev_of(sl.placement, p, s + 1)) << 3) | ((s + 1) / p)) : -1;
+                ga_tB[c * 32 + lane] =
+                    s > 0 ? (((leader + dev_of(sl.placement, p, s - 1)) << 3) | ((s - 1) / p)) : -1;
                 s0mask = (s0mask & ~(1u << c)) | ((s == 0 ? 1u : 0u) << c);
                 lastmask = (lastmask & ~(1u << c)) | ((s == S - 1 ? 1u : 0u) << c);
                 hF[c] = s == 0 ? (T)0 : (T)-1;
                 hB[c] = s == S - 1 ? (T)0 : (T)-1;
-                cntw[lane * 4 + c] = 0;
+                cntw[c * 32 + lane] = 0;
                 pleft = (pleft & ~((1u << c) | (1u << (V + c)))) | ((fl ? 1u : 0u) << c) |
                         ((bl ? 1u : 0u) << (V + c));
               }
@@ -630,7 +645,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
                 seen[c] = 0xffffffffu;
                 if (lane_on) {
                   const int64_t gate = sl.cap - stat - ac[c];  // cap - stat cannot overflow
-                  gaux[c * 32 + lane].gate = gate;
+                  ga_gate[c * 32 + lane] = gate;
                   fitmask |= (0 <= gate ? 1u : 0u) << c;
                 }
               }
@@ -749,7 +764,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         bool dirty = gdirty || force;
 #pragma unroll
         for (int c = 0; c < V; ++c) {
-          cw[c] = ((volatile unsigned*)cntw)[lane * 4 + c];
+          cw[c] = ((volatile unsigned*)cntw)[c * 32 + lane];
           dirty = dirty || cw[c] != seen[c];
         }
         if (!dirty) return;
@@ -818,11 +833,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
 #pragma unroll
         for (int c = 0; c < V; ++c) {
           if (g_unk & (1u << c)) {
-            const T x = sat_add((pleft >> c) & 1u ? nl : nr, gaux[c * 32 + lane].pF);
+            const T x = sat_add((pleft >> c) & 1u ? nl : nr, ga_pF[c * 32 + lane]);
             bound = x < bound ? x : bound;
           }
           if (g_unk & (1u << (V + c))) {
-            const T x = sat_add((pleft >> (V + c)) & 1u ? nl : nr, gaux[c * 32 + lane].pB);
+            const T x = sat_add((pleft >> (V + c)) & 1u ? nl : nr, ga_pB[c * 32 + lane]);
             bound = x < bound ? x : bound;
           }
         }
@@ -841,8 +856,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         if (ak == 0) peak = dyn > peak ? dyn : peak;
         int tgt = -1;
         const int dir = ak;
-        if (ak == 0) tgt = gaux[acx * 32 + lane].tF;
-        else if (ak == 1) tgt = gaux[acx * 32 + lane].tB;
+        if (ak == 0) tgt = ga_tF[acx * 32 + lane];
+        else if (ak == 1) tgt = ga_tB[acx * 32 + lane];
 #pragma unroll
         for (int c = 0; c < V; ++c) {
           if (c == acx) {
@@ -859,11 +874,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         }
         fitmask = 0;  // dyn changed: refresh the Eq. 2 gates
 #pragma unroll
-        for (int c = 0; c < V; ++c) fitmask |= (dyn <= gaux[c * 32 + lane].gate ? 1u : 0u) << c;
+        for (int c = 0; c < V; ++c) fitmask |= (dyn <= ga_gate[c * 32 + lane] ? 1u : 0u) << c;
         if (tgt >= 0) {  // publish the arrival, then count it for the consumer
           ring[rc.out_off + (aj & KM) * RS] = fin + rc.oc;
           if (kGreedyCommits > 1) __threadfence_block();  // readers within this round
-          atomicAdd(&cntw[(tgt >> 3) * 4 + (tgt & 7)], dir == 1 ? 0x10000u : 1u);
+          atomicAdd(&cntw[(tgt & 7) * 32 + (tgt >> 3)], dir == 1 ? 0x10000u : 1u);
         }
         bool all = true;
 #pragma unroll
