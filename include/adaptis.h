@@ -261,6 +261,59 @@ ADAPTIS_API adaptis_status adaptis_shard_indices(const adaptis_problem* problem,
                                                  const adaptis_space* space, int rank, int world,
                                                  uint64_t* out, uint64_t cap, uint64_t* n_out);
 
+/* Evaluate an explicit list of plans (Alg. 1 Steps 1-3 per plan),
+ * e.g. the neighbourhood of one Pipeline Generator step. `prep`
+ * must have been prepared from the same problem (any space; its tables are
+ * reused). Plan i: S == p*v, 1 <= v <= 4, S <= min(64, L), v > 1 requires
+ * m % p == 0, and (placement, policy) must be a combo of R12 (WAVE admits only
+ * GPIPE and GREEDY); else EINVAL naming the plan. cuts[0] and cuts[S] are taken
+ * as 0 and L; cuts that are not strictly increasing give status 1 (INVALID).
+ * Results go to host arrays `out` (n entries each) in plan order; `report`,
+ * when non-NULL, is a host array [n][3][p] receiving T_d, busy_d and M_d of
+ * every plan with status 0 or 2 (untouched otherwise). Not in FP32 cost mode
+ * (EINVAL). The context's GPU evaluates the whole list. */
+ADAPTIS_API adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared* prep,
+                                              const adaptis_plan* plans, uint64_t n,
+                                              const adaptis_results_soa* out, int64_t* report);
+
+/* Pipeline Generator (§4.3; reading R28 in DESIGN.md): seeds from the
+ * baseline partitions (S-1F1B equal-layer and Mist min-max, R20), placements
+ * (S-1F1B, I-1F1B, Hanayo) and schedules (S-1F1B, ZB) of P:346, then rounds of
+ * phase-by-phase tuning with rollback: partition (the exact
+ * best of the L1 ball of radius `radius` around the current cuts, one GPU
+ * search), placement (grouped stage-device permutations and v changes)
+ * and schedule (every policy of R12), each accepted only if it
+ * strictly lowers the makespan, until a round changes nothing. */
+typedef struct {
+  uint32_t vs_mask;          /* bit v-1 admits v virtual stages per device; 0 = {1, 2}        */
+  int32_t  radius;           /* partition-phase L1 radius, >= 1; 0 = 2                        */
+  int32_t  max_rounds;       /* tuning rounds, >= 1; 0 = 32                                   */
+} adaptis_gen_options;
+
+#define ADAPTIS_GEN_MAX_STEPS 128
+enum { ADAPTIS_GEN_SEED = 0, ADAPTIS_GEN_PARTITION = 1, ADAPTIS_GEN_PLACEMENT = 2,
+       ADAPTIS_GEN_SCHEDULE = 3 };
+
+typedef struct {
+  adaptis_plan plan;         /* the co-optimised pipeline                                     */
+  adaptis_result result;
+  int32_t p;
+  int64_t T_d[ADAPTIS_MAX_P], busy_d[ADAPTIS_MAX_P], M_d[ADAPTIS_MAX_P];
+  int32_t n_seeds;           /* seed plans evaluated                                          */
+  int32_t rounds;            /* tuning rounds run (the last one changed nothing)              */
+  uint64_t n_evaluated;      /* plans simulated in total (seeds + every neighbourhood)        */
+  int32_t n_steps;           /* accepted steps: the chosen seed, then each accepted tuning    */
+  int32_t step_phase[ADAPTIS_GEN_MAX_STEPS];     /* ADAPTIS_GEN_*                             */
+  int64_t step_makespan[ADAPTIS_GEN_MAX_STEPS];  /* makespan after the step (strictly falling) */
+  float   kernel_ms;         /* device time of all evaluation kernels                         */
+} adaptis_gen_result;
+
+/* EINVAL on an invalid problem/options (or FP32 cost mode); EINFEASIBLE if no
+ * seed satisfies Eq. 2 (out->n_steps = 0). */
+ADAPTIS_API adaptis_status adaptis_generate(adaptis_ctx* ctx, const adaptis_problem* problem,
+                                            const adaptis_gen_options* options,
+                                            adaptis_gen_result* out);
+
 /* Message of the last failure on `ctx` (or of the calling thread when ctx is NULL). */
 ADAPTIS_API const char*    adaptis_last_error(const adaptis_ctx* ctx);
 ADAPTIS_API const char*    adaptis_status_str(adaptis_status s);

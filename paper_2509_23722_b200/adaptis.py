@@ -79,6 +79,23 @@ class _Best(C.Structure):
                 ("n_pruned", C.c_uint64), ("kernel_ms", C.c_float)]
 
 
+class _GenOptions(C.Structure):
+    _fields_ = [("vs_mask", C.c_uint32), ("radius", C.c_int32), ("max_rounds", C.c_int32)]
+
+
+GEN_MAX_STEPS = 128
+GEN_PHASES = {0: "seed", 1: "partition", 2: "placement", 3: "schedule"}
+
+
+class _GenResult(C.Structure):
+    _fields_ = [("plan", _Plan), ("result", _Result), ("p", C.c_int32),
+                ("T_d", C.c_int64 * MAX_P), ("busy_d", C.c_int64 * MAX_P),
+                ("M_d", C.c_int64 * MAX_P), ("n_seeds", C.c_int32), ("rounds", C.c_int32),
+                ("n_evaluated", C.c_uint64), ("n_steps", C.c_int32),
+                ("step_phase", C.c_int32 * GEN_MAX_STEPS), ("step_makespan", C.c_int64 * GEN_MAX_STEPS),
+                ("kernel_ms", C.c_float)]
+
+
 class _LaunchInfo(C.Structure):
     _fields_ = [("group", C.c_int32), ("combo", C.c_int32), ("v", C.c_int32),
                 ("placement", C.c_int32), ("policy", C.c_int32), ("fallback", C.c_int32),
@@ -145,6 +162,12 @@ def lib():
             L.adaptis_search.argtypes = [C.c_void_p, C.POINTER(_Problem), C.POINTER(_Space), C.POINTER(_Best)]
             L.adaptis_search_prepared.restype = st
             L.adaptis_search_prepared.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Best)]
+            L.adaptis_eval_plans.restype = st
+            L.adaptis_eval_plans.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_uint64,
+                                             C.POINTER(_ResultsSoa), C.POINTER(C.c_int64)]
+            L.adaptis_generate.restype = st
+            L.adaptis_generate.argtypes = [C.c_void_p, C.POINTER(_Problem), C.POINTER(_GenOptions),
+                                           C.POINTER(_GenResult)]
             _lib = L
     return _lib
 
@@ -196,6 +219,20 @@ def _check(status, ctx_ptr=None):
 def plan_dict(pl: _Plan) -> dict:
     return {"v": pl.v, "placement": pl.placement, "policy": pl.policy, "S": pl.S,
             "cuts": [int(pl.cuts[i]) for i in range(pl.S + 1)]}
+
+
+def make_plans(plans) -> "C.Array":
+    """dicts {v, placement, policy, cuts (S+1 values or S-1 interior cuts)} -> adaptis_plan[]"""
+    arr = (_Plan * max(1, len(plans)))()
+    for i, d in enumerate(plans):
+        S = int(d.get("S", 0)) or (len(d["cuts"]) - 1)
+        cuts = list(d["cuts"])
+        if len(cuts) == S - 1:
+            cuts = [0] + cuts + [0]  # cuts[0] and cuts[S] are implied (0 and L)
+        arr[i].v, arr[i].placement, arr[i].policy, arr[i].S = d["v"], d["placement"], d["policy"], S
+        for k, c in enumerate(cuts[:S + 1]):
+            arr[i].cuts[k] = int(c)
+    return arr
 
 
 def space_size(pr: W.Problem, sp: W.Space) -> int:
@@ -332,6 +369,24 @@ class Context:
         st = lib().adaptis_search(self.ptr, C.byref(m.problem), C.byref(m.space), C.byref(b))
         return _best_dict(b, st, self.ptr)
 
+    def generate(self, pr: W.Problem, vs_mask: int = 0, radius: int = 0, max_rounds: int = 0) -> dict:
+        """adaptis_generate: the Pipeline Generator (R28) on this GPU."""
+        m = _Marshal(pr)
+        o = _GenOptions(vs_mask=vs_mask, radius=radius, max_rounds=max_rounds)
+        r = _GenResult()
+        st = lib().adaptis_generate(self.ptr, C.byref(m.problem), C.byref(o), C.byref(r))
+        if st not in (OK, EINFEASIBLE):
+            raise AdaptisError(st, _err(self.ptr))
+        p = r.p
+        n = r.n_steps
+        return {"status": st, "plan": plan_dict(r.plan), "makespan": int(r.result.makespan),
+                "peak_mem": int(r.result.peak_mem_bytes), "bubble": float(r.result.bubble_ratio),
+                "throughput": float(r.result.throughput), "cand_status": int(r.result.status),
+                "T_d": list(r.T_d[:p]), "busy_d": list(r.busy_d[:p]), "M_d": list(r.M_d[:p]),
+                "n_seeds": int(r.n_seeds), "rounds": int(r.rounds), "n_evaluated": int(r.n_evaluated),
+                "steps": [(GEN_PHASES[int(r.step_phase[i])], int(r.step_makespan[i])) for i in range(n)],
+                "kernel_ms": float(r.kernel_ms)}
+
 
 class Prepared:
     """Problem tables resident in HBM (adaptis_prepare) for repeated evaluation."""
@@ -359,6 +414,20 @@ class Prepared:
         b = _Best()
         st = lib().adaptis_search_prepared(self.ctx.ptr, self.ptr, C.byref(b))
         return _best_dict(b, st, self.ctx.ptr)
+
+    def eval_plans(self, plans, report: bool = False) -> dict:
+        """adaptis_eval_plans: results (and optionally T_d/busy_d/M_d) of explicit plans."""
+        n = len(plans)
+        arr = make_plans(plans)
+        out = _host_results(n)
+        soa = _soa_from_numpy(out)
+        rep = np.zeros((max(n, 1), 3, self.m.problem.p), np.int64) if report else None
+        _check(lib().adaptis_eval_plans(self.ctx.ptr, self.ptr, arr, n, C.byref(soa),
+                                        rep.ctypes.data_as(C.POINTER(C.c_int64)) if report else None),
+               self.ctx.ptr)
+        if report:
+            out["T_d"], out["busy_d"], out["M_d"] = rep[:n, 0], rep[:n, 1], rep[:n, 2]
+        return out
 
     def eval(self, first: int, count: int, device_out: bool = False):
         """Results for [first, first+count): numpy (host) or torch CUDA tensors."""

@@ -409,7 +409,7 @@ int ring_slots(int policy, int m) {
   return pw;
 }
 constexpr uint64_t kSeedPass = 4096;  // indices per segment in the pruned search's seed pass
-constexpr size_t kHdr = 8;  // [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds
+constexpr size_t kHdr = 8;  // [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds [5] pruned
 constexpr size_t kGreedySmemRing = 0;  // per warp: GREEDY rings live in global memory (L2)
 
 // global-memory ring scratch for a launch with s.ring_k slots; bounds the grid
@@ -446,20 +446,29 @@ SegLaunch make_launch(const adaptis_prepared* P, const Seg& sg) {
   return s;
 }
 
-// Evaluate [lo, hi) (global indices) on this context's GPU: every segment it
-// touches is launched; overflowed candidates are re-run by the fallback kernel.
-// mode_search: pack keys into d_key; else write SoA results at idx - eval_first.
-// Scratch words: [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds,
-// then per segment i at kHdr + kSegWords*i: [0] cursor [1] overflow count
-// [2] tasks [3] fallback cursor [4] fallback overflow count.
+// One kernel launch of an evaluation: a segment of the canonical order (or a
+// group of explicit plans) with its sharded position range, and the record
+// reported through adaptis_ctx_launch_info.
+struct Job {
+  SegLaunch s;
+  adaptis_launch_info info;
+};
+
+// Scratch words: [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds
+// [5] pruned, then per job i at kHdr + kSegWords*i: [0] cursor [1] overflow
+// count [2] tasks [3] fallback cursor [4] fallback overflow count.
 constexpr size_t kSegWords = 6;
-adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uint64_t hi,
-                         bool mode_search, int rank, int world, const adaptis_results_soa* dout,
-                         uint64_t eval_first, int64_t* report, float* kernel_ms,
-                         bool keep_key = false) {
-  const size_t nseg = P->segs.size();
-  const size_t nwords = kHdr + kSegWords * nseg;
-  adaptis_status st = ensure_scratch(ctx, nwords, kOverflowPerSeg * nseg);
+
+// Launch every job on this context's stream; candidates whose fast-path rings
+// filled up are re-run by the fallback kernel (exact, rings >= m).
+// mode_search: pack keys into the key word; else write SoA results at
+// idx - eval_first (and per-candidate reports when `report` is set).
+adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>& jobs,
+                        bool mode_search, const adaptis_results_soa* dout, uint64_t eval_first,
+                        int64_t* report, float* kernel_ms, bool keep_key) {
+  const size_t nseg = jobs.size();
+  const size_t nwords = kHdr + kSegWords * std::max<size_t>(nseg, 1);
+  adaptis_status st = ensure_scratch(ctx, nwords, kOverflowPerSeg * std::max<size_t>(nseg, 1));
   if (st != ADAPTIS_OK) return st;
   while (ctx->seg_events.size() < 2 * nseg) {
     cudaEvent_t e;
@@ -474,15 +483,9 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
   else
     CU(ctx, cudaMemcpyAsync(W, init.data(), nwords * 8, cudaMemcpyHostToDevice, ctx->stream));
   CU(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
-  std::vector<SegLaunch> launched(nseg);
   std::vector<char> active(nseg, 0);
   for (size_t i = 0; i < nseg; ++i) {
-    const Seg& sg = P->segs[i];
-    const uint64_t a = std::max(lo, sg.base), b = std::min(hi, sg.base + sg.count);
-    if (a >= b) continue;
-    SegLaunch s = make_launch(P, sg);
-    shard(a, b, rank, world, &s);
-    s.lo = a; s.hi = b;
+    SegLaunch& s = jobs[i].s;
     if (s.n_pos == 0) continue;
     unsigned long long* sw = W + kHdr + kSegWords * i;
     s.key = mode_search ? W : nullptr;
@@ -522,7 +525,6 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     if (e) return fail(ctx, ADAPTIS_ECUDA, "kernel launch (segment %zu): %s", i, cudaGetErrorString((cudaError_t)e));
     CU(ctx, cudaEventRecord(ctx->seg_events[2 * i + 1], ctx->stream));
     ctx->launches++;
-    launched[i] = s;
     active[i] = 1;
   }
   // fallback for candidates whose fast-path rings filled up (exact re-run, rings >= m)
@@ -537,7 +539,7 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     const unsigned int cnt = (unsigned int)(words[kHdr + kSegWords * i + 1] & 0xffffffffu);
     if (cnt == 0) continue;
     ctx->fallback_cands += cnt;
-    SegLaunch s = launched[i];
+    SegLaunch s = jobs[i].s;
     int K = 1;
     while (K < P->m) K <<= 1;
     s.ring_k = K;
@@ -572,10 +574,8 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     if (!active[i]) continue;
     float fb = 0.0f;
     if (active[i] == 2) CU(ctx, cudaEventElapsedTime(&fb, ctx->seg_events[2 * i], ctx->seg_events[2 * i + 1]));
-    const Seg& sg = P->segs[i];
-    adaptis_launch_info li{};
-    li.group = sg.group; li.combo = sg.combo; li.v = sg.v; li.placement = sg.placement;
-    li.policy = sg.policy; li.candidates = launched[i].n_pos;
+    adaptis_launch_info li = jobs[i].info;
+    li.candidates = jobs[i].s.n_pos;
     li.tasks = words[kHdr + kSegWords * i + 2];
     li.ms = seg_ms[i] + fb;
     li.fallback = active[i] == 2 ? (int32_t)(words[kHdr + kSegWords * i + 1] & 0xffffffffu) : 0;
@@ -584,6 +584,164 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
   }
   ctx->counters[0] += tasks;
   ctx->last_tasks = tasks;
+  return ADAPTIS_OK;
+}
+
+// Evaluate [lo, hi) (global indices) on this context's GPU: one job per
+// segment the range touches, sharded block-cyclically over `world` ranks.
+adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uint64_t hi,
+                         bool mode_search, int rank, int world, const adaptis_results_soa* dout,
+                         uint64_t eval_first, int64_t* report, float* kernel_ms,
+                         bool keep_key = false) {
+  std::vector<Job> jobs;
+  for (const Seg& sg : P->segs) {
+    const uint64_t a = std::max(lo, sg.base), b = std::min(hi, sg.base + sg.count);
+    if (a >= b) continue;
+    Job j{};
+    j.s = make_launch(P, sg);
+    shard(a, b, rank, world, &j.s);
+    j.s.lo = a; j.s.hi = b;
+    if (j.s.n_pos == 0) continue;
+    j.info.group = sg.group; j.info.combo = sg.combo; j.info.v = sg.v;
+    j.info.placement = sg.placement; j.info.policy = sg.policy;
+    jobs.push_back(j);
+  }
+  return run_jobs(ctx, P, jobs, mode_search, dout, eval_first, report, kernel_ms, keep_key);
+}
+
+void fill_plan(const adaptis_prepared& P, uint64_t index, adaptis_plan* out, bool* valid) {
+  memset(out, 0, sizeof(*out));
+  for (const Seg& s : P.segs) {
+    if (index < s.base || index >= s.base + s.count) continue;
+    out->v = s.v; out->placement = s.placement; out->policy = s.policy; out->S = s.S;
+    bool ok = decode_cuts(P.h_binom.data(), P.h_ball.data(), P.h_seeds.data(), s.group, s.part_mode,
+                          s.radius, s.S, P.L, index - s.base, out->cuts);
+    if (valid) *valid = ok;
+    return;
+  }
+}
+
+// (placement, policy) admitted for v by the combo table (R12), and its combo bit
+int combo_bit(int v, int placement, int policy) {
+  for (int k = 0; k < 6; ++k) {
+    int pl, po;
+    if (combo_of(v, k, &pl, &po) && pl == placement && po == policy) return k;
+  }
+  return -1;
+}
+
+// Explicit plans on the device: one job per (v, placement, policy) group,
+// positions mapped to plan (= output) indices in the caller's order.
+adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plans,
+                         uint64_t n, std::vector<int64_t>* mk, std::vector<int64_t>* peak,
+                         std::vector<float>* bubble, std::vector<uint8_t>* status,
+                         std::vector<int64_t>* report, float* kernel_ms) {
+  for (uint64_t i = 0; i < n; ++i) {
+    const adaptis_plan& pl = plans[i];
+    if (pl.v < 1 || pl.v > ADAPTIS_MAX_V)
+      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu].v = %d not in [1, 4]", (unsigned long long)i, pl.v);
+    if (pl.S != P->p * pl.v || pl.S > ADAPTIS_MAX_S || pl.S > P->L)
+      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu].S = %d (need p*v = %d <= min(64, L = %d))",
+                  (unsigned long long)i, pl.S, P->p * pl.v, P->L);
+    if (pl.v > 1 && P->m % P->p != 0)
+      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: v > 1 requires m %% p == 0 (R10)", (unsigned long long)i);
+    if (combo_bit(pl.v, pl.placement, pl.policy) < 0)
+      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: (placement %d, policy %d) is not a combo for v = %d (R12)",
+                  (unsigned long long)i, pl.placement, pl.policy, pl.v);
+  }
+  mk->assign(n, INT64_MAX);
+  if (peak) peak->assign(n, 0);
+  if (bubble) bubble->assign(n, 0.0f);
+  status->assign(n, 0);
+  if (report) report->assign((size_t)n * 3 * P->p, 0);
+  if (n == 0) return ADAPTIS_OK;
+  constexpr int CS = ADAPTIS_MAX_S + 1;
+  std::vector<int16_t> hcuts((size_t)n * CS, 0);
+  std::vector<std::vector<uint64_t>> groups(64);  // key (v-1)*16 + placement*4 + policy
+  for (uint64_t i = 0; i < n; ++i) {
+    const adaptis_plan& pl = plans[i];
+    int16_t* c = &hcuts[(size_t)i * CS];
+    for (int k = 1; k < pl.S; ++k) c[k] = pl.cuts[k];
+    c[0] = 0;
+    c[pl.S] = (int16_t)P->L;
+    groups[(pl.v - 1) * 16 + pl.placement * 4 + pl.policy].push_back(i);
+  }
+  std::vector<uint64_t> order;
+  order.reserve(n);
+  for (auto& g : groups) order.insert(order.end(), g.begin(), g.end());
+  CU(ctx, cudaSetDevice(ctx->device));
+  int16_t* d_cuts = nullptr; uint64_t* d_order = nullptr;
+  int64_t *d_mk = nullptr, *d_pk = nullptr, *d_rep = nullptr; float* d_bub = nullptr; uint8_t* d_st = nullptr;
+  adaptis_status st = ADAPTIS_OK;
+  auto cleanup = [&]() {
+    cudaFree(d_cuts); cudaFree(d_order); cudaFree(d_mk); cudaFree(d_pk); cudaFree(d_rep);
+    cudaFree(d_bub); cudaFree(d_st);
+  };
+#define CUP(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { cleanup(); \
+    return fail(ctx, ADAPTIS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
+  CUP(cudaMalloc(&d_cuts, hcuts.size() * 2));
+  CUP(cudaMalloc(&d_order, n * 8));
+  CUP(cudaMalloc(&d_mk, n * 8));
+  CUP(cudaMalloc(&d_pk, n * 8));
+  CUP(cudaMalloc(&d_bub, n * 4));
+  CUP(cudaMalloc(&d_st, n));
+  if (report) {
+    CUP(cudaMalloc(&d_rep, (size_t)n * 3 * P->p * 8));
+    CUP(cudaMemsetAsync(d_rep, 0, (size_t)n * 3 * P->p * 8, ctx->stream));
+  }
+  CUP(cudaMemcpyAsync(d_cuts, hcuts.data(), hcuts.size() * 2, cudaMemcpyHostToDevice, ctx->stream));
+  CUP(cudaMemcpyAsync(d_order, order.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  std::vector<Job> jobs;
+  uint64_t off = 0;
+  for (int key = 0; key < 64; ++key) {
+    const auto& g = groups[key];
+    if (g.empty()) continue;
+    const adaptis_plan& pl = plans[g[0]];
+    Seg sg{};
+    sg.group = 0; sg.combo = combo_bit(pl.v, pl.placement, pl.policy); sg.v = pl.v; sg.S = pl.S;
+    sg.placement = pl.placement; sg.policy = pl.policy; sg.part_mode = ADAPTIS_PART_FULL;
+    sg.base = 0; sg.count = n;
+    Job j{};
+    j.s = make_launch(P, sg);
+    j.s.lo = 0; j.s.hi = n; j.s.seg_base = 0;
+    j.s.n_pos = g.size(); j.s.n0 = g.size(); j.s.world = 1;
+    j.s.list_out = d_order + off;
+    j.s.list_cuts = d_cuts;
+    j.info.group = -1; j.info.combo = sg.combo; j.info.v = pl.v;
+    j.info.placement = pl.placement; j.info.policy = pl.policy;
+    jobs.push_back(j);
+    off += g.size();
+  }
+  adaptis_results_soa dout{d_mk, d_pk, d_bub, d_st, nullptr};
+  st = run_jobs(ctx, P, jobs, false, &dout, 0, d_rep, kernel_ms, false);
+  if (st != ADAPTIS_OK) { cleanup(); return st; }
+  CUP(cudaMemcpyAsync(mk->data(), d_mk, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (peak) CUP(cudaMemcpyAsync(peak->data(), d_pk, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (bubble) CUP(cudaMemcpyAsync(bubble->data(), d_bub, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CUP(cudaMemcpyAsync(status->data(), d_st, n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (report) CUP(cudaMemcpyAsync(report->data(), d_rep, (size_t)n * 3 * P->p * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUP(cudaStreamSynchronize(ctx->stream));
+#undef CUP
+  cleanup();
+  return ADAPTIS_OK;
+}
+
+// Best (makespan, lowest index) of a prepared space on this GPU alone (no
+// sharding, no allreduce): the generator's partition phase. Returns
+// EINFEASIBLE when nothing is feasible.
+adaptis_status best_of_space(adaptis_ctx* ctx, adaptis_prepared* P, adaptis_plan* plan,
+                             int64_t* makespan, float* kernel_ms) {
+  float t = 0;
+  adaptis_status st = run_range(ctx, P, 0, P->N, true, 0, 1, nullptr, 0, nullptr, &t);
+  if (kernel_ms) *kernel_ms += t;
+  if (st != ADAPTIS_OK) return st;
+  unsigned long long key = 0;
+  CU(ctx, cudaMemcpyAsync(&key, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  if (key == (~0ull >> 1)) return ADAPTIS_EINFEASIBLE;
+  const uint64_t idx = key & ((1ull << P->key_bits) - 1);
+  fill_plan(*P, idx, plan, nullptr);
+  *makespan = (int64_t)(key >> P->key_bits);
   return ADAPTIS_OK;
 }
 
@@ -674,18 +832,6 @@ adaptis_status adaptis_space_size(const adaptis_problem* problem, const adaptis_
   if (st != ADAPTIS_OK) return st;
   *n_out = P.N;
   return ADAPTIS_OK;
-}
-
-static void fill_plan(const adaptis_prepared& P, uint64_t index, adaptis_plan* out, bool* valid) {
-  memset(out, 0, sizeof(*out));
-  for (const Seg& s : P.segs) {
-    if (index < s.base || index >= s.base + s.count) continue;
-    out->v = s.v; out->placement = s.placement; out->policy = s.policy; out->S = s.S;
-    bool ok = decode_cuts(P.h_binom.data(), P.h_ball.data(), P.h_seeds.data(), s.group, s.part_mode,
-                          s.radius, s.S, P.L, index - s.base, out->cuts);
-    if (valid) *valid = ok;
-    return;
-  }
 }
 
 adaptis_status adaptis_decode(const adaptis_problem* problem, const adaptis_space* space,
@@ -862,6 +1008,235 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   if (P->tick == kTickF32) { float f; uint32_t u = (uint32_t)kv; memcpy(&f, &u, 4); agree = f == mkf; }
   else agree = mk == (int64_t)kv;
   if (!agree) return fail(ctx, ADAPTIS_ECUDA, "winner re-evaluation disagrees with its search key");
+  return ADAPTIS_OK;
+}
+
+adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plans,
+                                  uint64_t n, const adaptis_results_soa* out, int64_t* report) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");
+  if (n && !plans) return fail(ctx, ADAPTIS_EINVAL, "plans is NULL");
+  if (P->tick == kTickF32) return fail(ctx, ADAPTIS_EINVAL, "adaptis_eval_plans: FP32 cost mode is not supported");
+  std::vector<int64_t> mk, pk, rep;
+  std::vector<float> bub;
+  std::vector<uint8_t> stt;
+  adaptis_status st = run_plans(ctx, P, plans, n, &mk, &pk, &bub, &stt, report ? &rep : nullptr, nullptr);
+  if (st != ADAPTIS_OK) return st;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (out->makespan) out->makespan[i] = mk[i];
+    if (out->peak_mem_bytes) out->peak_mem_bytes[i] = pk[i];
+    if (out->bubble_ratio) out->bubble_ratio[i] = bub[i];
+    if (out->status) out->status[i] = stt[i];
+    if (out->makespan_f32) out->makespan_f32[i] = stt[i] == 0 ? (float)mk[i] : INFINITY;
+  }
+  if (report)
+    for (uint64_t i = 0; i < n; ++i)
+      if (stt[i] == ADAPTIS_CAND_OK || stt[i] == ADAPTIS_CAND_OVER_CAP)
+        memcpy(report + (size_t)i * 3 * P->p, rep.data() + (size_t)i * 3 * P->p, (size_t)3 * P->p * 8);
+  return ADAPTIS_OK;
+}
+
+// Pipeline Generator (reading R28): seeds, then rounds of
+// partition / placement / schedule tuning, each accepted only if it strictly
+// lowers the makespan (rollback otherwise), until a round changes nothing.
+adaptis_status adaptis_generate(adaptis_ctx* ctx, const adaptis_problem* problem,
+                                const adaptis_gen_options* options, adaptis_gen_result* out) {
+  if (!ctx) return fail(nullptr, ADAPTIS_EINVAL, "ctx is NULL");
+  if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");
+  memset(out, 0, sizeof(*out));
+  adaptis_gen_options o{};
+  if (options) o = *options;
+  const uint32_t vs_mask = o.vs_mask ? o.vs_mask : 0x3u;
+  const int R = o.radius ? o.radius : 2;
+  const int max_rounds = o.max_rounds ? o.max_rounds : 32;
+  if (R < 1 || R > kMaxRadius) return fail(ctx, ADAPTIS_EINVAL, "options.radius = %d not in [1, %d]", R, kMaxRadius);
+  if (max_rounds < 1) return fail(ctx, ADAPTIS_EINVAL, "options.max_rounds = %d < 1", max_rounds);
+  if (vs_mask & ~0xFu) return fail(ctx, ADAPTIS_EINVAL, "options.vs_mask = 0x%x admits v > 4", vs_mask);
+  if (!problem) return fail(ctx, ADAPTIS_EINVAL, "problem is NULL");
+  if (problem->cost_type != ADAPTIS_COST_TICKS)
+    return fail(ctx, ADAPTIS_EINVAL, "adaptis_generate: FP32 cost mode is not supported");
+  const int L = problem->layers.L, p = problem->p, m = problem->m;
+  // admitted v values (ascending): S = p*v <= min(64, L); v > 1 needs m % p == 0 (R10)
+  std::vector<int> vs;
+  for (int v = 1; v <= ADAPTIS_MAX_V; ++v)
+    if (((vs_mask >> (v - 1)) & 1u) && p * v <= std::min(ADAPTIS_MAX_S, L) && (v == 1 || m % p == 0))
+      vs.push_back(v);
+  if (vs.empty()) return fail(ctx, ADAPTIS_EINVAL, "options.vs_mask admits no v with p*v <= min(64, L)");
+  // tables: one prepared space (FULL v = vs[0], validated by build_space) for the plan lists
+  adaptis_space base{};
+  base.n_groups = 1;
+  base.group[0].v = vs[0];
+  base.group[0].part_mode = ADAPTIS_PART_BALL;  // any valid space: the tables only depend on the problem
+  base.group[0].radius = 0;
+  base.group[0].combo_mask = 1u << 1;
+  adaptis_prepared* P = nullptr;
+  adaptis_status st = adaptis_prepare(ctx, problem, &base, &P);
+  if (st != ADAPTIS_OK) return st;
+  float ms = 0;
+  uint64_t n_eval = 0;
+  auto mist = [&](int S, adaptis_plan* pl) {
+    int16_t c[ADAPTIS_MAX_S];
+    seed_minmax(problem->layers, S, c);
+    for (int i = 1; i < S; ++i) pl->cuts[i] = c[i - 1];
+    pl->cuts[0] = 0; pl->cuts[S] = (int16_t)L;
+  };
+  auto make = [&](int v, int placement, int policy) {
+    adaptis_plan pl{};
+    pl.v = v; pl.placement = placement; pl.policy = policy; pl.S = p * v;
+    return pl;
+  };
+  // evaluate a list, pick the first plan with the smallest makespan among status 0
+  auto eval_best = [&](const std::vector<adaptis_plan>& list, int* best, int64_t* best_mk) -> adaptis_status {
+    std::vector<int64_t> mk; std::vector<uint8_t> stt;
+    float t = 0;
+    adaptis_status s2 = run_plans(ctx, P, list.data(), list.size(), &mk, nullptr, nullptr, &stt, nullptr, &t);
+    ms += t;
+    n_eval += list.size();
+    *best = -1; *best_mk = INT64_MAX;
+    if (s2 != ADAPTIS_OK) return s2;
+    for (size_t i = 0; i < list.size(); ++i)
+      if (stt[i] == ADAPTIS_CAND_OK && mk[i] < *best_mk) { *best = (int)i; *best_mk = mk[i]; }
+    return ADAPTIS_OK;
+  };
+  auto push_step = [&](int phase, int64_t mk) {
+    if (out->n_steps < ADAPTIS_GEN_MAX_STEPS) {
+      out->step_phase[out->n_steps] = phase;
+      out->step_makespan[out->n_steps] = mk;
+      out->n_steps++;
+    }
+  };
+  // ---- seeds: partitions {equal layers (S-1F1B), min-max (Mist, R20)} x
+  // placement/schedule {S-1F1B, ZB} on SEQ (v = 1), {I-1F1B, ZB} on INTERLEAVED and
+  // Hanayo WAVE with the dynamic schedule (v >= 2; R12 admits no fixed 1F1B/ZB order on WAVE)
+  std::vector<adaptis_plan> seeds;
+  for (int v : vs) {
+    const int S = p * v;
+    for (int part = 0; part < 2; ++part) {
+      std::vector<std::pair<int, int>> combos;
+      if (v == 1) combos = {{ADAPTIS_SEQ, ADAPTIS_ONEF1B}, {ADAPTIS_SEQ, ADAPTIS_ZB}};
+      else combos = {{ADAPTIS_INTERLEAVED, ADAPTIS_ONEF1B}, {ADAPTIS_INTERLEAVED, ADAPTIS_ZB},
+                     {ADAPTIS_WAVE, ADAPTIS_GREEDY}};
+      for (auto& c : combos) {
+        adaptis_plan pl = make(v, c.first, c.second);
+        if (part == 0) {
+          for (int i = 1; i < S; ++i) pl.cuts[i] = (int16_t)((int64_t)i * L / S);
+          pl.cuts[0] = 0; pl.cuts[S] = (int16_t)L;
+        } else {
+          mist(S, &pl);
+        }
+        seeds.push_back(pl);
+      }
+    }
+  }
+  out->n_seeds = (int32_t)seeds.size();
+  int bi; int64_t cur_mk;
+  st = eval_best(seeds, &bi, &cur_mk);
+  if (st != ADAPTIS_OK) { adaptis_prepared_free(P); return st; }
+  if (bi < 0) {
+    out->n_evaluated = n_eval; out->kernel_ms = ms; out->p = p;
+    adaptis_prepared_free(P);
+    return fail(ctx, ADAPTIS_EINFEASIBLE, "no seed pipeline satisfies the memory constraint (Eq. 2)");
+  }
+  adaptis_plan cur = seeds[bi];
+  push_step(ADAPTIS_GEN_SEED, cur_mk);
+  // ---- tuning rounds
+  int rounds = 0;
+  for (; rounds < max_rounds;) {
+    ++rounds;
+    bool improved = false;
+    // (a) partition: exact best of the L1 ball of radius R around the cuts
+    {
+      adaptis_space sp{};
+      sp.n_groups = 1;
+      int16_t seed[ADAPTIS_MAX_S];
+      for (int i = 1; i < cur.S; ++i) seed[i - 1] = cur.cuts[i];
+      sp.group[0].v = cur.v; sp.group[0].part_mode = ADAPTIS_PART_BALL; sp.group[0].radius = R;
+      sp.group[0].seed_cuts = seed;
+      sp.group[0].combo_mask = 1u << combo_bit(cur.v, cur.placement, cur.policy);
+      adaptis_prepared* Q = nullptr;
+      st = adaptis_prepare(ctx, problem, &sp, &Q);
+      if (st != ADAPTIS_OK) { adaptis_prepared_free(P); return st; }
+      adaptis_plan best{}; int64_t bmk = INT64_MAX;
+      st = best_of_space(ctx, Q, &best, &bmk, &ms);
+      n_eval += Q->N;
+      adaptis_prepared_free(Q);
+      if (st != ADAPTIS_OK && st != ADAPTIS_EINFEASIBLE) { adaptis_prepared_free(P); return st; }
+      if (st == ADAPTIS_OK && bmk < cur_mk) {
+        cur = best; cur_mk = bmk; improved = true;
+        push_step(ADAPTIS_GEN_PARTITION, cur_mk);
+      }
+    }
+    // (b) placement: grouped stage-device permutations (INT <-> WAVE) and v changes
+    {
+      std::vector<adaptis_plan> list;
+      for (int v : vs) {
+        std::vector<int> pls = v == 1 ? std::vector<int>{ADAPTIS_SEQ}
+                                      : std::vector<int>{ADAPTIS_INTERLEAVED, ADAPTIS_WAVE};
+        for (int pl : pls) {
+          if (v == cur.v && pl == cur.placement) continue;
+          const int pol = combo_bit(v, pl, cur.policy) >= 0 ? cur.policy : ADAPTIS_GREEDY;
+          adaptis_plan q = make(v, pl, pol);
+          if (v == cur.v) memcpy(q.cuts, cur.cuts, sizeof(q.cuts));
+          else mist(p * v, &q);
+          list.push_back(q);
+        }
+      }
+      if (!list.empty()) {
+        int b2; int64_t mk2;
+        st = eval_best(list, &b2, &mk2);
+        if (st != ADAPTIS_OK) { adaptis_prepared_free(P); return st; }
+        if (b2 >= 0 && mk2 < cur_mk) {
+          cur = list[b2]; cur_mk = mk2; improved = true;
+          push_step(ADAPTIS_GEN_PLACEMENT, cur_mk);
+        }
+      }
+    }
+    // (c) schedule: every policy R12 admits for the placement
+    {
+      std::vector<adaptis_plan> list;
+      for (int pol = ADAPTIS_GPIPE; pol <= ADAPTIS_GREEDY; ++pol) {
+        if (pol == cur.policy || combo_bit(cur.v, cur.placement, pol) < 0) continue;
+        adaptis_plan q = cur;
+        q.policy = pol;
+        list.push_back(q);
+      }
+      if (!list.empty()) {
+        int b3; int64_t mk3;
+        st = eval_best(list, &b3, &mk3);
+        if (st != ADAPTIS_OK) { adaptis_prepared_free(P); return st; }
+        if (b3 >= 0 && mk3 < cur_mk) {
+          cur = list[b3]; cur_mk = mk3; improved = true;
+          push_step(ADAPTIS_GEN_SCHEDULE, cur_mk);
+        }
+      }
+    }
+    if (!improved) break;
+  }
+  // ---- report of the final plan
+  std::vector<int64_t> mk, pk, rep; std::vector<float> bub; std::vector<uint8_t> stt;
+  float t = 0;
+  st = run_plans(ctx, P, &cur, 1, &mk, &pk, &bub, &stt, &rep, &t);  // not counted in n_evaluated
+  ms += t;
+  adaptis_prepared_free(P);
+  if (st != ADAPTIS_OK) return st;
+  if (stt[0] != ADAPTIS_CAND_OK || mk[0] != cur_mk)
+    return fail(ctx, ADAPTIS_ECUDA, "generator: final re-evaluation disagrees (%lld vs %lld)",
+                (long long)mk[0], (long long)cur_mk);
+  out->plan = cur;
+  out->result.makespan = mk[0];
+  out->result.peak_mem_bytes = pk[0];
+  out->result.bubble_ratio = bub[0];
+  out->result.status = stt[0];
+  out->result.makespan_f32 = (float)mk[0];
+  out->result.throughput = (mk[0] > 0 && problem->tick_seconds > 0)
+      ? (double)m * (double)problem->tokens_per_microbatch / ((double)mk[0] * problem->tick_seconds) : 0.0;
+  out->p = p;
+  for (int d = 0; d < p; ++d) {
+    out->T_d[d] = rep[d]; out->busy_d[d] = rep[p + d]; out->M_d[d] = rep[2 * p + d];
+  }
+  out->rounds = rounds;
+  out->n_evaluated = n_eval;
+  out->kernel_ms = ms;
   return ADAPTIS_OK;
 }
 

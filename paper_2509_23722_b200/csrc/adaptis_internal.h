@@ -53,7 +53,7 @@ struct SegLaunch {
   float* out_bubble;
   uint8_t* out_status;
   float* out_makespan_f32;
-  int64_t* out_report;          // optional [3][p]: T_d, busy_d, M_d (single candidate)
+  int64_t* out_report;          // optional [candidate][3][p]: T_d, busy_d, M_d, at idx - eval_first
   unsigned long long* cursor;   // work-claim counter (zeroed per launch)
   unsigned int* overflow_count; // candidates whose fast-path rings filled up
   uint64_t* overflow_idx;       // their global indices (capacity overflow_cap)
@@ -65,6 +65,10 @@ struct SegLaunch {
   int prune;                    // search: skip candidates whose LB key exceeds the incumbent
   // fallback mode: positions index overflow_idx_in[] instead of [lo, hi)
   const uint64_t* list_idx;
+  // explicit-plan mode (adaptis_eval_plans): position q evaluates plan list_out[q]
+  // (also its output slot); cuts come from list_cuts[plan][ADAPTIS_MAX_S + 1]
+  const uint64_t* list_out;
+  const int16_t* list_cuts;
   int ring_k;                   // ring slots (fast path: kRingK; fallback: >= m)
   int64_t* gring;               // fallback: global ring scratch
   int tick;                     // kTickI32 (host-proved bound), kTickI64, kTickF32 (fp32 variant)

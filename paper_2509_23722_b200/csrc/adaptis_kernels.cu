@@ -210,6 +210,7 @@ __device__ __forceinline__ void colex_next(int16_t* cuts, int S) {
 
 __device__ __forceinline__ uint64_t pos_to_index(const SegLaunch& sl, uint64_t pos) {
   if (sl.list_idx) return sl.list_idx[pos];
+  if (sl.list_out) return sl.list_out[pos];
   return shard_index(pos, sl.n0, sl.start0, sl.first_chunk, sl.world);
 }
 
@@ -435,9 +436,10 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       }
     }
     if (sl.out_report && contrib && status >= 0) {
-      sl.out_report[d] = to_ticks(free_t);
-      sl.out_report[p + d] = to_ticks(busy);
-      sl.out_report[2 * p + d] = Md;
+      int64_t* rep = sl.out_report + (size_t)(idx - sl.eval_first) * 3 * p;
+      rep[d] = to_ticks(free_t);
+      rep[p + d] = to_ticks(busy);
+      rep[2 * p + d] = Md;
     }
   };
 
@@ -496,7 +498,10 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           DCHECK(!take || (idx >= sl.seg_base && idx < sl.hi), "idx", (long long)idx);
           if (take && d == 0) {
             const int16_t* seed = tab.seeds + sl.group * ADAPTIS_MAX_S;
-            if (idx == prev_idx + 1 && S > 1) {
+            if (sl.list_cuts) {  // explicit plan: cuts as given (validity checked below)
+              const int16_t* src = sl.list_cuts + (size_t)idx * (ADAPTIS_MAX_S + 1);
+              for (int i = 0; i <= S; ++i) cuts[i] = src[i];
+            } else if (idx == prev_idx + 1 && S > 1) {
               if (sl.part_mode == ADAPTIS_PART_FULL) colex_next(cuts, S);
               else ball_next(cuts, seed, S - 1, brem);
             } else {
