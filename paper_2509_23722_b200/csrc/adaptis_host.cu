@@ -72,6 +72,7 @@ struct adaptis_prepared {
 
 struct adaptis_ctx {
   int device = 0, rank = 0, world = 1, num_sms = 148;
+  int max_smem = 232448;  // cudaDevAttrMaxSharedMemoryPerBlockOptin (queried at create)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   adaptis_allreduce_min_fn allreduce = nullptr;
@@ -510,7 +511,14 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
     const size_t ring_bytes = (size_t)2 * s.ring_k * s.G * s.S * (P->tick == kTickI64 ? 8 : 4);
     static const size_t greedy_smem_ring =
         getenv("ADAPTIS_GREEDY_SMEM_RING") ? (size_t)atol(getenv("ADAPTIS_GREEDY_SMEM_RING")) : kGreedySmemRing;
-    const bool direct_global = s.policy == ADAPTIS_GREEDY && ring_bytes > greedy_smem_ring;
+    // the CTA's prefix table (6 x (L+1) int64) and the warps' state must fit in
+    // shared memory; rings move to global memory when they do not fit beside them
+    const bool direct_global = (s.policy == ADAPTIS_GREEDY && ring_bytes > greedy_smem_ring) ||
+                               smem_bytes(s, false) > (size_t)ctx->max_smem;
+    if (smem_bytes(s, true) > (size_t)ctx->max_smem)
+      return fail(ctx, ADAPTIS_EINVAL,
+                  "layers.L = %d, S = %d: %zu B of shared memory per CTA needed, the device allows %d",
+                  s.L, s.S, smem_bytes(s, true), ctx->max_smem);
     CU(ctx, cudaEventRecord(ctx->seg_events[2 * i], ctx->stream));
     int e;
     if (direct_global) {
@@ -775,6 +783,7 @@ adaptis_status adaptis_ctx_create(int cuda_device, int rank, int world, adaptis_
   c->device = cuda_device; c->rank = rank; c->world = world;
   cudaError_t e = cudaSetDevice(cuda_device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cuda_device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
