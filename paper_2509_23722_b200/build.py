@@ -24,7 +24,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     stale = not os.path.exists(LIB) or max(os.path.getmtime(f) for f in _inputs()) > os.path.getmtime(LIB)
     if not (force or stale):
         return LIB
-    extra = ["-D%s=%s" % (k, os.environ[k]) for k in ("ADAPTIS_GREEDY_MINB", "ADAPTIS_GREEDY_V4_MINB", "ADAPTIS_FIXED_V4_MINB", "ADAPTIS_GREEDY_COMMITS", "ADAPTIS_DEBUG", "ADAPTIS_KRUN") if os.environ.get(k)]
+    extra = ["-D%s=%s" % (k, os.environ[k]) for k in ("ADAPTIS_GREEDY_MINB", "ADAPTIS_GREEDY_V4_MINB", "ADAPTIS_FIXED_V4_MINB", "ADAPTIS_GREEDY_COMMITS", "ADAPTIS_DEBUG", "ADAPTIS_KRUN", "ADAPTIS_GREEDY_ALWAYS_DECIDE") if os.environ.get(k)]
     cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(os.path.dirname(HERE), "include"),
            *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -49,6 +49,9 @@ constexpr unsigned FULLMASK = 0xffffffffu;
 #define ADAPTIS_KRUN 32
 #endif
 constexpr int kRun = ADAPTIS_KRUN;  // consecutive positions a slot claims (incremental decode)
+#ifndef ADAPTIS_GREEDY_ALWAYS_DECIDE
+#define ADAPTIS_GREEDY_ALWAYS_DECIDE 2  // from this V up, decide() always recomputes
+#endif
 #ifndef ADAPTIS_GREEDY_COMMITS
 #define ADAPTIS_GREEDY_COMMITS 1
 #endif
@@ -122,6 +125,13 @@ __device__ __forceinline__ X seg_min(X v, int p2) {
   for (int o = 1; o < 32; o <<= 1)
     if (o < p2) { X w = __shfl_xor_sync(FULLMASK, v, o); v = w < v ? w : v; }
   return v;
+}
+// segment minimum over the slot's lanes `smask`: one REDUX for 32-bit ticks
+// (every slot passes its own mask), the shuffle ladder otherwise
+template <typename X>
+__device__ __forceinline__ X seg_min_m(X v, int p2, unsigned smask) {
+  if constexpr (std::is_same<X, int>::value) return __reduce_min_sync(smask, v);
+  else return seg_min(v, p2);
 }
 template <typename X>
 __device__ __forceinline__ X seg_sum(X v, int p2) {
@@ -239,6 +249,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   constexpr bool FUSED = (POLICY == ADAPTIS_GPIPE || POLICY == ADAPTIS_ONEF1B);
   constexpr bool ZB = (POLICY == ADAPTIS_ZB);
   constexpr bool GREEDY = (POLICY == ADAPTIS_GREEDY);
+  constexpr bool kAlwaysDecide = V >= ADAPTIS_GREEDY_ALWAYS_DECIDE;
   constexpr T INF = TT<T>::INF;
   constexpr T EMPTY = (T)-1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -639,7 +650,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             if (take && valid && (ov_m & smask)) flags |= F_PREOVER;
           }
           if constexpr (GREEDY) {
-            const T dm = seg_min(dmin, p2), cm = seg_min(cmin, p2);
+            const T dm = seg_min_m(dmin, p2, smask), cm = seg_min_m(cmin, p2, smask);
             if (take) {
               window = (cm == INF) ? INF : dm + cm;
               gdirty = true;
@@ -772,7 +783,9 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           cw[c] = ((volatile unsigned*)cntw)[c * 32 + lane];
           dirty = dirty || cw[c] != seen[c];
         }
-        if (!dirty) return;
+        // a lane-local early exit only saves warp instructions when every lane
+        // takes it: measured worth it at V = 1 only (ADAPTIS_GREEDY_ALWAYS_DECIDE)
+        if (!kAlwaysDecide && !dirty) return;
         gdirty = false;
         at = INF; ak = -1; g_unk = 0;
         unsigned okF = 0, okB = 0, okW = 0;
@@ -824,7 +837,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       // final (DESIGN.md Lemma 3').
       ts_fresh = kTstarEvery == 1 || (wrounds % kTstarEvery) == 0 || force_ts;
       if (ts_fresh) {  // t* is non-decreasing, so a stale value stays a valid (looser) bound
-        const T ts = seg_min(at, p2);
+        const T ts = seg_min_m(at, p2, smask);
         if (active) tstar = ts > tstar ? ts : tstar;
         force_ts = false;
       }
