@@ -284,3 +284,31 @@ def test_pruned_search_same_winner(ctx):
     b = c.search(pr, sp)
     assert b["n_pruned"] > 0.5 * b["n_candidates"]  # the LB prune removes most of cfg2
     c.close()
+
+
+@pytest.mark.parametrize("cid", [3, 4, 5])
+def test_config_winner_certified_by_oracle(ctx, cid):
+    """North star: bit-exact plans on all five configs. cfg1/cfg2 are searched
+    exhaustively by the oracle above; for cfg3-5 (1.5e8-9.5e8 candidates) the
+    GPU winner (pruned search, same winner as unpruned) is certified by the
+    oracle: same decode at that index, same makespan by the event loop, and an
+    element-by-element match on the 4096 candidates around it."""
+    pr, sp = W.config(cid)
+    ctx.set_prune(True)
+    try:
+        b = ctx.search(pr, sp)
+    finally:
+        ctx.set_prune(False)
+    idx = b["index"]
+    assert O.decode(pr, sp, idx)["cuts"] == b["plan"]["cuts"]
+    pl = b["plan"]
+    r = O.simulate(pr, pl["v"], pl["placement"], pl["policy"], pl["cuts"][1:-1])
+    assert r["status"] == 0 and r["makespan"] == b["makespan"]
+    assert r["T_d"] == b["T_d"] and r["M_d"] == b["M_d"] and r["busy_d"] == b["busy_d"]
+    N = O.space_size(pr, sp)
+    first = max(0, min(idx - 2048, N - 4096))
+    got, want = _eval_range(ctx, pr, sp, first, 4096)
+    _compare(got, want, "cfg%d around winner %d" % (cid, idx))
+    ok = np.asarray(want["status"]) == 0
+    ms = np.asarray(want["makespan"])[ok]
+    assert ms.min() >= b["makespan"]
