@@ -160,6 +160,12 @@ typedef struct {             /* output of adaptis_search                        
   int64_t T_d[ADAPTIS_MAX_P];    /* per-device completion time (Alg. 1 Step 3 output)        */
   int64_t busy_d[ADAPTIS_MAX_P]; /* per-device compute ticks                                  */
   int64_t M_d[ADAPTIS_MAX_P];    /* per-device peak memory, static + dynamic (Eq. 2)          */
+  /* Alg. 1 Step 3 accounting (reading R29; integer ticks only): with
+   * C_d = busy_d + comm_d, T_d = C_d + bubble_d - overlap_d holds exactly.       */
+  int64_t comm_d[ADAPTIS_MAX_P];    /* ProfiledCommCost: sum of transfers sent or received by d  */
+  int64_t exposed_d[ADAPTIS_MAX_P]; /* transfer time on d, within [0, T_d], while d computes nothing */
+  int64_t overlap_d[ADAPTIS_MAX_P]; /* OverlapTime(d) = comm_d - exposed_d                     */
+  int64_t bubble_d[ADAPTIS_MAX_P];  /* BubbleTime(d) = T_d - busy_d - exposed_d (>= 0)         */
   uint64_t n_candidates;     /* |space| (all ranks)                                          */
   uint64_t n_evaluated;      /* candidates this rank evaluated                               */
   uint64_t n_invalid;        /* of those, invalid decodes (status 1)                         */
@@ -269,9 +275,11 @@ ADAPTIS_API adaptis_status adaptis_shard_indices(const adaptis_problem* problem,
  * GPIPE and GREEDY); else EINVAL naming the plan. cuts[0] and cuts[S] are taken
  * as 0 and L; cuts that are not strictly increasing give status 1 (INVALID).
  * Results go to host arrays `out` (n entries each) in plan order; `report`,
- * when non-NULL, is a host array [n][3][p] receiving T_d, busy_d and M_d of
- * every plan with status 0 or 2 (untouched otherwise). Not in FP32 cost mode
- * (EINVAL). The context's GPU evaluates the whole list. */
+ * when non-NULL, is a host array [n][5][p] receiving T_d, busy_d, M_d, comm_d
+ * and exposed_d (R29, see adaptis_best) of every plan with status 0 or 2
+ * (untouched otherwise); its trace scratch (n * p * 3mv * 24 B) must stay
+ * under 2 GiB (EINVAL). Not in FP32 cost mode (EINVAL). The context's GPU
+ * evaluates the whole list. */
 ADAPTIS_API adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared* prep,
                                               const adaptis_plan* plans, uint64_t n,
                                               const adaptis_results_soa* out, int64_t* report);
@@ -299,6 +307,8 @@ typedef struct {
   adaptis_result result;
   int32_t p;
   int64_t T_d[ADAPTIS_MAX_P], busy_d[ADAPTIS_MAX_P], M_d[ADAPTIS_MAX_P];
+  int64_t comm_d[ADAPTIS_MAX_P], exposed_d[ADAPTIS_MAX_P];   /* as in adaptis_best (R29)       */
+  int64_t overlap_d[ADAPTIS_MAX_P], bubble_d[ADAPTIS_MAX_P];
   int32_t n_seeds;           /* seed plans evaluated                                          */
   int32_t rounds;            /* tuning rounds run (the last one changed nothing)              */
   uint64_t n_evaluated;      /* plans simulated in total (seeds + every neighbourhood)        */

@@ -314,3 +314,53 @@ def search(pr, sp, prune=True, nthreads=None):
     return {"index": int(b.index), "makespan": int(b.makespan), "plan": plan_dict(b.plan),
             "n_total": int(b.n_total), "n_invalid": int(b.n_invalid),
             "n_simulated": int(b.n_simulated), "n_feasible": int(b.n_feasible)}
+
+
+def comm_accounting(pr, v, placement, policy, cuts):
+    """Reading R29 (Alg. 1 Step 3: T_d = C_d + BubbleTime(d) -
+    OverlapTime(d), with C_d = busy_d + ProfiledCommCost), by brute force on the
+    integer tick grid of the event loop's trace:
+      * every cross-device dependency edge (F(s) -> F(s+1), B(s) -> B(s-1);
+        R3-R6) is a transfer occupying [producer finish, + latency) on both
+        the sending and the receiving device;
+      * comm_d = sum of the latencies of the transfers incident to d;
+      * exposed_d = ticks t < T_d with some incident transfer and no compute
+        on d; overlap_d = comm_d - exposed_d; bubble_d = T_d - busy_d - exposed_d.
+    Returns the simulate() dict extended with those four per-device lists."""
+    r = simulate(pr, v, placement, policy, cuts, trace=True)
+    L, p = len(pr.t_f), pr.p
+    cuts = list(cuts)
+    full = cuts if (cuts and cuts[0] == 0 and cuts[-1] == L) else [0] + cuts + [L]
+    S = len(full) - 1
+    fused = policy in (0, 1)  # GPIPE, ONEF1B run B and W fused (R2)
+    dev = [device_of_stage(placement, p, v, s) for s in range(S)]
+    tf = [int(sum(pr.t_f[full[s]:full[s + 1]])) for s in range(S)]
+    tb = [int(sum(pr.t_b[full[s]:full[s + 1]])) for s in range(S)]
+    tw = [int(sum(pr.t_w[full[s]:full[s + 1]])) for s in range(S)]
+    dur = {0: tf, 1: [b + w for b, w in zip(tb, tw)] if fused else tb, 2: tw}
+    out = {k: [0] * p for k in ("comm_d", "exposed_d", "overlap_d", "bubble_d")}
+    if r["status"] not in (0, 2) or "trace" not in r:
+        return {**r, **out}
+    T = r["T_d"]
+    busy = [np.zeros(max(T[d], 1), bool) for d in range(p)]
+    xfer = [np.zeros(max(T[d], 1), bool) for d in range(p)]
+    for d, lst in enumerate(r["trace"]):
+        for (k, s, j, st) in lst:
+            fin = st + dur[k][s]
+            busy[d][st:fin] = True
+            tgt = None
+            if k == 0 and s + 1 < S and dev[s + 1] != d:
+                tgt, lat = dev[s + 1], int(pr.comm[full[s + 1] - 1])
+            elif k == 1 and s > 0 and dev[s - 1] != d:
+                tgt, lat = dev[s - 1], int(pr.comm[full[s] - 1])
+            if tgt is None or lat == 0:
+                continue
+            for e in (d, tgt):
+                out["comm_d"][e] += lat
+                xfer[e][fin:fin + lat] = True  # numpy clips at T_e
+    for d in range(p):
+        n = T[d]
+        out["exposed_d"][d] = int(np.count_nonzero(xfer[d][:n] & ~busy[d][:n]))
+        out["overlap_d"][d] = out["comm_d"][d] - out["exposed_d"][d]
+        out["bubble_d"][d] = T[d] - r["busy_d"][d] - out["exposed_d"][d]
+    return {**r, **out}

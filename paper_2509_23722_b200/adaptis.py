@@ -71,10 +71,14 @@ class _Result(C.Structure):
                 ("makespan_f32", C.c_float)]
 
 
+ACCT = ("comm_d", "exposed_d", "overlap_d", "bubble_d")  # R29, Alg. 1 Step 3 accounting
+
+
 class _Best(C.Structure):
     _fields_ = [("index", C.c_uint64), ("plan", _Plan), ("result", _Result), ("p", C.c_int32),
                 ("T_d", C.c_int64 * MAX_P), ("busy_d", C.c_int64 * MAX_P),
-                ("M_d", C.c_int64 * MAX_P), ("n_candidates", C.c_uint64),
+                ("M_d", C.c_int64 * MAX_P)] + [(k, C.c_int64 * MAX_P) for k in ACCT] + [
+                ("n_candidates", C.c_uint64),
                 ("n_evaluated", C.c_uint64), ("n_invalid", C.c_uint64), ("n_tasks", C.c_uint64),
                 ("n_pruned", C.c_uint64), ("kernel_ms", C.c_float)]
 
@@ -90,7 +94,8 @@ GEN_PHASES = {0: "seed", 1: "partition", 2: "placement", 3: "schedule"}
 class _GenResult(C.Structure):
     _fields_ = [("plan", _Plan), ("result", _Result), ("p", C.c_int32),
                 ("T_d", C.c_int64 * MAX_P), ("busy_d", C.c_int64 * MAX_P),
-                ("M_d", C.c_int64 * MAX_P), ("n_seeds", C.c_int32), ("rounds", C.c_int32),
+                ("M_d", C.c_int64 * MAX_P)] + [(k, C.c_int64 * MAX_P) for k in ACCT] + [
+                ("n_seeds", C.c_int32), ("rounds", C.c_int32),
                 ("n_evaluated", C.c_uint64), ("n_steps", C.c_int32),
                 ("step_phase", C.c_int32 * GEN_MAX_STEPS), ("step_makespan", C.c_int64 * GEN_MAX_STEPS),
                 ("kernel_ms", C.c_float)]
@@ -111,7 +116,7 @@ _lib = None
 def exported_symbols():
     """Entry points declared in include/adaptis.h."""
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(adaptis_[a-z_]+)\s*\(", src)) - {"adaptis_allreduce_min_fn"})
+    return sorted(set(re.findall(r"ADAPTIS_API\s+[\w\s\*]*?\b(adaptis_[a-z_]+)\s*\(", src)))
 
 
 def lib():
@@ -383,6 +388,7 @@ class Context:
                 "peak_mem": int(r.result.peak_mem_bytes), "bubble": float(r.result.bubble_ratio),
                 "throughput": float(r.result.throughput), "cand_status": int(r.result.status),
                 "T_d": list(r.T_d[:p]), "busy_d": list(r.busy_d[:p]), "M_d": list(r.M_d[:p]),
+                **{k: list(getattr(r, k)[:p]) for k in ACCT},
                 "n_seeds": int(r.n_seeds), "rounds": int(r.rounds), "n_evaluated": int(r.n_evaluated),
                 "steps": [(GEN_PHASES[int(r.step_phase[i])], int(r.step_makespan[i])) for i in range(n)],
                 "kernel_ms": float(r.kernel_ms)}
@@ -421,12 +427,15 @@ class Prepared:
         arr = make_plans(plans)
         out = _host_results(n)
         soa = _soa_from_numpy(out)
-        rep = np.zeros((max(n, 1), 3, self.m.problem.p), np.int64) if report else None
+        rep = np.zeros((max(n, 1), 5, self.m.problem.p), np.int64) if report else None
         _check(lib().adaptis_eval_plans(self.ctx.ptr, self.ptr, arr, n, C.byref(soa),
                                         rep.ctypes.data_as(C.POINTER(C.c_int64)) if report else None),
                self.ctx.ptr)
         if report:
             out["T_d"], out["busy_d"], out["M_d"] = rep[:n, 0], rep[:n, 1], rep[:n, 2]
+            out["comm_d"], out["exposed_d"] = rep[:n, 3], rep[:n, 4]
+            out["overlap_d"] = out["comm_d"] - out["exposed_d"]
+            out["bubble_d"] = out["T_d"] - out["busy_d"] - out["exposed_d"]
         return out
 
     def eval(self, first: int, count: int, device_out: bool = False):
@@ -475,6 +484,7 @@ def _best_dict(b: _Best, st: int, ctx_ptr) -> dict:
             "bubble": float(b.result.bubble_ratio), "throughput": float(b.result.throughput),
             "cand_status": int(b.result.status),
             "T_d": list(b.T_d[:p]), "busy_d": list(b.busy_d[:p]), "M_d": list(b.M_d[:p]),
+            **{k: list(getattr(b, k)[:p]) for k in ACCT},
             "n_candidates": int(b.n_candidates), "n_evaluated": int(b.n_evaluated),
             "n_invalid": int(b.n_invalid), "n_tasks": int(b.n_tasks), "n_pruned": int(b.n_pruned),
             "kernel_ms": float(b.kernel_ms)}

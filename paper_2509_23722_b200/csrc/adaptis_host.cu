@@ -371,7 +371,7 @@ adaptis_status ensure_scratch(adaptis_ctx* ctx, size_t words, size_t overflow_ca
     CU(ctx, cudaMalloc(&ctx->d_overflow, overflow_cap * 8));
     ctx->overflow_cap = overflow_cap;
   }
-  if (!ctx->d_report) CU(ctx, cudaMalloc(&ctx->d_report, 3 * ADAPTIS_MAX_P * 8));
+  if (!ctx->d_report) CU(ctx, cudaMalloc(&ctx->d_report, 5 * ADAPTIS_MAX_P * 8));
   return ADAPTIS_OK;
 }
 
@@ -464,9 +464,16 @@ constexpr size_t kSegWords = 6;
 // filled up are re-run by the fallback kernel (exact, rings >= m).
 // mode_search: pack keys into the key word; else write SoA results at
 // idx - eval_first (and per-candidate reports when `report` is set).
+struct TraceBuf {  // report mode with communication accounting (R29)
+  TraceEntry* trace = nullptr;
+  int* trace_n = nullptr;
+  int cap = 0;
+};
+
 adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>& jobs,
                         bool mode_search, const adaptis_results_soa* dout, uint64_t eval_first,
-                        int64_t* report, float* kernel_ms, bool keep_key) {
+                        int64_t* report, float* kernel_ms, bool keep_key,
+                        const TraceBuf* tb = nullptr) {
   const size_t nseg = jobs.size();
   const size_t nwords = kHdr + kSegWords * std::max<size_t>(nseg, 1);
   adaptis_status st = ensure_scratch(ctx, nwords, kOverflowPerSeg * std::max<size_t>(nseg, 1));
@@ -497,6 +504,7 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
       s.out_makespan_f32 = dout->makespan_f32;
     }
     s.out_report = report;
+    if (tb && P->tick != kTickF32) { s.trace = tb->trace; s.trace_n = tb->trace_n; s.trace_cap = tb->cap; }
     s.cursor = sw + 0;
     s.overflow_count = reinterpret_cast<unsigned int*>(sw + 1);
     s.overflow_idx = ctx->d_overflow + kOverflowPerSeg * i;
@@ -514,7 +522,7 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
     // the CTA's prefix table (6 x (L+1) int64) and the warps' state must fit in
     // shared memory; rings move to global memory when they do not fit beside them
     const bool direct_global = (s.policy == ADAPTIS_GREEDY && ring_bytes > greedy_smem_ring) ||
-                               smem_bytes(s, false) > (size_t)ctx->max_smem;
+                               smem_bytes(s, false) > (size_t)ctx->max_smem || s.trace != nullptr;
     if (smem_bytes(s, true) > (size_t)ctx->max_smem)
       return fail(ctx, ADAPTIS_EINVAL,
                   "layers.L = %d, S = %d: %zu B of shared memory per CTA needed, the device allows %d",
@@ -600,7 +608,7 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
 adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uint64_t hi,
                          bool mode_search, int rank, int world, const adaptis_results_soa* dout,
                          uint64_t eval_first, int64_t* report, float* kernel_ms,
-                         bool keep_key = false) {
+                         bool keep_key = false, const TraceBuf* tb = nullptr) {
   std::vector<Job> jobs;
   for (const Seg& sg : P->segs) {
     const uint64_t a = std::max(lo, sg.base), b = std::min(hi, sg.base + sg.count);
@@ -614,7 +622,7 @@ adaptis_status run_range(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uin
     j.info.placement = sg.placement; j.info.policy = sg.policy;
     jobs.push_back(j);
   }
-  return run_jobs(ctx, P, jobs, mode_search, dout, eval_first, report, kernel_ms, keep_key);
+  return run_jobs(ctx, P, jobs, mode_search, dout, eval_first, report, kernel_ms, keep_key, tb);
 }
 
 void fill_plan(const adaptis_prepared& P, uint64_t index, adaptis_plan* out, bool* valid) {
@@ -661,7 +669,7 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
   if (peak) peak->assign(n, 0);
   if (bubble) bubble->assign(n, 0.0f);
   status->assign(n, 0);
-  if (report) report->assign((size_t)n * 3 * P->p, 0);
+  if (report) report->assign((size_t)n * 5 * P->p, 0);
   if (n == 0) return ADAPTIS_OK;
   constexpr int CS = ADAPTIS_MAX_S + 1;
   std::vector<int16_t> hcuts((size_t)n * CS, 0);
@@ -680,10 +688,11 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
   CU(ctx, cudaSetDevice(ctx->device));
   int16_t* d_cuts = nullptr; uint64_t* d_order = nullptr;
   int64_t *d_mk = nullptr, *d_pk = nullptr, *d_rep = nullptr; float* d_bub = nullptr; uint8_t* d_st = nullptr;
+  TraceBuf tb;
   adaptis_status st = ADAPTIS_OK;
   auto cleanup = [&]() {
     cudaFree(d_cuts); cudaFree(d_order); cudaFree(d_mk); cudaFree(d_pk); cudaFree(d_rep);
-    cudaFree(d_bub); cudaFree(d_st);
+    cudaFree(d_bub); cudaFree(d_st); cudaFree(tb.trace); cudaFree(tb.trace_n);
   };
 #define CUP(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { cleanup(); \
     return fail(ctx, ADAPTIS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
@@ -693,9 +702,24 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
   CUP(cudaMalloc(&d_pk, n * 8));
   CUP(cudaMalloc(&d_bub, n * 4));
   CUP(cudaMalloc(&d_st, n));
+  const bool account = report && P->tick != kTickF32;
   if (report) {
-    CUP(cudaMalloc(&d_rep, (size_t)n * 3 * P->p * 8));
-    CUP(cudaMemsetAsync(d_rep, 0, (size_t)n * 3 * P->p * 8, ctx->stream));
+    CUP(cudaMalloc(&d_rep, (size_t)n * 5 * P->p * 8));
+    CUP(cudaMemsetAsync(d_rep, 0, (size_t)n * 5 * P->p * 8, ctx->stream));
+  }
+  if (account) {  // one trace per (plan, device): at most 3 m v tasks (R29)
+    int vmax = 1;
+    for (uint64_t i = 0; i < n; ++i) vmax = std::max(vmax, (int)plans[i].v);
+    tb.cap = 3 * P->m * vmax;
+    const size_t bytes = (size_t)n * P->p * tb.cap * sizeof(TraceEntry);
+    if (bytes > ((size_t)1 << 31)) {
+      cleanup();
+      return fail(ctx, ADAPTIS_EINVAL, "report for %llu plans needs %zu B of trace scratch (> 2 GiB): split the list",
+                  (unsigned long long)n, bytes);
+    }
+    CUP(cudaMalloc(&tb.trace, bytes));
+    CUP(cudaMalloc(&tb.trace_n, (size_t)n * P->p * sizeof(int)));
+    CUP(cudaMemsetAsync(tb.trace_n, 0, (size_t)n * P->p * sizeof(int), ctx->stream));
   }
   CUP(cudaMemcpyAsync(d_cuts, hcuts.data(), hcuts.size() * 2, cudaMemcpyHostToDevice, ctx->stream));
   CUP(cudaMemcpyAsync(d_order, order.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
@@ -721,13 +745,17 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
     off += g.size();
   }
   adaptis_results_soa dout{d_mk, d_pk, d_bub, d_st, nullptr};
-  st = run_jobs(ctx, P, jobs, false, &dout, 0, d_rep, kernel_ms, false);
+  st = run_jobs(ctx, P, jobs, false, &dout, 0, d_rep, kernel_ms, false, account ? &tb : nullptr);
   if (st != ADAPTIS_OK) { cleanup(); return st; }
+  if (account) {
+    const int e = launch_comm_account(tb.trace, tb.trace_n, tb.cap, P->p, n, d_rep, ctx->stream);
+    if (e) { cleanup(); return fail(ctx, ADAPTIS_ECUDA, "comm accounting: %s", cudaGetErrorString((cudaError_t)e)); }
+  }
   CUP(cudaMemcpyAsync(mk->data(), d_mk, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   if (peak) CUP(cudaMemcpyAsync(peak->data(), d_pk, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   if (bubble) CUP(cudaMemcpyAsync(bubble->data(), d_bub, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CUP(cudaMemcpyAsync(status->data(), d_st, n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (report) CUP(cudaMemcpyAsync(report->data(), d_rep, (size_t)n * 3 * P->p * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (report) CUP(cudaMemcpyAsync(report->data(), d_rep, (size_t)n * 5 * P->p * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUP(cudaStreamSynchronize(ctx->stream));
 #undef CUP
   cleanup();
@@ -980,13 +1008,29 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   out->index = idx;
   fill_plan(*P, idx, &out->plan, nullptr);
   // winner report: the same kernel on the single winning index
-  std::vector<int64_t> rep(3 * P->p);
+  std::vector<int64_t> rep(5 * P->p, 0);
   int64_t mk = 0, pk = 0; float bub = 0, mkf = 0; uint8_t stt = 0;
   int64_t *dmk = nullptr, *dpk = nullptr; float *dbub = nullptr, *dmkf = nullptr; uint8_t* dst = nullptr;
   CU(ctx, cudaMalloc(&dmk, 8)); CU(ctx, cudaMalloc(&dpk, 8)); CU(ctx, cudaMalloc(&dbub, 4));
   CU(ctx, cudaMalloc(&dst, 1)); CU(ctx, cudaMalloc(&dmkf, 4));
+  CU(ctx, cudaMemsetAsync(ctx->d_report, 0, 5 * ADAPTIS_MAX_P * 8, ctx->stream));
   adaptis_results_soa so{dmk, dpk, dbub, dst, dmkf};
-  st = run_range(ctx, P, idx, idx + 1, false, 0, 1, &so, idx, ctx->d_report, nullptr);
+  // with integer ticks the winner is re-run with its device traces for the
+  // communication accounting of R29 (comm, exposed, overlap, bubble per device)
+  TraceBuf tb;
+  const bool account = P->tick != kTickF32;
+  if (account) {
+    tb.cap = 3 * P->m * out->plan.v;
+    CU(ctx, cudaMalloc(&tb.trace, (size_t)P->p * tb.cap * sizeof(TraceEntry)));
+    CU(ctx, cudaMalloc(&tb.trace_n, (size_t)P->p * sizeof(int)));
+    CU(ctx, cudaMemsetAsync(tb.trace_n, 0, (size_t)P->p * sizeof(int), ctx->stream));
+  }
+  st = run_range(ctx, P, idx, idx + 1, false, 0, 1, &so, idx, ctx->d_report, nullptr, false,
+                 account ? &tb : nullptr);
+  if (st == ADAPTIS_OK && account) {
+    const int e = launch_comm_account(tb.trace, tb.trace_n, tb.cap, P->p, 1, ctx->d_report, ctx->stream);
+    if (e) st = fail(ctx, ADAPTIS_ECUDA, "comm accounting: %s", cudaGetErrorString((cudaError_t)e));
+  }
   if (st == ADAPTIS_OK) {
     CU(ctx, cudaMemcpyAsync(&mk, dmk, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(&pk, dpk, 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -997,6 +1041,7 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
     CU(ctx, cudaStreamSynchronize(ctx->stream));
   }
   cudaFree(dmk); cudaFree(dpk); cudaFree(dbub); cudaFree(dst); cudaFree(dmkf);
+  cudaFree(tb.trace); cudaFree(tb.trace_n);
   ctx->last_info = search_info;  // report the search's launches, not the re-evaluation
   if (st != ADAPTIS_OK) return st;
   out->result.makespan = mk;
@@ -1011,6 +1056,10 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
     out->T_d[d] = rep[d];
     out->busy_d[d] = rep[P->p + d];
     out->M_d[d] = rep[2 * P->p + d];
+    out->comm_d[d] = rep[3 * P->p + d];
+    out->exposed_d[d] = rep[4 * P->p + d];
+    out->overlap_d[d] = out->comm_d[d] - out->exposed_d[d];
+    out->bubble_d[d] = out->T_d[d] - out->busy_d[d] - out->exposed_d[d];
   }
   const unsigned long long kv = key >> P->key_bits;
   bool agree;
@@ -1041,7 +1090,7 @@ adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared* P, const a
   if (report)
     for (uint64_t i = 0; i < n; ++i)
       if (stt[i] == ADAPTIS_CAND_OK || stt[i] == ADAPTIS_CAND_OVER_CAP)
-        memcpy(report + (size_t)i * 3 * P->p, rep.data() + (size_t)i * 3 * P->p, (size_t)3 * P->p * 8);
+        memcpy(report + (size_t)i * 5 * P->p, rep.data() + (size_t)i * 5 * P->p, (size_t)5 * P->p * 8);
   return ADAPTIS_OK;
 }
 
@@ -1242,6 +1291,9 @@ adaptis_status adaptis_generate(adaptis_ctx* ctx, const adaptis_problem* problem
   out->p = p;
   for (int d = 0; d < p; ++d) {
     out->T_d[d] = rep[d]; out->busy_d[d] = rep[p + d]; out->M_d[d] = rep[2 * p + d];
+    out->comm_d[d] = rep[3 * p + d]; out->exposed_d[d] = rep[4 * p + d];
+    out->overlap_d[d] = out->comm_d[d] - out->exposed_d[d];
+    out->bubble_d[d] = out->T_d[d] - out->busy_d[d] - out->exposed_d[d];
   }
   out->rounds = rounds;
   out->n_evaluated = n_eval;

@@ -69,9 +69,22 @@ struct SegLaunch {
   // (also its output slot); cuts come from list_cuts[plan][ADAPTIS_MAX_S + 1]
   const uint64_t* list_out;
   const int16_t* list_cuts;
+  // report mode with communication accounting (R29): every committed task of
+  // candidate o on device d is appended to trace[(o * p + d) * trace_cap + k]
+  // and the count stored in trace_n[o * p + d]
+  struct TraceEntry* trace;
+  int* trace_n;
+  int trace_cap;
   int ring_k;                   // ring slots (fast path: kRingK; fallback: >= m)
   int64_t* gring;               // fallback: global ring scratch
   int tick;                     // kTickI32 (host-proved bound), kTickI64, kTickF32 (fp32 variant)
+};
+
+// one committed task in report mode (R29): its compute interval and, when its
+// output crosses devices, the transfer [fin, fin + oc] to device `tgt` (-1: none)
+struct TraceEntry {
+  int64_t start, fin;
+  int32_t oc, tgt;
 };
 
 #ifdef __CUDACC__
@@ -107,6 +120,12 @@ ADAPTIS_LAYOUT_HD WarpLayout warp_layout(int S, int G, int V, int K, int tsz, in
 }
 
 // launchers implemented in adaptis_kernels.cu
+// R29 communication accounting over the traces of n candidates: per device,
+// comm = sum of incident transfer lengths, exposed = |union of incident
+// transfers within [0, T_d], outside the device's compute intervals|; written
+// to report rows 3 and 4 ([candidate][5][p]). Returns a cudaError_t.
+int launch_comm_account(const TraceEntry* trace, const int* trace_n, int trace_cap, int p,
+                        uint64_t n, int64_t* report, void* stream);
 int launch_segment(const DevTables& t, const SegLaunch& s, int num_sms, void* stream,
                    bool fallback, unsigned grid_limit);
 int occupancy_ctas_per_sm(const SegLaunch& s, bool fallback);

@@ -242,7 +242,7 @@ template <int POLICY, int V> struct MinBlocks {
                                    : (V >= 3 ? ADAPTIS_GREEDY_V4_MINB : ADAPTIS_GREEDY_MINB);
 };
 
-template <int POLICY, int V, typename T, bool GRING>
+template <int POLICY, int V, typename T, bool GRING, bool TRACE = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MinBlocks<POLICY, V>::value)
 seg_kernel(const DevTables tab, const SegLaunch sl) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -386,6 +386,22 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   bool exhausted = false;       // warp-uniform: the launch's positions are all claimed
   unsigned wrounds = 0;
   unsigned ctasks = 0, clive = 0;  // this lane's tasks / live rounds since the last flush
+  int ntr = 0;                     // TRACE: tasks recorded for the slot's current candidate
+  // TRACE (report mode, R29): append a committed task [start, fin) and its output
+  // transfer (latency oc to device tdev, -1: none) to this candidate's device trace
+  auto trace_task = [&](T start, T fin, T oc, int tdev) {
+    if constexpr (TRACE) {
+      if (ntr < sl.trace_cap) {
+        TraceEntry e;
+        e.start = to_ticks(start);
+        e.fin = to_ticks(fin);
+        e.oc = (int32_t)to_ticks(oc);
+        e.tgt = tdev;
+        sl.trace[((size_t)(cold.idx - sl.eval_first) * p + d) * sl.trace_cap + ntr] = e;
+      }
+      ++ntr;
+    }
+  };
 
   auto next_task = [&]() {
     if (nF < tot && (POLICY == ADAPTIS_GPIPE || nF - nB <= wup)) { tk = 0; tc = fp.c; tj = fp.mb(); }
@@ -447,10 +463,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       }
     }
     if (sl.out_report && contrib && status >= 0) {
-      int64_t* rep = sl.out_report + (size_t)(idx - sl.eval_first) * 3 * p;
+      int64_t* rep = sl.out_report + (size_t)(idx - sl.eval_first) * 5 * p;
       rep[d] = to_ticks(free_t);
       rep[p + d] = to_ticks(busy);
       rep[2 * p + d] = Md;
+      if constexpr (TRACE) sl.trace_n[(size_t)(idx - sl.eval_first) * p + d] = ntr;
     }
   };
 
@@ -547,6 +564,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           if (take) {
             flags = valid ? 0 : F_INVALID;
             free_t = 0; dyn = 0; peak = 0; stat = 0;
+            ntr = 0;
           }
           // ---- a2/a3 aggregation into task records
           T dmin = INF, cmin = INF;
@@ -739,6 +757,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             else runW = r >= 0 && free_t < r;
             if (!runW) break;
             const int c = V - 1 - wp.c;
+            trace_task(free_t, free_t + REC(2, c).dur, (T)0, -1);
             free_t += REC(2, c).dur;
             dyn += DMEM(2, c);
             ++nW; wp.next(p, V); ++ctasks;
@@ -750,6 +769,13 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         if (xgo && !ofree) { blocked = true; xgo = false; }
         if (xgo) {
           const T fin = (free_t > r ? free_t : r) + tr.dur;
+          if constexpr (TRACE) {
+            const int s0 = stage_of(sl.placement, p, tc, d);
+            const int s1 = tk == 0 ? s0 + 1 : s0 - 1;
+            int tdev = (oaddr >= 0 && s1 >= 0 && s1 < S) ? dev_of(sl.placement, p, s1) : -1;
+            if (tdev == d) tdev = -1;
+            trace_task(fin - tr.dur, fin, tdev >= 0 ? tr.oc : (T)0, tdev);
+          }
           free_t = fin;
           if (oaddr >= 0) ring[oaddr] = fin + tr.oc;
           if (iaddr >= 0) ring[iaddr] = EMPTY;
@@ -869,6 +895,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         const int acx = g_acx, aj = g_aj;
         const Rec<T> rc = REC(ak, acx);
         const T fin = at + rc.dur;
+        if constexpr (TRACE) {
+          const int tg = ak == 0 ? ga_tF[acx * 32 + lane] : (ak == 1 ? ga_tB[acx * 32 + lane] : -1);
+          const int tdev = tg >= 0 ? (tg >> 3) - leader : -1;
+          trace_task(at, fin, (tdev >= 0 && tdev != d) ? rc.oc : (T)0, tdev == d ? -1 : tdev);
+        }
         free_t = fin;
         dyn += DMEM(ak, acx);
         if (ak == 0) peak = dyn > peak ? dyn : peak;
@@ -972,32 +1003,110 @@ size_t smem_bytes(const SegLaunch& s, bool fallback) {
 
 using KFn = void (*)(const DevTables, const SegLaunch);
 
+// report launches with a trace (R29) use the global-ring kernel instantiated
+// with TRACE (integer ticks only); every other launch keeps its hot kernel
 template <int POLICY, int V, typename T>
-static KFn pick_fb(bool fallback) {
+static KFn pick_fb(bool fallback, bool trace) {
+  if constexpr (!std::is_floating_point<T>::value)
+    if (trace) return (KFn)seg_kernel<POLICY, V, T, true, true>;
   return fallback ? (KFn)seg_kernel<POLICY, V, T, true> : (KFn)seg_kernel<POLICY, V, T, false>;
 }
 template <int POLICY, typename T>
-static KFn pick_v(int v, bool fb) {
+static KFn pick_v(int v, bool fb, bool tr) {
   switch (v) {
-    case 1: return pick_fb<POLICY, 1, T>(fb);
-    case 2: return pick_fb<POLICY, 2, T>(fb);
-    case 3: return pick_fb<POLICY, 3, T>(fb);
-    default: return pick_fb<POLICY, 4, T>(fb);
+    case 1: return pick_fb<POLICY, 1, T>(fb, tr);
+    case 2: return pick_fb<POLICY, 2, T>(fb, tr);
+    case 3: return pick_fb<POLICY, 3, T>(fb, tr);
+    default: return pick_fb<POLICY, 4, T>(fb, tr);
   }
 }
 template <typename T>
-static KFn pick_pol(int pol, int v, bool fb) {
+static KFn pick_pol(int pol, int v, bool fb, bool tr) {
   switch (pol) {
-    case ADAPTIS_GPIPE: return pick_v<ADAPTIS_GPIPE, T>(v, fb);
-    case ADAPTIS_ONEF1B: return pick_v<ADAPTIS_ONEF1B, T>(v, fb);
-    case ADAPTIS_ZB: return pick_v<ADAPTIS_ZB, T>(v, fb);
-    default: return pick_v<ADAPTIS_GREEDY, T>(v, fb);
+    case ADAPTIS_GPIPE: return pick_v<ADAPTIS_GPIPE, T>(v, fb, tr);
+    case ADAPTIS_ONEF1B: return pick_v<ADAPTIS_ONEF1B, T>(v, fb, tr);
+    case ADAPTIS_ZB: return pick_v<ADAPTIS_ZB, T>(v, fb, tr);
+    default: return pick_v<ADAPTIS_GREEDY, T>(v, fb, tr);
   }
 }
 static KFn pick(const SegLaunch& s, bool fb) {
-  if (s.tick == kTickI64) return pick_pol<int64_t>(s.policy, s.v, fb);
-  if (s.tick == kTickF32) return pick_pol<float>(s.policy, s.v, fb);
-  return pick_pol<int32_t>(s.policy, s.v, fb);
+  const bool tr = s.trace != nullptr;
+  if (s.tick == kTickI64) return pick_pol<int64_t>(s.policy, s.v, fb, tr);
+  if (s.tick == kTickF32) return pick_pol<float>(s.policy, s.v, fb, tr);
+  return pick_pol<int32_t>(s.policy, s.v, fb, tr);
+}
+
+// ---- R29 communication accounting: one thread per (candidate, device)
+__global__ void comm_account_kernel(const TraceEntry* __restrict__ trace, const int* __restrict__ trace_n,
+                                    int cap, int p, uint64_t n, int64_t* __restrict__ report) {
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= n * (uint64_t)p) return;
+  const uint64_t o = gid / p;
+  const int d = (int)(gid % p);
+  int64_t* rep = report + o * 5 * p;
+  const int64_t Td = rep[d];
+  const TraceEntry* base = trace + o * p * (size_t)cap;
+  int ptr[ADAPTIS_MAX_P], len[ADAPTIS_MAX_P];
+  for (int l = 0; l < p; ++l) {
+    ptr[l] = 0;
+    const int k = trace_n[o * p + l];
+    len[l] = k < cap ? k : cap;
+  }
+  const TraceEntry* own = base + (size_t)d * cap;
+  // transfers incident to d: d's own outputs to other devices, and every
+  // device's outputs to d; each device's trace is in execution order, so every
+  // stream is sorted by transfer start (= producer finish): a p-way merge
+  auto relevant = [&](int l, const TraceEntry& e) {
+    return e.oc > 0 && e.tgt >= 0 && (l == d ? e.tgt != d : e.tgt == d);
+  };
+  int64_t comm = 0, exposed = 0, u0 = 0, u1 = -1;
+  int ci = 0;  // first compute interval of d that may still overlap a union segment
+  auto flush = [&]() {  // |[u0, u1] clipped to [0, Td] minus d's compute intervals|
+    const int64_t a = u0 < 0 ? 0 : u0, b = u1 < Td ? u1 : Td;
+    if (b <= a) return;
+    while (ci < len[d] && own[ci].fin <= a) ++ci;
+    int64_t covered = 0;
+    for (int j = ci; j < len[d] && own[j].start < b; ++j) {
+      const int64_t x = own[j].start > a ? own[j].start : a;
+      const int64_t y = own[j].fin < b ? own[j].fin : b;
+      if (y > x) covered += y - x;
+    }
+    exposed += (b - a) - covered;
+  };
+  for (;;) {
+    int best = -1;
+    int64_t bs = 0;
+    for (int l = 0; l < p; ++l) {
+      while (ptr[l] < len[l] && !relevant(l, base[(size_t)l * cap + ptr[l]])) ++ptr[l];
+      if (ptr[l] < len[l]) {
+        const int64_t st = base[(size_t)l * cap + ptr[l]].fin;
+        if (best < 0 || st < bs) { best = l; bs = st; }
+      }
+    }
+    if (best < 0) break;
+    const TraceEntry& e = base[(size_t)best * cap + ptr[best]];
+    ++ptr[best];
+    const int64_t a = e.fin, b = e.fin + e.oc;
+    comm += e.oc;
+    if (u1 < 0 || a > u1) {  // a new disjoint union segment
+      if (u1 >= 0) flush();
+      u0 = a; u1 = b;
+    } else if (b > u1) {
+      u1 = b;
+    }
+  }
+  if (u1 >= 0) flush();
+  rep[3 * p + d] = comm;
+  rep[4 * p + d] = exposed;
+}
+
+int launch_comm_account(const TraceEntry* trace, const int* trace_n, int trace_cap, int p,
+                        uint64_t n, int64_t* report, void* stream) {
+  if (n == 0) return 0;
+  const uint64_t threads = n * (uint64_t)p;
+  const unsigned grid = (unsigned)((threads + 127) / 128);
+  comm_account_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(trace, trace_n, trace_cap, p, n, report);
+  return (int)cudaGetLastError();
 }
 
 int occupancy_ctas_per_sm(const SegLaunch& s, bool fallback) {

@@ -4,6 +4,7 @@ host-side canonical order (adaptis_space_size / adaptis_decode, shared with
 the kernels' decode) agrees with the oracle's independent recursive
 enumerator and recursive-descent decoder."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -11,6 +12,8 @@ import pytest
 from oracle import oracle as O
 from paper_2509_23722_b200 import adaptis as A
 from paper_2509_23722_b200 import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -97,3 +100,32 @@ def test_overflow_is_reported():
     with pytest.raises(A.AdaptisError) as e:
         A.space_size(pr, W.Space([W.Group(1, W.FULL, combo_mask=0xF)]))
     assert e.value.status == A.EOVERFLOW
+
+
+def test_ctypes_layouts_match_header(tmp_path):
+    """The binding's ctypes structures have the sizes and field offsets the C
+    compiler gives the structs of include/adaptis.h (ABI check, no GPU)."""
+    import ctypes as C
+    import subprocess
+    from paper_2509_23722_b200 import adaptis as A
+    src = tmp_path / "layout.c"
+    src.write_text(r'''
+#include <stddef.h>
+#include <stdio.h>
+#include "adaptis.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(adaptis_problem), sizeof(adaptis_plan),
+         sizeof(adaptis_result), sizeof(adaptis_best), offsetof(adaptis_best, comm_d),
+         offsetof(adaptis_best, n_candidates), sizeof(adaptis_gen_result),
+         offsetof(adaptis_gen_result, step_makespan), sizeof(adaptis_launch_info),
+         sizeof(adaptis_gen_options));
+  return 0;
+}
+''')
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    want = [C.sizeof(A._Problem), C.sizeof(A._Plan), C.sizeof(A._Result), C.sizeof(A._Best),
+            A._Best.comm_d.offset, A._Best.n_candidates.offset, C.sizeof(A._GenResult),
+            A._GenResult.step_makespan.offset, C.sizeof(A._LaunchInfo), C.sizeof(A._GenOptions)]
+    assert got == want

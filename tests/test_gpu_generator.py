@@ -1,4 +1,5 @@
-"""GPU parity of the explicit-plan evaluator (adaptis_eval_plans) and of the
+"""GPU parity of the explicit-plan evaluator (adaptis_eval_plans, including the
+R29 communication accounting of its per-device report) and of the
 Pipeline Generator (adaptis_generate, reading R28) against the
 oracle: per-plan results and per-device reports bit-exact against
 oracle.simulate; the generator's whole trajectory (every accepted step, the
@@ -59,7 +60,7 @@ def check_plans(prep, pr, plans):
         if any(a >= b for a, b in zip(d["cuts"], d["cuts"][1:])):
             assert got["status"][i] == 1, (i, d)
             continue
-        want = O.simulate(pr, d["v"], d["placement"], d["policy"], d["cuts"][1:S])
+        want = O.comm_accounting(pr, d["v"], d["placement"], d["policy"], d["cuts"][1:S])
         assert got["status"][i] == want["status"], (i, d, got["status"][i], want)
         if want["status"] == 0:
             assert got["makespan"][i] == want["makespan"], (i, d)
@@ -69,6 +70,8 @@ def check_plans(prep, pr, plans):
             assert list(got["busy_d"][i]) == want["busy_d"], (i, d)
         if want["status"] == 0:
             assert list(got["T_d"][i]) == want["T_d"], (i, d)
+            for k in ("comm_d", "exposed_d", "overlap_d", "bubble_d"):  # R29
+                assert list(got[k][i]) == want[k], (i, d, k, list(got[k][i]), want[k])
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3])

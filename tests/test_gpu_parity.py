@@ -302,9 +302,11 @@ def test_config_winner_certified_by_oracle(ctx, cid):
     idx = b["index"]
     assert O.decode(pr, sp, idx)["cuts"] == b["plan"]["cuts"]
     pl = b["plan"]
-    r = O.simulate(pr, pl["v"], pl["placement"], pl["policy"], pl["cuts"][1:-1])
+    r = O.comm_accounting(pr, pl["v"], pl["placement"], pl["policy"], pl["cuts"][1:-1])
     assert r["status"] == 0 and r["makespan"] == b["makespan"]
     assert r["T_d"] == b["T_d"] and r["M_d"] == b["M_d"] and r["busy_d"] == b["busy_d"]
+    for k in ("comm_d", "exposed_d", "overlap_d", "bubble_d"):  # R29 accounting of the winner
+        assert r[k] == b[k], k
     N = O.space_size(pr, sp)
     first = max(0, min(idx - 2048, N - 4096))
     got, want = _eval_range(ctx, pr, sp, first, 4096)

@@ -9,6 +9,7 @@ import itertools
 import json
 import math
 import os
+import random
 from fractions import Fraction
 
 import numpy as np
@@ -376,3 +377,64 @@ def test_f64_closed_forms_with_fractional_costs(p, m):
     g = O.simulate(prf, 1, W.SEQ, W.GPIPE, seq_cuts(p))
     o = O.simulate(prf, 1, W.SEQ, W.ONEF1B, seq_cuts(p))
     assert g["makespan_f"] == (m + p - 1) * (tf + tb + tw) == o["makespan_f"]
+
+
+# ----------------------------------------------------------------- R29 comm accounting
+def _acct_problem(L, p, m, tf, tb, tw, comm):
+    z = [0] * L
+    return W.Problem(t_f=tf, t_b=tb, t_w=tw, act=z, stash=z, weight=z, grad=z, comm=comm, p=p, m=m)
+
+
+def test_comm_accounting_hand_example():
+    """GPipe, p = 2, m = 1, t_F = 1, fused B = t_B + t_W = 2, latency 3 (worked by hand):
+    d0 computes [0,1] and [10,12], its transfers are [1,4] and [7,10] -> exposed 6,
+    bubble 3 (idle [4,7]); d1 computes [4,7], transfers [1,4] and [7,10] (the latter
+    after T_1 = 7) -> exposed 3, overlap 3, bubble 1."""
+    pr = _acct_problem(2, 2, 1, [1, 1], [1, 1], [1, 1], [3, 0])
+    r = O.comm_accounting(pr, 1, 0, 0, [1])
+    assert r["T_d"] == [12, 7] and r["busy_d"] == [3, 3]
+    assert r["comm_d"] == [6, 6] and r["exposed_d"] == [6, 3]
+    assert r["overlap_d"] == [0, 3] and r["bubble_d"] == [3, 1]
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+def test_comm_accounting_spec_device_comm_total(policy):
+    """S:198 example: S = 2, P = 2, nmb = 3, one boundary of 10 ticks -> each
+    device sends 3 and receives 3 transfers: comm total 2 x 3 x 10 = 60."""
+    pr = _acct_problem(2, 2, 3, [5, 5], [5, 5], [2, 2], [10, 0])
+    r = O.comm_accounting(pr, 1, 0, policy, [1])
+    assert r["comm_d"] == [60, 60]
+
+
+@pytest.mark.parametrize("p,m", [(2, 2), (3, 4), (4, 4), (4, 7)])
+def test_comm_accounting_zero_comm_1f1b(p, m):
+    """Zero comm: no exposed or overlapped transfer time, and device 0 of a
+    homogeneous S-1F1B pipeline idles (p-1)(t_F+t_B) (S:210 closed form)."""
+    f, b, w = 3, 4, 2
+    pr = _acct_problem(p, p, m, [f] * p, [b] * p, [w] * p, [0] * p)
+    r = O.comm_accounting(pr, 1, 0, 1, list(range(1, p)))
+    assert r["comm_d"] == [0] * p and r["exposed_d"] == [0] * p
+    assert r["bubble_d"][0] == (p - 1) * (f + b + w)  # fused B runs t_B + t_W (R2)
+
+
+def test_comm_accounting_identity_and_bounds():
+    """Alg. 1 Step 3 identity T_d = (busy_d + comm_d) + bubble_d - overlap_d, and
+    0 <= exposed_d <= min(comm_d, T_d - busy_d), on random plans of every policy."""
+    rng = W.SplitMix64(29)
+    n = 0
+    for t in range(60):
+        p = [2, 3, 4][t % 3]
+        L = 2 * p + 2
+        pr = W.random_problem(rng, L, p, 2 * p, tmax=7, cmax=6, bytes_max=0)
+        v = 1 + (t % 2)
+        S = p * v
+        cuts = sorted(random.Random(t).sample(range(1, L), S - 1))
+        for pl, po in ([(0, k) for k in range(4)] if v == 1 else [(1, k) for k in range(4)] + [(2, 0), (2, 3)]):
+            r = O.comm_accounting(pr, v, pl, po, cuts)
+            if r["status"] != 0:
+                continue
+            n += 1
+            for d in range(p):
+                assert r["T_d"][d] == r["busy_d"][d] + r["comm_d"][d] + r["bubble_d"][d] - r["overlap_d"][d]
+                assert 0 <= r["exposed_d"][d] <= min(r["comm_d"][d], r["T_d"][d] - r["busy_d"][d])
+    assert n > 200
