@@ -295,7 +295,10 @@ def main():
                            "l2": "flushed (256 MiB write) between timed steps"},
                 "best": {"index": best["index"], "makespan_ticks": best["makespan"],
                          "plan": best["plan"], "bubble": best["bubble"],
-                         "peak_mem_bytes": best["peak_mem"]},
+                         "peak_mem_bytes": best["peak_mem"],
+                         # Alg. 1 Step 3 per device (R29): T_d = busy + comm + bubble - overlap
+                         "T_d": best["T_d"], "busy_d": best["busy_d"], "comm_d": best["comm_d"],
+                         "overlap_d": best["overlap_d"], "bubble_d": best["bubble_d"]},
                 "e2e": {"value": valid / (e2e_ms_step / 1000.0), "unit": UNIT,
                         "ms_per_step": e2e_ms_step, "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},

@@ -1,0 +1,28 @@
+// adaptis_inst_greedy.cu — instantiations of the segment kernel for ADAPTIS_GREEDY
+// (one translation unit per policy so that nvcc builds them in parallel).
+#include "adaptis_seg.cuh"
+
+namespace adaptis {
+
+template <int V, typename T>
+static KFn pick_fb_greedy(bool fallback, bool trace) {
+  if constexpr (!std::is_floating_point<T>::value)
+    if (trace) return (KFn)seg_kernel<ADAPTIS_GREEDY, V, T, true, true>;
+  return fallback ? (KFn)seg_kernel<ADAPTIS_GREEDY, V, T, true> : (KFn)seg_kernel<ADAPTIS_GREEDY, V, T, false>;
+}
+template <typename T>
+static KFn pick_v_greedy(int v, bool fb, bool tr) {
+  switch (v) {
+    case 1: return pick_fb_greedy<1, T>(fb, tr);
+    case 2: return pick_fb_greedy<2, T>(fb, tr);
+    case 3: return pick_fb_greedy<3, T>(fb, tr);
+    default: return pick_fb_greedy<4, T>(fb, tr);
+  }
+}
+KFn pick_policy_greedy(int tick, int v, bool fb, bool tr) {
+  if (tick == kTickI64) return pick_v_greedy<int64_t>(v, fb, tr);
+  if (tick == kTickF32) return pick_v_greedy<float>(v, fb, tr);
+  return pick_v_greedy<int32_t>(v, fb, tr);
+}
+
+}  // namespace adaptis
