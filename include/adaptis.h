@@ -267,6 +267,15 @@ ADAPTIS_API adaptis_status adaptis_shard_indices(const adaptis_problem* problem,
                                                  const adaptis_space* space, int rank, int world,
                                                  uint64_t* out, uint64_t cap, uint64_t* n_out);
 
+/* Evaluate an arbitrary list of global indices of the prepared space (decoded
+ * on the device, canonical order R19; Alg. 1 Steps 1-3 per candidate) and
+ * write results to host arrays `out` (n entries each) in list order.
+ * Duplicates are allowed. EINVAL if some index >= |space| (the message names
+ * it). The context's GPU evaluates the whole list (no sharding). */
+ADAPTIS_API adaptis_status adaptis_eval_indices(adaptis_ctx* ctx, adaptis_prepared* prep,
+                                                const uint64_t* indices, uint64_t n,
+                                                const adaptis_results_soa* out);
+
 /* Evaluate an explicit list of plans (Alg. 1 Steps 1-3 per plan),
  * e.g. the neighbourhood of one Pipeline Generator step. `prep`
  * must have been prepared from the same problem (any space; its tables are

@@ -167,6 +167,9 @@ def lib():
             L.adaptis_search.argtypes = [C.c_void_p, C.POINTER(_Problem), C.POINTER(_Space), C.POINTER(_Best)]
             L.adaptis_search_prepared.restype = st
             L.adaptis_search_prepared.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Best)]
+            L.adaptis_eval_indices.restype = st
+            L.adaptis_eval_indices.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64,
+                                               C.POINTER(_ResultsSoa)]
             L.adaptis_eval_plans.restype = st
             L.adaptis_eval_plans.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_uint64,
                                              C.POINTER(_ResultsSoa), C.POINTER(C.c_int64)]
@@ -420,6 +423,15 @@ class Prepared:
         b = _Best()
         st = lib().adaptis_search_prepared(self.ctx.ptr, self.ptr, C.byref(b))
         return _best_dict(b, st, self.ctx.ptr)
+
+    def eval_indices(self, indices) -> dict:
+        """adaptis_eval_indices: results for arbitrary global indices (device decode)."""
+        idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
+        out = _host_results(len(idx))
+        soa = _soa_from_numpy(out)
+        _check(lib().adaptis_eval_indices(self.ctx.ptr, self.ptr, idx.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                          len(idx), C.byref(soa)), self.ctx.ptr)
+        return out
 
     def eval_plans(self, plans, report: bool = False) -> dict:
         """adaptis_eval_plans: results (and optionally T_d/busy_d/M_d) of explicit plans."""

@@ -560,7 +560,8 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
     while (K < P->m) K <<= 1;
     s.ring_k = K;
     if (cnt <= kOverflowPerSeg) {
-      s.list_idx = s.overflow_idx;
+      if (s.list_slot) s.list_slot = s.overflow_idx;  // explicit-index mode records slots
+      else s.list_idx = s.overflow_idx;
       s.n_pos = cnt;
     }  // else: re-run the whole segment shard in fallback mode
     unsigned long long* sw = W + kHdr + kSegWords * i;
@@ -1066,6 +1067,76 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   if (P->tick == kTickF32) { float f; uint32_t u = (uint32_t)kv; memcpy(&f, &u, 4); agree = f == mkf; }
   else agree = mk == (int64_t)kv;
   if (!agree) return fail(ctx, ADAPTIS_ECUDA, "winner re-evaluation disagrees with its search key");
+  return ADAPTIS_OK;
+}
+
+adaptis_status adaptis_eval_indices(adaptis_ctx* ctx, adaptis_prepared* P, const uint64_t* indices,
+                                    uint64_t n, const adaptis_results_soa* out) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");
+  if (n && !indices) return fail(ctx, ADAPTIS_EINVAL, "indices is NULL");
+  if (n == 0) return ADAPTIS_OK;
+  // slots grouped by segment (one launch each), in the caller's order within a segment
+  std::vector<std::vector<uint64_t>> by_seg(P->segs.size());
+  for (uint64_t q = 0; q < n; ++q) {
+    const uint64_t i = indices[q];
+    if (i >= P->N)
+      return fail(ctx, ADAPTIS_EINVAL, "indices[%llu] = %llu >= |space| = %llu", (unsigned long long)q,
+                  (unsigned long long)i, (unsigned long long)P->N);
+    size_t lo = 0, hi = P->segs.size();
+    while (hi - lo > 1) {  // last segment with base <= i
+      const size_t mid = (lo + hi) / 2;
+      if (P->segs[mid].base <= i) lo = mid; else hi = mid;
+    }
+    by_seg[lo].push_back(q);
+  }
+  std::vector<uint64_t> slots;
+  slots.reserve(n);
+  for (auto& v : by_seg) slots.insert(slots.end(), v.begin(), v.end());
+  CU(ctx, cudaSetDevice(ctx->device));
+  uint64_t *d_idx = nullptr, *d_slots = nullptr;
+  void* tmp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  adaptis_status st = ADAPTIS_OK;
+  auto cleanup = [&]() { cudaFree(d_idx); cudaFree(d_slots); for (void* t : tmp) cudaFree(t); };
+#define CUI(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { cleanup(); \
+    return fail(ctx, ADAPTIS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
+  CUI(cudaMalloc(&d_idx, n * 8));
+  CUI(cudaMalloc(&d_slots, n * 8));
+  CUI(cudaMemcpyAsync(d_idx, indices, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CUI(cudaMemcpyAsync(d_slots, slots.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  adaptis_results_soa dout{};
+  if (out->makespan) { CUI(cudaMalloc(&tmp[0], n * 8)); dout.makespan = (int64_t*)tmp[0]; }
+  if (out->peak_mem_bytes) { CUI(cudaMalloc(&tmp[1], n * 8)); dout.peak_mem_bytes = (int64_t*)tmp[1]; }
+  if (out->bubble_ratio) { CUI(cudaMalloc(&tmp[2], n * 4)); dout.bubble_ratio = (float*)tmp[2]; }
+  if (out->status) { CUI(cudaMalloc(&tmp[3], n)); dout.status = (uint8_t*)tmp[3]; }
+  if (out->makespan_f32) { CUI(cudaMalloc(&tmp[4], n * 4)); dout.makespan_f32 = (float*)tmp[4]; }
+  std::vector<Job> jobs;
+  uint64_t off = 0;
+  for (size_t i = 0; i < P->segs.size(); ++i) {
+    const uint64_t k = by_seg[i].size();
+    if (k == 0) continue;
+    const Seg& sg = P->segs[i];
+    Job j{};
+    j.s = make_launch(P, sg);
+    j.s.lo = sg.base; j.s.hi = sg.base + sg.count;
+    j.s.n_pos = k; j.s.n0 = k; j.s.world = 1;
+    j.s.list_slot = d_slots + off;
+    j.s.slot_idx = d_idx;
+    j.info.group = sg.group; j.info.combo = sg.combo; j.info.v = sg.v;
+    j.info.placement = sg.placement; j.info.policy = sg.policy;
+    jobs.push_back(j);
+    off += k;
+  }
+  st = run_jobs(ctx, P, jobs, false, &dout, 0, nullptr, nullptr, false);
+  if (st != ADAPTIS_OK) { cleanup(); return st; }
+  if (out->makespan) CUI(cudaMemcpyAsync(out->makespan, tmp[0], n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (out->peak_mem_bytes) CUI(cudaMemcpyAsync(out->peak_mem_bytes, tmp[1], n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (out->bubble_ratio) CUI(cudaMemcpyAsync(out->bubble_ratio, tmp[2], n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (out->status) CUI(cudaMemcpyAsync(out->status, tmp[3], n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (out->makespan_f32) CUI(cudaMemcpyAsync(out->makespan_f32, tmp[4], n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CUI(cudaStreamSynchronize(ctx->stream));
+#undef CUI
+  cleanup();
   return ADAPTIS_OK;
 }
 

@@ -69,6 +69,11 @@ struct SegLaunch {
   // (also its output slot); cuts come from list_cuts[plan][ADAPTIS_MAX_S + 1]
   const uint64_t* list_out;
   const int16_t* list_cuts;
+  // explicit-index mode (adaptis_eval_indices): position q writes output slot
+  // list_slot[q], which holds global index slot_idx[slot]; overflowed
+  // candidates record their slot, so the fallback re-run lists slots too
+  const uint64_t* list_slot;
+  const uint64_t* slot_idx;
   // report mode with communication accounting (R29): every committed task of
   // candidate o on device d is appended to trace[(o * p + d) * trace_cap + k]
   // and the count stored in trace_n[o * p + d]
@@ -113,7 +118,7 @@ ADAPTIS_LAYOUT_HD WarpLayout warp_layout(int S, int G, int V, int K, int tsz, in
   l.cuts_off = off; off += align16(G * (S + 1) * 2);
   l.cnt_off = off;  off += 32 * 4 * 4;  // GREEDY produced-count words [chunk][lane]
   l.gaux_off = off; off += align16(V * 32 * gaux_sz);  // GREEDY per-chunk statics
-  l.cold_off = off; off += 32 * 56;                    // per-lane cold state (LaneCold)
+  l.cold_off = off; off += 32 * 64;                    // per-lane cold state (LaneCold)
   l.ring_off = off; if (!gring) off += 2 * K * G * S * tsz;
   l.per_warp = align16(off);
   return l;

@@ -94,8 +94,9 @@ struct LaneCold {
   unsigned long long key;         // running minimum of the packed argmin key
   unsigned long long invalid, tasks, live;  // counters flushed at kernel exit
   unsigned long long pruned;
+  uint64_t slot;                  // eval: output slot of the candidate (idx - eval_first, or list_slot)
 };
-static_assert(sizeof(LaneCold) == 56, "LaneCold layout");
+static_assert(sizeof(LaneCold) == 64, "LaneCold layout");
 
 enum : int { F_INVALID = 1, F_PREOVER = 2, F_STUCK = 4, F_OVERFLOW = 8, F_PRUNED = 16 };
 
@@ -220,6 +221,7 @@ __device__ __forceinline__ void colex_next(int16_t* cuts, int S) {
 }
 
 __device__ __forceinline__ uint64_t pos_to_index(const SegLaunch& sl, uint64_t pos) {
+  if (sl.list_slot) return sl.slot_idx[sl.list_slot[pos]];
   if (sl.list_idx) return sl.list_idx[pos];
   if (sl.list_out) return sl.list_out[pos];
   return shard_index(pos, sl.n0, sl.start0, sl.first_chunk, sl.world);
@@ -322,7 +324,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   T* ga_pF = reinterpret_cast<T*>(ga_tB + V * 32);
   T* ga_pB = ga_pF + V * 32;
   LaneCold& cold = reinterpret_cast<LaneCold*>(wbase + lay.cold_off)[threadIdx.x & 31];
-  cold.idx = 0; cold.busy = 0; cold.key = ~0ull >> 1; cold.invalid = 0; cold.tasks = 0; cold.live = 0;
+  cold.idx = 0; cold.slot = 0; cold.busy = 0; cold.key = ~0ull >> 1; cold.invalid = 0; cold.tasks = 0; cold.live = 0;
   cold.pruned = 0;
   T* ring;
   if constexpr (GRING) {
@@ -398,7 +400,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         e.fin = to_ticks(fin);
         e.oc = (int32_t)to_ticks(oc);
         e.tgt = tdev;
-        sl.trace[((size_t)(cold.idx - sl.eval_first) * p + d) * sl.trace_cap + ntr] = e;
+        sl.trace[((size_t)cold.slot * p + d) * sl.trace_cap + ntr] = e;
       }
       ++ntr;
     }
@@ -435,7 +437,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
     if (fl && d == 0) {
       if (status == -2) {
         const unsigned k = atomicAdd(sl.overflow_count, 1u);
-        if (k < sl.overflow_cap) sl.overflow_idx[k] = idx;
+        if (k < sl.overflow_cap) sl.overflow_idx[k] = sl.list_slot ? cold.slot : idx;
       } else {
         if (status == ADAPTIS_CAND_INVALID) ++cold.invalid;
         if (status == -3) ++cold.pruned;
@@ -451,7 +453,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             }
           }
         } else {
-          const uint64_t o = idx - sl.eval_first;
+          const uint64_t o = cold.slot;
           if (sl.out_status) sl.out_status[o] = (uint8_t)status;
           if (sl.out_makespan) sl.out_makespan[o] = status == 0 ? mk : INT64_MAX;
           if (sl.out_makespan_f32) sl.out_makespan_f32[o] = status == 0 ? (float)mkT : INFINITY;
@@ -464,11 +466,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       }
     }
     if (sl.out_report && contrib && status >= 0) {
-      int64_t* rep = sl.out_report + (size_t)(idx - sl.eval_first) * 5 * p;
+      int64_t* rep = sl.out_report + (size_t)cold.slot * 5 * p;
       rep[d] = to_ticks(free_t);
       rep[p + d] = to_ticks(busy);
       rep[2 * p + d] = Md;
-      if constexpr (TRACE) sl.trace_n[(size_t)(idx - sl.eval_first) * p + d] = ntr;
+      if constexpr (TRACE) sl.trace_n[(size_t)cold.slot * p + d] = ntr;
     }
   };
 
@@ -523,7 +525,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           // ---- a1 decode: the successor of the previous candidate when the slot
           // moves to the next index, else unranking from scratch
           uint64_t idx = 0;
-          if (take) { idx = pos_to_index(sl, mypos); cold.idx = idx; }
+          if (take) {
+            idx = pos_to_index(sl, mypos);
+            cold.idx = idx;
+            cold.slot = sl.list_slot ? sl.list_slot[mypos] : idx - sl.eval_first;
+          }
           DCHECK(!take || (idx >= sl.seg_base && idx < sl.hi), "idx", (long long)idx);
           if (take && d == 0) {
             const int16_t* seed = tab.seeds + sl.group * ADAPTIS_MAX_S;

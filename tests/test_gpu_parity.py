@@ -314,3 +314,28 @@ def test_config_winner_certified_by_oracle(ctx, cid):
     ok = np.asarray(want["status"]) == 0
     ms = np.asarray(want["makespan"])[ok]
     assert ms.min() >= b["makespan"]
+
+
+@pytest.mark.parametrize("cid,n", [(3, 100_000), (4, 100_000), (5, 20_000)])
+def test_uniform_indices_device_decode(ctx, cid, n):
+    """seeded-uniform indices (seed 12345) per BALL config through
+    adaptis_eval_indices (device decode of arbitrary indices, duplicates
+    allowed), element by element against the oracle."""
+    pr, sp = W.config(cid)
+    N = O.space_size(pr, sp)
+    idx = np.random.default_rng(12345).integers(0, N, n).astype(np.uint64)
+    idx[: min(64, n)] = idx[0]  # duplicates share one result
+    prep = ctx.prepare(pr, sp)
+    got = prep.eval_indices(idx)
+    want = O.eval_indices(pr, sp, idx)
+    _compare(got, want, "cfg%d uniform" % cid)
+    assert np.bincount(np.asarray(want["status"]), minlength=4)[0] > n // 20
+
+
+def test_eval_indices_rejects_out_of_range(ctx):
+    from paper_2509_23722_b200 import adaptis as A
+    pr, sp = W.config(1)
+    prep = ctx.prepare(pr, sp)
+    with pytest.raises(A.AdaptisError) as e:
+        prep.eval_indices([0, 244])
+    assert e.value.status == A.EINVAL and "indices[1]" in str(e.value)
