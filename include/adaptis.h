@@ -61,6 +61,17 @@ enum { ADAPTIS_SEQ = 0, ADAPTIS_INTERLEAVED = 1, ADAPTIS_WAVE = 2 };
 /* Workload-scheduling policies (§2.4, §4.3, readings R9-R14):
  * GPIPE and ONEF1B run B and W fused; ZB and GREEDY split them. */
 enum { ADAPTIS_GPIPE = 0, ADAPTIS_ONEF1B = 1, ADAPTIS_ZB = 2, ADAPTIS_GREEDY = 3 };
+/* Explicit per-device task orders ("workload scheduling results"; reading
+ * R30), for adaptis_eval_lists only: LIST splits B and W (W tasks are listed),
+ * LIST_FUSED runs B and W fused (no W tasks). */
+enum { ADAPTIS_LIST = 4, ADAPTIS_LIST_FUSED = 5 };
+
+/* One task of an explicit per-device order: kind 0 = F, 1 = B, 2 = W. */
+typedef struct {
+  int16_t kind;
+  int16_t stage;             /* 0 <= stage < S, a stage of the listing device        */
+  int32_t mb;                /* micro-batch, 0 <= mb < m                              */
+} adaptis_task;
 
 /* Cost arithmetic (R1): exact int64 ticks, or the fp32-cost variant whose
  * makespans agree with an fp64 evaluation within 1e-5 relative. */
@@ -275,6 +286,20 @@ ADAPTIS_API adaptis_status adaptis_shard_indices(const adaptis_problem* problem,
 ADAPTIS_API adaptis_status adaptis_eval_indices(adaptis_ctx* ctx, adaptis_prepared* prep,
                                                 const uint64_t* indices, uint64_t n,
                                                 const adaptis_results_soa* out);
+
+/* Evaluate plans with explicit per-device task orders (Alg. 1 Step 3 on given
+ * workload scheduling results; reading R30). Plan i has policy
+ * ADAPTIS_LIST or ADAPTIS_LIST_FUSED, any placement of R12 for its v, and its
+ * device d executes tasks[offsets[i*(p+1)+d] .. offsets[i*(p+1)+d+1]) in order:
+ * every (F, B[, W]) x own stage x micro-batch exactly once, with F(s,j) before
+ * B(s,j) before W(s,j) on the device (else EINVAL naming plan, device and
+ * task). Cross-device waits follow the DAG; a cyclic wait gives status
+ * STUCK, a peak above the cap OVER_CAP (split precedence, R26). Outputs as
+ * adaptis_eval_plans (report [n][5][p] optional). Not in FP32 cost mode. */
+ADAPTIS_API adaptis_status adaptis_eval_lists(adaptis_ctx* ctx, adaptis_prepared* prep,
+                                              const adaptis_plan* plans, const adaptis_task* tasks,
+                                              const uint64_t* offsets, uint64_t n,
+                                              const adaptis_results_soa* out, int64_t* report);
 
 /* Evaluate an explicit list of plans (Alg. 1 Steps 1-3 per plan),
  * e.g. the neighbourhood of one Pipeline Generator step. `prep`

@@ -364,3 +364,49 @@ def comm_accounting(pr, v, placement, policy, cuts):
         out["overlap_d"][d] = out["comm_d"][d] - out["exposed_d"][d]
         out["bubble_d"][d] = T[d] - r["busy_d"][d] - out["exposed_d"][d]
     return {**r, **out}
+
+
+def simulate_lists(pr, v, placement, fused, cuts, lists):
+    """Reading R30 (Alg. 1 Step 3 on explicit workload scheduling results):
+    device d executes lists[d] = [(kind, stage, mb), ...] in order; times are the
+    longest path over the task DAG plus the list edges (the independent checker
+    `longest_path`); memory is walked along each list with the R16 rules. A
+    cyclic wait gives status 3 (stuck), a device above the cap status 2."""
+    L, p, m = len(pr.t_f), pr.p, pr.m
+    cuts = list(cuts)
+    full = cuts if (cuts and cuts[0] == 0 and cuts[-1] == L) else [0] + cuts + [L]
+    S = len(full) - 1
+
+    def ssum(col, s):
+        return int(sum(col[full[s]:full[s + 1]]))
+    tf = [ssum(pr.t_f, s) for s in range(S)]
+    tb = [ssum(pr.t_b, s) for s in range(S)]
+    tw = [ssum(pr.t_w, s) for s in range(S)]
+    act = [ssum(pr.act, s) for s in range(S)]
+    sta = [ssum(pr.stash, s) for s in range(S)]
+    wg = [ssum(pr.weight, s) + ssum(pr.grad, s) for s in range(S)]
+    dev = [device_of_stage(placement, p, v, s) for s in range(S)]
+    dur = {0: tf, 1: [b + w for b, w in zip(tb, tw)] if fused else tb, 2: tw}
+    busy = [0] * p
+    Md = [0] * p
+    for d in range(p):
+        stat = sum(wg[s] for s in range(S) if dev[s] == d)
+        dyn = peak = 0
+        for (k, s, j) in lists[d]:
+            busy[d] += dur[k][s]
+            if k == 0:
+                dyn += act[s] + sta[s]
+                peak = max(peak, dyn)
+            elif k == 1:
+                dyn -= act[s] + (sta[s] if fused else 0)
+            else:
+                dyn -= sta[s]
+        Md[d] = stat + peak
+    lp = longest_path(pr, v, placement, full[1:-1], fused, lists)
+    out = {"busy_d": busy, "M_d": Md}
+    if lp is None:
+        return {**out, "status": 3, "makespan": INT64_MAX, "peak_mem": 0, "T_d": [0] * p}
+    mk, Td, _ = lp
+    status = 2 if max(Md) > pr.cap else 0
+    return {**out, "status": status, "makespan": mk if status == 0 else INT64_MAX,
+            "peak_mem": max(Md), "T_d": Td}

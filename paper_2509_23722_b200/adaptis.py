@@ -170,6 +170,10 @@ def lib():
             L.adaptis_eval_indices.restype = st
             L.adaptis_eval_indices.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64,
                                                C.POINTER(_ResultsSoa)]
+            L.adaptis_eval_lists.restype = st
+            L.adaptis_eval_lists.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
+                                             C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(_ResultsSoa),
+                                             C.POINTER(C.c_int64)]
             L.adaptis_eval_plans.restype = st
             L.adaptis_eval_plans.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_uint64,
                                              C.POINTER(_ResultsSoa), C.POINTER(C.c_int64)]
@@ -448,6 +452,35 @@ class Prepared:
             out["comm_d"], out["exposed_d"] = rep[:n, 3], rep[:n, 4]
             out["overlap_d"] = out["comm_d"] - out["exposed_d"]
             out["bubble_d"] = out["T_d"] - out["busy_d"] - out["exposed_d"]
+        return out
+
+    def eval_lists(self, plans, lists, report: bool = False) -> dict:
+        """adaptis_eval_lists: plans (policy LIST = 4 / LIST_FUSED = 5) with explicit
+        per-device orders lists[i][d] = [(kind, stage, mb), ...] (R30)."""
+        n = len(plans)
+        p = self.m.problem.p
+        arr = make_plans(plans)
+        flat = [t for per_plan in lists for dev in per_plan for t in dev]
+        tasks = np.zeros(max(1, len(flat)), dtype=[("kind", "<i2"), ("stage", "<i2"), ("mb", "<i4")])
+        for q, (k, s_, j) in enumerate(flat):
+            tasks[q] = (k, s_, j)
+        offs = np.zeros(max(1, n * (p + 1)), np.uint64)
+        pos = 0
+        for i, per_plan in enumerate(lists):
+            for d in range(p):
+                offs[i * (p + 1) + d] = pos
+                pos += len(per_plan[d])
+            offs[i * (p + 1) + p] = pos
+        out = _host_results(n)
+        soa = _soa_from_numpy(out)
+        rep = np.zeros((max(n, 1), 5, p), np.int64) if report else None
+        _check(lib().adaptis_eval_lists(self.ctx.ptr, self.ptr, arr, tasks.ctypes.data,
+                                        offs.ctypes.data_as(C.POINTER(C.c_uint64)), n, C.byref(soa),
+                                        rep.ctypes.data_as(C.POINTER(C.c_int64)) if report else None),
+               self.ctx.ptr)
+        if report:
+            out["T_d"], out["busy_d"], out["M_d"] = rep[:n, 0], rep[:n, 1], rep[:n, 2]
+            out["comm_d"], out["exposed_d"] = rep[:n, 3], rep[:n, 4]
         return out
 
     def eval(self, first: int, count: int, device_out: bool = False):

@@ -649,12 +649,73 @@ int combo_bit(int v, int placement, int policy) {
 
 // Explicit plans on the device: one job per (v, placement, policy) group,
 // positions mapped to plan (= output) indices in the caller's order.
+int host_dev_of(int placement, int p, int s) {  // R12
+  if (placement == ADAPTIS_SEQ) return s;
+  if (placement == ADAPTIS_INTERLEAVED) return s % p;
+  const int c = s / p, j = s - c * p;
+  return (c & 1) ? p - 1 - j : j;
+}
+
+// R30: every (kind, own stage, mb) exactly once per device, F < B < W per (stage, mb)
+adaptis_status validate_lists(adaptis_ctx* ctx, const adaptis_prepared* P, const adaptis_plan* plans,
+                              const adaptis_task* tasks, const uint64_t* offsets, uint64_t n) {
+  const int p = P->p, m = P->m;
+  for (uint64_t i = 0; i < n; ++i) {
+    const adaptis_plan& pl = plans[i];
+    const bool fused = pl.policy == ADAPTIS_LIST_FUSED;
+    const int nk = fused ? 2 : 3, S = pl.S;
+    std::vector<int64_t> pos((size_t)nk * S * m, -1);
+    const uint64_t* off = offsets + i * (uint64_t)(p + 1);
+    for (int d = 0; d < p; ++d) {
+      if (off[d + 1] < off[d])
+        return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: offsets of device %d decrease", (unsigned long long)i, d);
+      for (uint64_t q = off[d]; q < off[d + 1]; ++q) {
+        const adaptis_task& t = tasks[q];
+        if (t.kind < 0 || t.kind >= nk || t.stage < 0 || t.stage >= S || t.mb < 0 || t.mb >= m ||
+            host_dev_of(pl.placement, p, t.stage) != d)
+          return fail(ctx, ADAPTIS_EINVAL, "plans[%llu] device %d task %llu (kind %d, stage %d, mb %d) is not a task of this device",
+                      (unsigned long long)i, d, (unsigned long long)(q - off[d]), t.kind, t.stage, t.mb);
+        int64_t& slot = pos[((size_t)t.kind * S + t.stage) * m + t.mb];
+        if (slot >= 0)
+          return fail(ctx, ADAPTIS_EINVAL, "plans[%llu] device %d lists (kind %d, stage %d, mb %d) twice",
+                      (unsigned long long)i, d, t.kind, t.stage, t.mb);
+        slot = (int64_t)q;
+      }
+    }
+    for (int k = 0; k < nk; ++k)
+      for (int s2 = 0; s2 < S; ++s2)
+        for (int j = 0; j < m; ++j) {
+          const int64_t x = pos[((size_t)k * S + s2) * m + j];
+          if (x < 0)
+            return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: (kind %d, stage %d, mb %d) is not listed",
+                        (unsigned long long)i, k, s2, j);
+          if (k > 0 && x < pos[((size_t)(k - 1) * S + s2) * m + j])
+            return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: (kind %d, stage %d, mb %d) is listed before its %s",
+                        (unsigned long long)i, k, s2, j, k == 1 ? "F" : "B");
+        }
+  }
+  return ADAPTIS_OK;
+}
+
 adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plans,
                          uint64_t n, std::vector<int64_t>* mk, std::vector<int64_t>* peak,
                          std::vector<float>* bubble, std::vector<uint8_t>* status,
-                         std::vector<int64_t>* report, float* kernel_ms) {
+                         std::vector<int64_t>* report, float* kernel_ms,
+                         const adaptis_task* tasks = nullptr, const uint64_t* offsets = nullptr) {
   for (uint64_t i = 0; i < n; ++i) {
     const adaptis_plan& pl = plans[i];
+    if (pl.policy == ADAPTIS_LIST || pl.policy == ADAPTIS_LIST_FUSED) {
+      if (!tasks || !offsets)
+        return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: LIST policies need task lists (adaptis_eval_lists)",
+                    (unsigned long long)i);
+      const bool ok_pl = pl.v == 1 ? pl.placement == ADAPTIS_SEQ
+                                   : (pl.placement == ADAPTIS_INTERLEAVED || pl.placement == ADAPTIS_WAVE);
+      if (pl.v < 1 || pl.v > ADAPTIS_MAX_V || pl.S != P->p * pl.v || pl.S > ADAPTIS_MAX_S || pl.S > P->L ||
+          (pl.v > 1 && P->m % P->p != 0) || !ok_pl)
+        return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: v = %d, S = %d, placement %d not admitted (R10, R12)",
+                    (unsigned long long)i, pl.v, pl.S, pl.placement);
+      continue;
+    }
     if (pl.v < 1 || pl.v > ADAPTIS_MAX_V)
       return fail(ctx, ADAPTIS_EINVAL, "plans[%llu].v = %d not in [1, 4]", (unsigned long long)i, pl.v);
     if (pl.S != P->p * pl.v || pl.S > ADAPTIS_MAX_S || pl.S > P->L)
@@ -674,14 +735,14 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
   if (n == 0) return ADAPTIS_OK;
   constexpr int CS = ADAPTIS_MAX_S + 1;
   std::vector<int16_t> hcuts((size_t)n * CS, 0);
-  std::vector<std::vector<uint64_t>> groups(64);  // key (v-1)*16 + placement*4 + policy
+  std::vector<std::vector<uint64_t>> groups(128);  // key (v-1)*32 + placement*8 + policy
   for (uint64_t i = 0; i < n; ++i) {
     const adaptis_plan& pl = plans[i];
     int16_t* c = &hcuts[(size_t)i * CS];
     for (int k = 1; k < pl.S; ++k) c[k] = pl.cuts[k];
     c[0] = 0;
     c[pl.S] = (int16_t)P->L;
-    groups[(pl.v - 1) * 16 + pl.placement * 4 + pl.policy].push_back(i);
+    groups[(pl.v - 1) * 32 + pl.placement * 8 + pl.policy].push_back(i);
   }
   std::vector<uint64_t> order;
   order.reserve(n);
@@ -690,10 +751,12 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
   int16_t* d_cuts = nullptr; uint64_t* d_order = nullptr;
   int64_t *d_mk = nullptr, *d_pk = nullptr, *d_rep = nullptr; float* d_bub = nullptr; uint8_t* d_st = nullptr;
   TraceBuf tb;
+  adaptis_task* d_tasks = nullptr; uint64_t* d_toff = nullptr;
   adaptis_status st = ADAPTIS_OK;
   auto cleanup = [&]() {
     cudaFree(d_cuts); cudaFree(d_order); cudaFree(d_mk); cudaFree(d_pk); cudaFree(d_rep);
     cudaFree(d_bub); cudaFree(d_st); cudaFree(tb.trace); cudaFree(tb.trace_n);
+    cudaFree(d_tasks); cudaFree(d_toff);
   };
 #define CUP(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { cleanup(); \
     return fail(ctx, ADAPTIS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
@@ -722,11 +785,18 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
     CUP(cudaMalloc(&tb.trace_n, (size_t)n * P->p * sizeof(int)));
     CUP(cudaMemsetAsync(tb.trace_n, 0, (size_t)n * P->p * sizeof(int), ctx->stream));
   }
+  if (tasks) {
+    const uint64_t ntask = offsets[n * (uint64_t)(P->p + 1) - 1];
+    CUP(cudaMalloc(&d_tasks, std::max<uint64_t>(ntask, 1) * sizeof(adaptis_task)));
+    CUP(cudaMalloc(&d_toff, n * (P->p + 1) * 8));
+    CUP(cudaMemcpyAsync(d_tasks, tasks, ntask * sizeof(adaptis_task), cudaMemcpyHostToDevice, ctx->stream));
+    CUP(cudaMemcpyAsync(d_toff, offsets, n * (P->p + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
   CUP(cudaMemcpyAsync(d_cuts, hcuts.data(), hcuts.size() * 2, cudaMemcpyHostToDevice, ctx->stream));
   CUP(cudaMemcpyAsync(d_order, order.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
   std::vector<Job> jobs;
   uint64_t off = 0;
-  for (int key = 0; key < 64; ++key) {
+  for (int key = 0; key < 128; ++key) {
     const auto& g = groups[key];
     if (g.empty()) continue;
     const adaptis_plan& pl = plans[g[0]];
@@ -740,6 +810,10 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
     j.s.n_pos = g.size(); j.s.n0 = g.size(); j.s.world = 1;
     j.s.list_out = d_order + off;
     j.s.list_cuts = d_cuts;
+    if (pl.policy == ADAPTIS_LIST || pl.policy == ADAPTIS_LIST_FUSED) {
+      j.s.list_tasks = d_tasks;
+      j.s.list_task_off = d_toff;
+    }
     j.info.group = -1; j.info.combo = sg.combo; j.info.v = pl.v;
     j.info.placement = pl.placement; j.info.policy = pl.policy;
     jobs.push_back(j);
@@ -1140,16 +1214,18 @@ adaptis_status adaptis_eval_indices(adaptis_ctx* ctx, adaptis_prepared* P, const
   return ADAPTIS_OK;
 }
 
-adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plans,
-                                  uint64_t n, const adaptis_results_soa* out, int64_t* report) {
+static adaptis_status eval_plans_common(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plans,
+                                        uint64_t n, const adaptis_results_soa* out, int64_t* report,
+                                        const adaptis_task* tasks, const uint64_t* offsets) {
   if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
   if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");
   if (n && !plans) return fail(ctx, ADAPTIS_EINVAL, "plans is NULL");
-  if (P->tick == kTickF32) return fail(ctx, ADAPTIS_EINVAL, "adaptis_eval_plans: FP32 cost mode is not supported");
+  if (P->tick == kTickF32) return fail(ctx, ADAPTIS_EINVAL, "FP32 cost mode is not supported for explicit plans");
   std::vector<int64_t> mk, pk, rep;
   std::vector<float> bub;
   std::vector<uint8_t> stt;
-  adaptis_status st = run_plans(ctx, P, plans, n, &mk, &pk, &bub, &stt, report ? &rep : nullptr, nullptr);
+  adaptis_status st = run_plans(ctx, P, plans, n, &mk, &pk, &bub, &stt, report ? &rep : nullptr, nullptr,
+                                tasks, offsets);
   if (st != ADAPTIS_OK) return st;
   for (uint64_t i = 0; i < n; ++i) {
     if (out->makespan) out->makespan[i] = mk[i];
@@ -1163,6 +1239,33 @@ adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared* P, const a
       if (stt[i] == ADAPTIS_CAND_OK || stt[i] == ADAPTIS_CAND_OVER_CAP)
         memcpy(report + (size_t)i * 5 * P->p, rep.data() + (size_t)i * 5 * P->p, (size_t)5 * P->p * 8);
   return ADAPTIS_OK;
+}
+
+adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plans,
+                                  uint64_t n, const adaptis_results_soa* out, int64_t* report) {
+  for (uint64_t i = 0; i < n && plans; ++i)
+    if (plans[i].policy == ADAPTIS_LIST || plans[i].policy == ADAPTIS_LIST_FUSED)
+      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: LIST policies go through adaptis_eval_lists",
+                  (unsigned long long)i);
+  return eval_plans_common(ctx, P, plans, n, out, report, nullptr, nullptr);
+}
+
+adaptis_status adaptis_eval_lists(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plans,
+                                  const adaptis_task* tasks, const uint64_t* offsets, uint64_t n,
+                                  const adaptis_results_soa* out, int64_t* report) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (n && (!plans || !tasks || !offsets)) return fail(ctx, ADAPTIS_EINVAL, "plans, tasks or offsets is NULL");
+  for (uint64_t i = 0; i < n; ++i) {
+    const adaptis_plan& pl = plans[i];
+    if (pl.policy != ADAPTIS_LIST && pl.policy != ADAPTIS_LIST_FUSED)
+      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu].policy = %d is not ADAPTIS_LIST or ADAPTIS_LIST_FUSED",
+                  (unsigned long long)i, pl.policy);
+    if (pl.S != P->p * pl.v || pl.S < 1 || pl.S > ADAPTIS_MAX_S)
+      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu].S = %d != p * v", (unsigned long long)i, pl.S);
+  }
+  adaptis_status st = validate_lists(ctx, P, plans, tasks, offsets, n);
+  if (st != ADAPTIS_OK) return st;
+  return eval_plans_common(ctx, P, plans, n, out, report, tasks, offsets);
 }
 
 // Pipeline Generator (reading R28): seeds, then rounds of

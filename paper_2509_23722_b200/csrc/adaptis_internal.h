@@ -73,6 +73,10 @@ struct SegLaunch {
   // list_slot[q], which holds global index slot_idx[slot]; overflowed
   // candidates record their slot, so the fallback re-run lists slots too
   const uint64_t* list_slot;
+  // LIST policies (R30): device d of candidate slot o runs
+  // list_tasks[list_task_off[o * (p + 1) + d] .. list_task_off[o * (p + 1) + d + 1])
+  const adaptis_task* list_tasks;
+  const uint64_t* list_task_off;
   const uint64_t* slot_idx;
   // report mode with communication accounting (R29): every committed task of
   // candidate o on device d is appended to trace[(o * p + d) * trace_cap + k]

@@ -29,6 +29,8 @@ static KFn pick(const SegLaunch& s, bool fb) {
     case ADAPTIS_GPIPE: return pick_policy_gpipe(s.tick, s.v, fb, tr);
     case ADAPTIS_ONEF1B: return pick_policy_onef1b(s.tick, s.v, fb, tr);
     case ADAPTIS_ZB: return pick_policy_zb(s.tick, s.v, fb, tr);
+    case ADAPTIS_LIST: return pick_policy_list(s.tick, s.v, fb, tr, false);
+    case ADAPTIS_LIST_FUSED: return pick_policy_list(s.tick, s.v, fb, tr, true);
     default: return pick_policy_greedy(s.tick, s.v, fb, tr);
   }
 }

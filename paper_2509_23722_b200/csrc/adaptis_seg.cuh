@@ -251,6 +251,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr bool FUSED = (POLICY == ADAPTIS_GPIPE || POLICY == ADAPTIS_ONEF1B);
   constexpr bool ZB = (POLICY == ADAPTIS_ZB);
+  constexpr bool LISTP = (POLICY == ADAPTIS_LIST || POLICY == ADAPTIS_LIST_FUSED);
+  constexpr bool BFUSED = FUSED || POLICY == ADAPTIS_LIST_FUSED;  // B runs t_B + t_W, frees act + stash
   constexpr bool GREEDY = (POLICY == ADAPTIS_GREEDY);
   constexpr bool kAlwaysDecide = V >= ADAPTIS_GREEDY_ALWAYS_DECIDE;
   constexpr T INF = TT<T>::INF;
@@ -407,6 +409,15 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   };
 
   auto next_task = [&]() {
+    if constexpr (LISTP) {  // R30: the next task of this device's explicit order (nF = tasks done)
+      const uint64_t* off = sl.list_task_off + cold.slot * (uint64_t)(p + 1);
+      const uint64_t b = off[d], e = off[d + 1];
+      if (b + (uint64_t)nF >= e) { tk = 3; return; }  // list finished
+      const adaptis_task t = sl.list_tasks[b + nF];
+      tk = t.kind; tc = t.stage / p; tj = t.mb;
+      tr = REC(tk, tc);
+      return;
+    }
     if (nF < tot && (POLICY == ADAPTIS_GPIPE || nF - nB <= wup)) { tk = 0; tc = fp.c; tj = fp.mb(); }
     else if (nB < tot) { tk = 1; tc = V - 1 - bp.c; tj = bp.mb(); }
     else { tk = 2; return; }
@@ -610,7 +621,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
               rf.dur = (T)cF; rf.oc = oF;
               rf.in_off = s > 0 ? row : -1;
               rf.out_off = s < S - 1 ? row + 1 : -1;
-              rb.dur = (T)(FUSED ? cB + cW : cB); rb.oc = oB;
+              rb.dur = (T)(BFUSED ? cB + cW : cB); rb.oc = oB;
               rb.in_off = s < S - 1 ? BOFF + row : -1;
               rb.out_off = s > 0 ? BOFF + row - 1 : -1;
               rw.dur = (T)cW; rw.oc = 0; rw.in_off = -1; rw.out_off = -1;
@@ -619,7 +630,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
               REC(2, c) = rw;
               if constexpr (!FUSED) {
                 DMEM(0, c) = act + sta;
-                DMEM(1, c) = -act;
+                DMEM(1, c) = BFUSED ? -(act + sta) : -act;
                 DMEM(2, c) = -sta;
               }
               ac[c] = act + sta;
@@ -753,7 +764,38 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         ofree = oaddr < 0 || ring[oaddr] == EMPTY;
       }
       __syncwarp();
-      if (live) {  // phase B: execute
+      if (LISTP && live) {  // phase B of an explicit order (R30): W at free_t, F/B when ready
+        if (tk == 2) {
+          trace_task(free_t, free_t + tr.dur, (T)0, -1);
+          free_t += tr.dur;
+          dyn += DMEM(2, tc);
+          ++nF; ++ctasks;
+          progressed = true;
+          next_task();
+        } else if (tk < 2) {
+          bool xgo = r >= 0;
+          if (xgo && !ofree) { blocked = true; xgo = false; }
+          if (xgo) {
+            const T fin = (free_t > r ? free_t : r) + tr.dur;
+            if constexpr (TRACE) {
+              const int s0 = stage_of(sl.placement, p, tc, d);
+              const int s1 = tk == 0 ? s0 + 1 : s0 - 1;
+              int tdev = (oaddr >= 0 && s1 >= 0 && s1 < S) ? dev_of(sl.placement, p, s1) : -1;
+              if (tdev == d) tdev = -1;
+              trace_task(fin - tr.dur, fin, tdev >= 0 ? tr.oc : (T)0, tdev);
+            }
+            free_t = fin;
+            if (oaddr >= 0) ring[oaddr] = fin + tr.oc;
+            if (iaddr >= 0) ring[iaddr] = EMPTY;
+            dyn += DMEM(tk, tc);
+            if (tk == 0) peak = dyn > peak ? dyn : peak;
+            ++nF; ++ctasks;
+            progressed = true;
+            next_task();
+          }
+        }
+        if (tk == 3) done = true;
+      } else if (live) {  // phase B: execute
         if constexpr (ZB) {
           // R13: (i) memory-forced W before an F that does not fit, (ii) W fill while free < r
           for (;;) {
@@ -999,5 +1041,6 @@ KFn pick_policy_gpipe(int tick, int v, bool fb, bool tr);
 KFn pick_policy_onef1b(int tick, int v, bool fb, bool tr);
 KFn pick_policy_zb(int tick, int v, bool fb, bool tr);
 KFn pick_policy_greedy(int tick, int v, bool fb, bool tr);
+KFn pick_policy_list(int tick, int v, bool fb, bool tr, bool fused);
 
 }  // namespace adaptis

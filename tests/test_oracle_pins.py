@@ -438,3 +438,54 @@ def test_comm_accounting_identity_and_bounds():
                 assert r["T_d"][d] == r["busy_d"][d] + r["comm_d"][d] + r["bubble_d"][d] - r["overlap_d"][d]
                 assert 0 <= r["exposed_d"][d] <= min(r["comm_d"][d], r["T_d"][d] - r["busy_d"][d])
     assert n > 200
+
+
+# ----------------------------------------------------------------- R30 explicit orders
+def _realised_lists(r, fused):
+    """The event loop's realised per-device order as (kind, stage, mb) lists."""
+    return [[(k, s, j) for (k, s, j, _st) in lst if not (fused and k == 2)] for lst in r["trace"]]
+
+
+def test_simulate_lists_reproduces_event_loop():
+    """Feeding the event loop's own realised order back as an explicit schedule
+    reproduces its status, makespan, T_d, busy_d and M_d, for every policy and
+    placement (fused for GPIPE / 1F1B, split for ZB / GREEDY), with binding caps."""
+    rng = W.SplitMix64(30)
+    n = 0
+    for t in range(80):
+        p = [1, 2, 3, 4][t % 4]
+        L = 2 * p + 3
+        cap = W.INT64_MAX if t % 3 else 40 + (t * 7) % 60
+        pr = W.random_problem(rng, L, p, 2 * p, tmax=7, cmax=4, bytes_max=5, cap=cap)
+        v = 1 + (t % 2)
+        S = p * v
+        cuts = sorted(random.Random(t).sample(range(1, L), S - 1))
+        combos = [(0, k) for k in range(4)] if v == 1 else [(1, k) for k in range(4)] + [(2, 0), (2, 3)]
+        for pl, po in combos:
+            r = O.simulate(pr, v, pl, po, cuts, trace=True)
+            if r["status"] == 3:
+                continue
+            fused = po in (0, 1)
+            q = O.simulate_lists(pr, v, pl, fused, cuts, _realised_lists(r, fused))
+            assert q["status"] == r["status"], (t, pl, po)
+            assert q["busy_d"] == r["busy_d"] and q["M_d"] == r["M_d"]
+            if r["status"] == 0:
+                assert q["makespan"] == r["makespan"] and q["T_d"] == r["T_d"]
+            n += 1
+    assert n > 300
+
+
+def test_simulate_lists_cyclic_wait_is_stuck():
+    """The S-1F1B lists evaluate like the policy; two devices whose orders cross
+    (d0 runs B(0,0) before sending F(0,1), d1 runs F(1,1) before sending
+    B(1,0)) wait on each other: status 3."""
+    z = [0, 0]
+    pr = W.Problem(t_f=[1, 1], t_b=[1, 1], t_w=[1, 1], act=z, stash=z, weight=z, grad=z,
+                   comm=[1, 0], p=2, m=2)
+    s1f1b = [[(0, 0, 0), (0, 0, 1), (1, 0, 0), (1, 0, 1)],   # d0: warm-up 1, then F B F B
+             [(0, 1, 0), (1, 1, 0), (0, 1, 1), (1, 1, 1)]]   # d1: F B F B (S:288 lists)
+    r = O.simulate_lists(pr, 1, 0, True, [1], s1f1b)
+    assert r["status"] == 0 and r["makespan"] == O.simulate(pr, 1, 0, 1, [1])["makespan"]
+    crossed = [[(0, 0, 0), (1, 0, 0), (0, 0, 1), (1, 0, 1)],  # d0 waits for B(1,0) before F(0,1)
+               [(0, 1, 0), (0, 1, 1), (1, 1, 0), (1, 1, 1)]]  # d1 waits for F(0,1) before B(1,0)
+    assert O.simulate_lists(pr, 1, 0, True, [1], crossed)["status"] == 3
