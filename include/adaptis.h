@@ -301,6 +301,24 @@ ADAPTIS_API adaptis_status adaptis_eval_lists(adaptis_ctx* ctx, adaptis_prepared
                                               const uint64_t* offsets, uint64_t n,
                                               const adaptis_results_soa* out, int64_t* report);
 
+/* OOM repair ("advances the execution of the latest B and W to ahead of
+ * this time to free up memory, continuing this process until all potential OOM
+ * errors are resolved"; reading R31) of one explicit schedule (policy LIST or
+ * LIST_FUSED, lists as in adaptis_eval_lists). Each step evaluates the
+ * schedule on the GPU, finds the earliest Eq. 2 violation (the first F of a
+ * device whose allocation exceeds the cap, earliest start over devices, ties
+ * to the lower device) and moves the latest-listed B of that device whose F
+ * is listed earlier and whose input has arrived by that time to just before
+ * the F (its W right after it when split). It stops when the schedule fits
+ * (result->status 0), nothing can move or it got stuck (status 2 / 3), or
+ * after max_moves moves (<= 0: the number of tasks). tasks_out (same size and
+ * offsets as the input) receives the repaired lists; *n_moves the moves made. */
+ADAPTIS_API adaptis_status adaptis_repair_oom(adaptis_ctx* ctx, adaptis_prepared* prep,
+                                              const adaptis_plan* plan, const adaptis_task* tasks,
+                                              const uint64_t* offsets, int32_t max_moves,
+                                              adaptis_task* tasks_out, adaptis_result* result,
+                                              int32_t* n_moves);
+
 /* Evaluate an explicit list of plans (Alg. 1 Steps 1-3 per plan),
  * e.g. the neighbourhood of one Pipeline Generator step. `prep`
  * must have been prepared from the same problem (any space; its tables are

@@ -410,3 +410,92 @@ def simulate_lists(pr, v, placement, fused, cuts, lists):
     status = 2 if max(Md) > pr.cap else 0
     return {**out, "status": status, "makespan": mk if status == 0 else INT64_MAX,
             "peak_mem": max(Md), "T_d": Td}
+
+
+def repair_oom(pr, v, placement, fused, cuts, lists, max_moves=0):
+    """Reading R31 ("identifies potential OOM time ... advances the
+    execution of the latest B and W to ahead of this time to free up memory,
+    continuing this process until all potential OOM errors are resolved"),
+    written out on top of simulate_lists / longest_path:
+      1. simulate the lists; stop unless the status is 2 (over the cap);
+      2. per device, walk the list's memory (R16) to the first F whose
+         allocation exceeds the cap; visit these violations by start time
+         (ties: lower device) and take the first with a movable B:
+      3. on that device, among the B listed after that F whose own F is
+         listed before it and whose input B(s+1, j) (same device: listed
+         before it; other device: finish + latency <= that time) is there,
+         take the latest listed; move it just before the F (its W right after
+         it when split);
+      4. repeat (at most max_moves moves; <= 0: the number of tasks).
+    Returns (lists, moves, simulate_lists result)."""
+    L, p = len(pr.t_f), pr.p
+    cuts = list(cuts)
+    full = cuts if (cuts and cuts[0] == 0 and cuts[-1] == L) else [0] + cuts + [L]
+    S = len(full) - 1
+
+    def ssum(col, s):
+        return int(sum(col[full[s]:full[s + 1]]))
+    act = [ssum(pr.act, s) for s in range(S)]
+    sta = [ssum(pr.stash, s) for s in range(S)]
+    wg = [ssum(pr.weight, s) + ssum(pr.grad, s) for s in range(S)]
+    dur_f = [ssum(pr.t_f, s) for s in range(S)]
+    dur_b = [ssum(pr.t_b, s) + (ssum(pr.t_w, s) if fused else 0) for s in range(S)]
+    dur_w = [ssum(pr.t_w, s) for s in range(S)]
+    dev = [device_of_stage(placement, p, v, s) for s in range(S)]
+    lists = [list(x) for x in lists]
+    total = sum(len(x) for x in lists)
+    if max_moves <= 0:
+        max_moves = total
+    moves = 0
+    while True:
+        r = simulate_lists(pr, v, placement, fused, full, lists)
+        if r["status"] != 2 or moves >= max_moves:
+            return lists, moves, r
+        lp = longest_path(pr, v, placement, full[1:-1], fused, lists)
+        starts = lp[2]
+        where = {}
+        for d in range(p):
+            for i, t in enumerate(lists[d]):
+                where[t] = (d, i)
+        viols = []
+        for d in range(p):
+            stat = sum(wg[s] for s in range(S) if dev[s] == d)
+            dyn = 0
+            for i, (k, s, j) in enumerate(lists[d]):
+                if k == 0:
+                    dyn += act[s] + sta[s]
+                    if stat + dyn > pr.cap:
+                        viols.append((starts[d][i], d, i))
+                        break
+                elif k == 1:
+                    dyn -= act[s] + (sta[s] if fused else 0)
+                else:
+                    dyn -= sta[s]
+        chosen = None
+        for tv, d, q in sorted(viols):  # earliest violation with a movable B
+            for i in range(len(lists[d]) - 1, q, -1):
+                k, s, j = lists[d][i]
+                if k != 1 or where[(0, s, j)][1] >= q:
+                    continue
+                if s + 1 < S:
+                    d2, i2 = where[(1, s + 1, j)]
+                    if d2 == d:
+                        if i2 >= q:
+                            continue
+                    else:
+                        lat = int(pr.comm[full[s + 1] - 1])
+                        if starts[d2][i2] + dur_b[s + 1] + lat > tv:
+                            continue
+                chosen = i
+                break
+            if chosen is not None:
+                break
+        if chosen is None:
+            return lists, moves, r
+        b = lists[d].pop(chosen)
+        lists[d].insert(q, b)
+        if not fused:
+            wi = lists[d].index((2, b[1], b[2]))
+            if wi > q + 1:
+                lists[d].insert(q + 1, lists[d].pop(wi))
+        moves += 1

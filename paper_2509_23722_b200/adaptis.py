@@ -174,6 +174,10 @@ def lib():
             L.adaptis_eval_lists.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
                                              C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(_ResultsSoa),
                                              C.POINTER(C.c_int64)]
+            L.adaptis_repair_oom.restype = st
+            L.adaptis_repair_oom.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
+                                             C.POINTER(C.c_uint64), C.c_int32, C.c_void_p,
+                                             C.POINTER(_Result), C.POINTER(C.c_int32)]
             L.adaptis_eval_plans.restype = st
             L.adaptis_eval_plans.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_uint64,
                                              C.POINTER(_ResultsSoa), C.POINTER(C.c_int64)]
@@ -482,6 +486,37 @@ class Prepared:
             out["T_d"], out["busy_d"], out["M_d"] = rep[:n, 0], rep[:n, 1], rep[:n, 2]
             out["comm_d"], out["exposed_d"] = rep[:n, 3], rep[:n, 4]
         return out
+
+    @staticmethod
+    def _task_arrays(lists_per_plan, p):
+        flat = [t for per_plan in lists_per_plan for dev in per_plan for t in dev]
+        tasks = np.zeros(max(1, len(flat)), dtype=[("kind", "<i2"), ("stage", "<i2"), ("mb", "<i4")])
+        for q, (k, s_, j) in enumerate(flat):
+            tasks[q] = (k, s_, j)
+        offs = np.zeros(max(1, len(lists_per_plan) * (p + 1)), np.uint64)
+        pos = 0
+        for i, per_plan in enumerate(lists_per_plan):
+            for d in range(p):
+                offs[i * (p + 1) + d] = pos
+                pos += len(per_plan[d])
+            offs[i * (p + 1) + p] = pos
+        return tasks, offs
+
+    def repair_oom(self, plan, lists, max_moves: int = 0) -> dict:
+        """adaptis_repair_oom (R31): the repaired per-device lists and their result."""
+        p = self.m.problem.p
+        arr = make_plans([plan])
+        tasks, offs = self._task_arrays([lists], p)
+        out_tasks = np.zeros_like(tasks)
+        res = _Result()
+        nm = C.c_int32()
+        _check(lib().adaptis_repair_oom(self.ctx.ptr, self.ptr, arr, tasks.ctypes.data,
+                                        offs.ctypes.data_as(C.POINTER(C.c_uint64)), max_moves,
+                                        out_tasks.ctypes.data, C.byref(res), C.byref(nm)), self.ctx.ptr)
+        rep = [[(int(t["kind"]), int(t["stage"]), int(t["mb"])) for t in out_tasks[int(offs[d]):int(offs[d + 1])]]
+               for d in range(p)]
+        return {"lists": rep, "moves": int(nm.value), "status": int(res.status),
+                "makespan": int(res.makespan), "peak_mem": int(res.peak_mem_bytes)}
 
     def eval(self, first: int, count: int, device_out: bool = False):
         """Results for [first, first+count): numpy (host) or torch CUDA tensors."""

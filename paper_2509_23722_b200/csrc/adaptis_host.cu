@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "adaptis_decode.cuh"
@@ -57,6 +58,7 @@ struct adaptis_prepared {
   int tick = kTickI32;
   std::vector<uint64_t> h_binom, h_ball;
   std::vector<int16_t> h_seeds;
+  std::vector<int64_t> h_cols, h_comm;  // host copies of the layer columns (kNumCols x L) and comm
   int group_v[ADAPTIS_MAX_GROUPS] = {0};
   // device
   double* d_colsf = nullptr;
@@ -324,6 +326,8 @@ adaptis_status upload(adaptis_ctx* ctx, const adaptis_problem* pr, adaptis_prepa
   }
   std::vector<int64_t> comm(Ly.comm_ticks, Ly.comm_ticks + L);
   comm[L - 1] = 0;
+  P->h_cols = cols;
+  P->h_comm = comm;
   CU(ctx, cudaSetDevice(ctx->device));
   if (P->tick == kTickF32) {  // the fp32-cost variant's real-valued durations and latencies
     std::vector<double> cf((size_t)3 * L);
@@ -401,6 +405,9 @@ int ring_slots(int policy, int m) {
   int mp = 1;
   while (mp < m) mp <<= 1;
   if (policy == ADAPTIS_GREEDY) return mp;  // GREEDY rings are never full: >= m slots
+  // explicit orders (R30) need not produce an edge's items in micro-batch order,
+  // so every micro-batch gets its own slot (Lemma 4 does not apply)
+  if (policy == ADAPTIS_LIST || policy == ADAPTIS_LIST_FUSED) return mp;
   int k = kRingK;
   const char* e = getenv("ADAPTIS_RING_K");
   if (e && atoi(e) > 0) k = atoi(e);
@@ -522,7 +529,8 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
     // the CTA's prefix table (6 x (L+1) int64) and the warps' state must fit in
     // shared memory; rings move to global memory when they do not fit beside them
     const bool direct_global = (s.policy == ADAPTIS_GREEDY && ring_bytes > greedy_smem_ring) ||
-                               smem_bytes(s, false) > (size_t)ctx->max_smem || s.trace != nullptr;
+                               smem_bytes(s, false) > (size_t)ctx->max_smem || s.trace != nullptr ||
+                               s.policy == ADAPTIS_LIST || s.policy == ADAPTIS_LIST_FUSED;
     if (smem_bytes(s, true) > (size_t)ctx->max_smem)
       return fail(ctx, ADAPTIS_EINVAL,
                   "layers.L = %d, S = %d: %zu B of shared memory per CTA needed, the device allows %d",
@@ -701,7 +709,10 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
                          uint64_t n, std::vector<int64_t>* mk, std::vector<int64_t>* peak,
                          std::vector<float>* bubble, std::vector<uint8_t>* status,
                          std::vector<int64_t>* report, float* kernel_ms,
-                         const adaptis_task* tasks = nullptr, const uint64_t* offsets = nullptr) {
+                         const adaptis_task* tasks = nullptr, const uint64_t* offsets = nullptr,
+                         std::vector<TraceEntry>* trace_out = nullptr, int* trace_cap_out = nullptr) {
+  std::vector<int64_t> rep_local;
+  if (trace_out && !report) report = &rep_local;  // the trace rides on the report launch
   for (uint64_t i = 0; i < n; ++i) {
     const adaptis_plan& pl = plans[i];
     if (pl.policy == ADAPTIS_LIST || pl.policy == ADAPTIS_LIST_FUSED) {
@@ -831,6 +842,12 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
   if (bubble) CUP(cudaMemcpyAsync(bubble->data(), d_bub, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CUP(cudaMemcpyAsync(status->data(), d_st, n, cudaMemcpyDeviceToHost, ctx->stream));
   if (report) CUP(cudaMemcpyAsync(report->data(), d_rep, (size_t)n * 5 * P->p * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (trace_out && account) {
+    trace_out->resize((size_t)n * P->p * tb.cap);
+    CUP(cudaMemcpyAsync(trace_out->data(), tb.trace, trace_out->size() * sizeof(TraceEntry),
+                        cudaMemcpyDeviceToHost, ctx->stream));
+    if (trace_cap_out) *trace_cap_out = tb.cap;
+  }
   CUP(cudaStreamSynchronize(ctx->stream));
 #undef CUP
   cleanup();
@@ -1141,6 +1158,143 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   if (P->tick == kTickF32) { float f; uint32_t u = (uint32_t)kv; memcpy(&f, &u, 4); agree = f == mkf; }
   else agree = mk == (int64_t)kv;
   if (!agree) return fail(ctx, ADAPTIS_ECUDA, "winner re-evaluation disagrees with its search key");
+  return ADAPTIS_OK;
+}
+
+// OOM repair (reading R31) on an explicit schedule: evaluate on the GPU
+// (with per-task start times from the trace), find the earliest Eq. 2
+// violation (the first F of a device whose allocation exceeds the cap, earliest
+// start over devices, ties to the lower device), advance the latest-listed B
+// of that device whose F is listed earlier and whose cross-device input has
+// arrived by then (its W follows it when split) to just before that F, repeat.
+adaptis_status adaptis_repair_oom(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plan,
+                                  const adaptis_task* tasks, const uint64_t* offsets, int32_t max_moves,
+                                  adaptis_task* tasks_out, adaptis_result* result, int32_t* n_moves) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!plan || !tasks || !offsets || !tasks_out || !result || !n_moves)
+    return fail(ctx, ADAPTIS_EINVAL, "a pointer argument is NULL");
+  if (P->tick == kTickF32) return fail(ctx, ADAPTIS_EINVAL, "FP32 cost mode is not supported for explicit plans");
+  if (plan->policy != ADAPTIS_LIST && plan->policy != ADAPTIS_LIST_FUSED)
+    return fail(ctx, ADAPTIS_EINVAL, "plan.policy = %d is not ADAPTIS_LIST or ADAPTIS_LIST_FUSED", plan->policy);
+  if (plan->S != P->p * plan->v || plan->S < 1 || plan->S > ADAPTIS_MAX_S)
+    return fail(ctx, ADAPTIS_EINVAL, "plan.S = %d != p * v", plan->S);
+  adaptis_status st = validate_lists(ctx, P, plan, tasks, offsets, 1);
+  if (st != ADAPTIS_OK) return st;
+  const int p = P->p, m = P->m, S = plan->S, L = P->L;
+  const bool fused = plan->policy == ADAPTIS_LIST_FUSED;
+  const uint64_t total = offsets[p];
+  if (max_moves <= 0) max_moves = (int32_t)std::min<uint64_t>(total, INT32_MAX);
+  std::vector<int> cuts(S + 1);
+  for (int i = 1; i < S; ++i) cuts[i] = plan->cuts[i];
+  cuts[0] = 0; cuts[S] = L;
+  for (int i = 0; i < S; ++i)
+    if (cuts[i] >= cuts[i + 1]) return fail(ctx, ADAPTIS_EINVAL, "plan.cuts not strictly increasing");
+  auto csum = [&](int col, int s2) {
+    int64_t x = 0;
+    for (int l = cuts[s2]; l < cuts[s2 + 1]; ++l) x += P->h_cols[(size_t)col * L + l];
+    return x;
+  };
+  std::vector<int64_t> act(S), sta(S), wg(S), xB(S, 0);
+  std::vector<int> dev(S);
+  for (int s2 = 0; s2 < S; ++s2) {
+    act[s2] = csum(kColAct, s2); sta[s2] = csum(kColStash, s2); wg[s2] = csum(kColWG, s2);
+    dev[s2] = host_dev_of(plan->placement, p, s2);
+  }
+  for (int s2 = 0; s2 + 1 < S; ++s2)  // latency of the B input of stage s2 (from stage s2 + 1)
+    xB[s2] = dev[s2 + 1] != dev[s2] ? P->h_comm[cuts[s2 + 1] - 1] : 0;
+  std::vector<adaptis_task> cur(tasks, tasks + total);
+  int32_t moves = 0;
+  std::vector<int64_t> mk, pk; std::vector<float> bub; std::vector<uint8_t> stt;
+  std::vector<TraceEntry> trace;
+  int cap = 0;
+  const int nk = fused ? 2 : 3;
+  std::vector<int> pos((size_t)nk * S * m);
+  for (;;) {
+    st = run_plans(ctx, P, plan, 1, &mk, &pk, &bub, &stt, nullptr, nullptr, cur.data(), offsets, &trace, &cap);
+    if (st != ADAPTIS_OK) return st;
+    if (stt[0] != ADAPTIS_CAND_OVER_CAP || moves >= max_moves) break;
+    for (int d = 0; d < p; ++d)
+      for (uint64_t q = offsets[d]; q < offsets[d + 1]; ++q) {
+        const adaptis_task& t = cur[q];
+        pos[((size_t)t.kind * S + t.stage) * m + t.mb] = (int)(q - offsets[d]);
+      }
+    // violations: the first F of each device over the cap; visited by start time
+    // (ties: lower device), the first with a movable B is repaired
+    std::vector<std::tuple<int64_t, int, int>> viols;
+    for (int d = 0; d < p; ++d) {
+      int64_t stat = 0, dyn = 0;
+      for (int s2 = 0; s2 < S; ++s2) if (dev[s2] == d) stat += wg[s2];
+      for (uint64_t q = offsets[d]; q < offsets[d + 1]; ++q) {
+        const adaptis_task& t = cur[q];
+        if (t.kind == 0) {
+          dyn += act[t.stage] + sta[t.stage];
+          if (stat + dyn > P->cap) {
+            const int k = (int)(q - offsets[d]);
+            viols.emplace_back(trace[(size_t)d * cap + k].start, d, k);
+            break;
+          }
+        } else if (t.kind == 1) {
+          dyn -= act[t.stage] + (fused ? sta[t.stage] : 0);
+        } else {
+          dyn -= sta[t.stage];
+        }
+      }
+    }
+    std::sort(viols.begin(), viols.end());
+    int bd = -1, bq = 0, chosen = -1;
+    uint64_t o = 0;
+    int len = 0;
+    for (const auto& vi : viols) {
+      // the latest-listed B of that device that is DAG-feasible before the violation
+      const int64_t bt = std::get<0>(vi);
+      bd = std::get<1>(vi); bq = std::get<2>(vi);
+      o = offsets[bd];
+      len = (int)(offsets[bd + 1] - o);
+      for (int r = len - 1; r > bq && chosen < 0; --r) {
+        const adaptis_task& t = cur[o + r];
+        if (t.kind != 1) continue;
+        const int s2 = t.stage, j = t.mb;
+        if (pos[((size_t)0 * S + s2) * m + j] >= bq) continue;  // its F is not yet listed
+        if (s2 + 1 < S) {
+          const int d2 = dev[s2 + 1];
+          const int pb = pos[((size_t)1 * S + s2 + 1) * m + j];
+          if (d2 == bd) {
+            if (pb >= bq) continue;  // same-device input listed after the violation
+          } else if (trace[(size_t)d2 * cap + pb].fin + xB[s2] > bt) {
+            continue;  // the input has not arrived by the violation time
+          }
+        }
+        chosen = r;
+      }
+      if (chosen >= 0) break;
+    }
+    if (chosen < 0) break;  // no violation can be repaired by advancing a B
+    const adaptis_task b = cur[o + chosen];
+    cur.erase(cur.begin() + o + chosen);
+    cur.insert(cur.begin() + o + bq, b);
+    if (!fused) {  // its W follows it
+      for (int r = bq + 1; r < len; ++r) {
+        const adaptis_task& w = cur[o + r];
+        if (w.kind == 2 && w.stage == b.stage && w.mb == b.mb) {
+          const adaptis_task wt = w;
+          cur.erase(cur.begin() + o + r);
+          cur.insert(cur.begin() + o + bq + 1, wt);
+          break;
+        }
+      }
+    }
+    ++moves;
+  }
+  std::copy(cur.begin(), cur.end(), tasks_out);
+  *n_moves = moves;
+  memset(result, 0, sizeof(*result));
+  result->makespan = mk[0];
+  result->peak_mem_bytes = pk[0];
+  result->bubble_ratio = bub[0];
+  result->status = stt[0];
+  result->makespan_f32 = stt[0] == 0 ? (float)mk[0] : INFINITY;
+  result->throughput = (stt[0] == 0 && mk[0] > 0 && P->tick_seconds > 0)
+      ? (double)m * (double)P->tokens_per_mb / ((double)mk[0] * P->tick_seconds) : 0.0;
   return ADAPTIS_OK;
 }
 

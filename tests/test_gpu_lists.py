@@ -37,6 +37,21 @@ def realised(pr, v, pl, po, cuts):
     return fused, [[(k, s, j) for (k, s, j, _t) in lst if not (fused and k == 2)] for lst in r["trace"]]
 
 
+def swap_mbs(lists, rng):
+    """Per device, emit the micro-batches of every (kind, stage) in a random order
+    (far from Lemma 4's micro-batch order) while keeping F < B < W per (stage, mb)."""
+    out = []
+    for lst in lists:
+        perm = {}
+        for (k, s, j) in lst:
+            perm.setdefault(s, None)
+        order = list(range(max(j for (_k, _s, j) in lst) + 1))
+        rng.shuffle(order)
+        rank = {j: i for i, j in enumerate(order)}
+        out.append(sorted(lst, key=lambda t: (t[0], rank[t[2]], t[1])))
+    return out
+
+
 def perturb(lists, rng, noise):
     """A random linear extension near the given order: per device, tasks keyed by
     position + noise, emitted greedily while keeping F < B < W per (stage, mb)."""
@@ -70,6 +85,25 @@ def check(prep, pr, items):
             assert list(got["M_d"][i]) == want["M_d"] and list(got["busy_d"][i]) == want["busy_d"], i
         n_stuck += want["status"] == 3
     return n_ok, n_stuck
+
+
+def test_orders_out_of_microbatch_order(ctx):
+    """Orders whose producers emit micro-batches far out of order (GPipe-like
+    lists with shuffled micro-batches): every micro-batch has its own ring slot."""
+    prng = random.Random(5)
+    rng = W.SplitMix64(505)
+    for t in range(6):
+        p = [1, 2, 3][t % 3]
+        L = 2 * p + 3
+        pr = W.random_problem(rng, L, p, 12, tmax=6, cmax=3, bytes_max=4)
+        prep = ctx.prepare(pr, W.Space([W.Group(1, W.FULL, combo_mask=0xF)]))
+        cuts = sorted(prng.sample(range(1, L), p - 1))
+        items = []
+        for po in (0, 2):
+            fused, lists = realised(pr, 1, 0, po, cuts)
+            items.append((1, 0, fused, cuts, swap_mbs(lists, prng)))
+        ok, _ = check(prep, pr, items)
+        assert ok >= 1
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3])
@@ -141,3 +175,75 @@ def test_lists_validation(ctx):
         assert e.value.status == A.EINVAL, why
     with pytest.raises(A.AdaptisError):  # W listed in a fused plan
         prep.eval_lists([plan], [[good[0] + [(2, 0, 0)], good[1]]])
+
+
+# ----------------------------------------------------------------- R31 OOM repair
+def test_repair_oom_worked_example_gpu(ctx):
+    # the oracle pin's single-device case with L = 2 rows (the library needs L >= 2):
+    # stage sums t_F 2, t_B + t_W 4, 10 B per activation, cap 25
+    pr = W.Problem(t_f=[1, 1], t_b=[1, 1], t_w=[1, 1], act=[5, 5], stash=[0, 0], weight=[0, 0],
+                   grad=[0, 0], comm=[0, 0], p=1, m=4, cap=25)
+    prep = ctx.prepare(pr, W.Space([W.Group(1, W.FULL, combo_mask=0xF)]))
+    plan = {"v": 1, "placement": 0, "policy": LIST_FUSED, "S": 1, "cuts": [0, 2]}
+    gp = [[(0, 0, j) for j in range(4)] + [(1, 0, j) for j in range(4)]]
+    r = prep.repair_oom(plan, gp)
+    assert r["moves"] == 2 and r["status"] == 0 and r["makespan"] == 24
+    assert r["lists"] == [[(0, 0, 0), (0, 0, 1), (1, 0, 1), (0, 0, 2), (1, 0, 2), (0, 0, 3), (1, 0, 0), (1, 0, 3)]]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_repair_oom_matches_oracle(ctx, seed):
+    """Over-cap realised orders of GPipe / 1F1B / ZB repaired on the GPU and by the
+    oracle: same final lists, number of moves, status and makespan."""
+    rng = W.SplitMix64(700 + seed)
+    prng = random.Random(seed)
+    n_cases = n_fixed = 0
+    for t in range(12):
+        p = [1, 2, 3, 4][t % 4]
+        L = 2 * p + 3
+        pr = W.random_problem(rng, L, p, 2 * p + 2, tmax=6, cmax=3, bytes_max=8)
+        v = 1 + (t % 2) if (2 * p + 2) % p == 0 else 1
+        S = p * v
+        cuts = sorted(prng.sample(range(1, L), S - 1))
+        pl = 0 if v == 1 else 1
+        for po in (0, 1, 2):
+            r0 = O.simulate(pr, v, pl, po, cuts, trace=True)
+            # a cap between the static memory and the schedule's peak makes it over the cap
+            stat = max(m_ - 0 for m_ in r0["M_d"])
+            pr.cap = max(1, stat - 1 - prng.randrange(0, 6))
+            r = O.simulate(pr, v, pl, po, cuts, trace=True)
+            if r["status"] != 2:
+                continue
+            fused = po in (0, 1)
+            lists = [[(k, s, j) for (k, s, j, _t) in lst if not (fused and k == 2)] for lst in r["trace"]]
+            prep = ctx.prepare(pr, W.Space([W.Group(1, W.FULL, combo_mask=0xF)]))
+            plan = {"v": v, "placement": pl, "policy": LIST_FUSED if fused else LIST, "S": S,
+                    "cuts": [0] + cuts + [L]}
+            got = prep.repair_oom(plan, lists)
+            wl, wm, wr = O.repair_oom(pr, v, pl, fused, cuts, lists)
+            assert got["moves"] == wm and got["lists"] == wl, (t, po)
+            assert got["status"] == wr["status"], (t, po)
+            if wr["status"] == 0:
+                assert got["makespan"] == wr["makespan"]
+                n_fixed += 1
+            n_cases += 1
+            pr.cap = W.INT64_MAX
+    assert n_cases > 10 and n_fixed > 0
+
+
+def test_repair_oom_cfg3_order(ctx):
+    """A cfg3 1F1B plan whose cap is tightened below its peak, repaired on the GPU
+    and by the oracle."""
+    pr, sp = W.config(3)
+    cuts = W.config(3)[1].groups[0].seed_cuts or O.seed_minmax(
+        [pr.t_f[i] + pr.t_b[i] + pr.t_w[i] for i in range(len(pr.t_f))], pr.p)[1]
+    r0 = O.simulate(pr, 1, 0, 1, cuts, trace=True)
+    pr.cap = int(max(r0["M_d"]) - 1)
+    r = O.simulate(pr, 1, 0, 1, cuts, trace=True)
+    assert r["status"] == 2
+    lists = [[(k, s, j) for (k, s, j, _t) in lst if k != 2] for lst in r["trace"]]
+    prep = ctx.prepare(pr, sp)
+    plan = {"v": 1, "placement": 0, "policy": LIST_FUSED, "S": pr.p, "cuts": [0] + list(cuts) + [len(pr.t_f)]}
+    got = prep.repair_oom(plan, lists)
+    wl, wm, wr = O.repair_oom(pr, 1, 0, True, cuts, lists)
+    assert (got["moves"], got["status"], got["lists"]) == (wm, wr["status"], wl)

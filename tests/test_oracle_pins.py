@@ -489,3 +489,42 @@ def test_simulate_lists_cyclic_wait_is_stuck():
     crossed = [[(0, 0, 0), (1, 0, 0), (0, 0, 1), (1, 0, 1)],  # d0 waits for B(1,0) before F(0,1)
                [(0, 1, 0), (0, 1, 1), (1, 1, 0), (1, 1, 1)]]  # d1 waits for F(0,1) before B(1,0)
     assert O.simulate_lists(pr, 1, 0, True, [1], crossed)["status"] == 3
+
+
+# ----------------------------------------------------------------- R31 OOM repair
+def _one_device(cap, weight=0):
+    return W.Problem(t_f=[2], t_b=[2], t_w=[1], act=[10], stash=[0], weight=[weight], grad=[0],
+                     comm=[0], p=1, m=4, cap=cap)
+
+
+def test_repair_oom_worked_example():
+    """One device, GPipe order F0 F1 F2 F3 B0 B1 B2 B3, 10 B per activation, cap 25
+    (two in flight). By hand: F2 overflows (30); the latest B whose F precedes it
+    is B1 -> F0 F1 B1 F2 F3 B0 B2 B3; now F3 overflows; the latest eligible B is
+    B2 -> F0 F1 B1 F2 B2 F3 B0 B3, which fits. Two moves, makespan unchanged (20)."""
+    pr = _one_device(25)
+    gp = [[(0, 0, j) for j in range(4)] + [(1, 0, j) for j in range(4)]]
+    lists, moves, r = O.repair_oom(pr, 1, 0, True, [], gp)
+    assert moves == 2 and r["status"] == 0 and r["makespan"] == 20
+    assert lists == [[(0, 0, 0), (0, 0, 1), (1, 0, 1), (0, 0, 2), (1, 0, 2), (0, 0, 3), (1, 0, 0), (1, 0, 3)]]
+    assert max(r["M_d"]) <= 25
+
+
+def test_repair_oom_identity_and_unrepairable():
+    gp = [[(0, 0, j) for j in range(4)] + [(1, 0, j) for j in range(4)]]
+    lists, moves, r = O.repair_oom(_one_device(40), 1, 0, True, [], gp)   # fits: identity
+    assert moves == 0 and r["status"] == 0 and lists == gp
+    lists, moves, r = O.repair_oom(_one_device(5, weight=6), 1, 0, True, [], gp)  # static > cap
+    assert moves == 0 and r["status"] == 2 and lists == gp
+
+
+def test_repair_oom_split_moves_w_with_b():
+    """Split B/W: the advanced B takes its W right behind it; stash frees at W."""
+    pr = W.Problem(t_f=[2], t_b=[2], t_w=[1], act=[6], stash=[4], weight=[0], grad=[0],
+                   comm=[0], p=1, m=3, cap=25)
+    order = [[(0, 0, 0), (0, 0, 1), (0, 0, 2), (1, 0, 0), (2, 0, 0), (1, 0, 1), (2, 0, 1),
+              (1, 0, 2), (2, 0, 2)]]
+    lists, moves, r = O.repair_oom(pr, 1, 0, False, [], order)
+    assert r["status"] == 0 and moves == 1
+    assert lists == [[(0, 0, 0), (0, 0, 1), (1, 0, 1), (2, 0, 1), (0, 0, 2), (1, 0, 0), (2, 0, 0),
+                      (1, 0, 2), (2, 0, 2)]]
