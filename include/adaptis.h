@@ -319,6 +319,25 @@ ADAPTIS_API adaptis_status adaptis_repair_oom(adaptis_ctx* ctx, adaptis_prepared
                                               adaptis_task* tasks_out, adaptis_result* result,
                                               int32_t* n_moves);
 
+/* Overlap-aware reordering ("avoid scheduling dependent computation
+ * tasks consecutively and instead delay certain computations to enable
+ * communication overlap"; reading R32) of one explicit schedule (LIST or
+ * LIST_FUSED, status 0). Each round evaluates, in one GPU batch, every
+ * schedule that moves the nearest later independent task (its own F / B
+ * already listed) in front of a task whose device idled waiting for its
+ * cross-device input, and accepts the one with the largest total OverlapTime
+ * (R29) among those whose makespan does not grow and whose overlap grows
+ * (ties: smaller makespan, then first). It stops when no candidate qualifies
+ * or after max_swaps accepted moves (<= 0: the number of tasks). tasks_out
+ * receives the tuned lists (offsets unchanged); overlap_* (may be NULL) the
+ * total OverlapTime before and after. */
+ADAPTIS_API adaptis_status adaptis_tune_overlap(adaptis_ctx* ctx, adaptis_prepared* prep,
+                                                const adaptis_plan* plan, const adaptis_task* tasks,
+                                                const uint64_t* offsets, int32_t max_swaps,
+                                                adaptis_task* tasks_out, adaptis_result* result,
+                                                int32_t* n_swaps, int64_t* overlap_before,
+                                                int64_t* overlap_after);
+
 /* Evaluate an explicit list of plans (Alg. 1 Steps 1-3 per plan),
  * e.g. the neighbourhood of one Pipeline Generator step. `prep`
  * must have been prepared from the same problem (any space; its tables are

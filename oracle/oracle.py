@@ -499,3 +499,115 @@ def repair_oom(pr, v, placement, fused, cuts, lists, max_moves=0):
             if wi > q + 1:
                 lists[d].insert(q + 1, lists[d].pop(wi))
         moves += 1
+
+
+def _list_schedule(pr, v, placement, fused, cuts, lists):
+    """Stage data, durations and the longest-path starts of explicit lists."""
+    L, p = len(pr.t_f), pr.p
+    full = list(cuts) if (cuts and cuts[0] == 0 and cuts[-1] == L) else [0] + list(cuts) + [L]
+    S = len(full) - 1
+
+    def ssum(col, s):
+        return int(sum(col[full[s]:full[s + 1]]))
+    dur = {0: [ssum(pr.t_f, s) for s in range(S)],
+           1: [ssum(pr.t_b, s) + (ssum(pr.t_w, s) if fused else 0) for s in range(S)],
+           2: [ssum(pr.t_w, s) for s in range(S)]}
+    dev = [device_of_stage(placement, p, v, s) for s in range(S)]
+    lp = longest_path(pr, v, placement, full[1:-1], fused, lists)
+    return full, S, dur, dev, lp
+
+
+def comm_accounting_lists(pr, v, placement, fused, cuts, lists):
+    """R29 for explicit lists (R30), by brute force on the tick grid of the
+    longest-path schedule: comm_d, exposed_d, overlap_d, bubble_d per device."""
+    r = simulate_lists(pr, v, placement, fused, cuts, lists)
+    p = pr.p
+    out = {k: [0] * p for k in ("comm_d", "exposed_d", "overlap_d", "bubble_d")}
+    if r["status"] not in (0, 2):
+        return {**r, **out}
+    full, S, dur, dev, lp = _list_schedule(pr, v, placement, fused, cuts, lists)
+    T = r["T_d"]
+    busy = [np.zeros(max(T[d], 1), bool) for d in range(p)]
+    xfer = [np.zeros(max(T[d], 1), bool) for d in range(p)]
+    for d in range(p):
+        for (k, s, j), st in zip(lists[d], lp[2][d]):
+            fin = st + dur[k][s]
+            busy[d][st:fin] = True
+            tgt = None
+            if k == 0 and s + 1 < S and dev[s + 1] != d:
+                tgt, lat = dev[s + 1], int(pr.comm[full[s + 1] - 1])
+            elif k == 1 and s > 0 and dev[s - 1] != d:
+                tgt, lat = dev[s - 1], int(pr.comm[full[s] - 1])
+            if tgt is None or lat == 0:
+                continue
+            for e in (d, tgt):
+                out["comm_d"][e] += lat
+                xfer[e][fin:fin + lat] = True
+    for d in range(p):
+        n = T[d]
+        out["exposed_d"][d] = int(np.count_nonzero(xfer[d][:n] & ~busy[d][:n]))
+        out["overlap_d"][d] = out["comm_d"][d] - out["exposed_d"][d]
+        out["bubble_d"][d] = T[d] - r["busy_d"][d] - out["exposed_d"][d]
+    return {**r, **out}
+
+
+def overlap_candidates(pr, v, placement, fused, cuts, lists):
+    """R32 neighbourhood: for every task X with a cross-device input whose device
+    idles before it, the schedule with the nearest later task Y independent of
+    X (Y's own F / B listed before X) moved in front of X. Returns lists of lists."""
+    full, S, dur, dev, lp = _list_schedule(pr, v, placement, fused, cuts, lists)
+    if lp is None:
+        return []
+    starts = lp[2]
+    out = []
+    for d in range(pr.p):
+        lst = lists[d]
+        where = {t: i for i, t in enumerate(lst)}
+        for i, (k, s, j) in enumerate(lst):
+            cross = (k == 0 and s > 0 and dev[s - 1] != d) or (k == 1 and s + 1 < S and dev[s + 1] != d)
+            if not cross:
+                continue
+            prev_fin = 0 if i == 0 else starts[d][i - 1] + dur[lst[i - 1][0]][lst[i - 1][1]]
+            if starts[d][i] <= prev_fin:
+                continue  # no idle gap before X: its input was not waited for
+            for q in range(i + 1, len(lst)):
+                ky, sy, jy = lst[q]
+                if ky > 0 and where[(ky - 1, sy, jy)] >= i:
+                    continue  # Y's own predecessor is not listed before X
+                new = [list(x) for x in lists]
+                y = new[d].pop(q)
+                new[d].insert(i, y)
+                out.append(new)
+                break
+    return out
+
+
+def tune_overlap(pr, v, placement, fused, cuts, lists, max_rounds=0):
+    """Reading R32 ("avoid scheduling dependent computation tasks
+    consecutively and instead delay certain computations to enable communication
+    overlap"): per round, evaluate every R32 neighbour and accept the one with
+    the largest total OverlapTime among those that keep the makespan and raise
+    the overlap (ties: smaller makespan, then first); stop when none does.
+    Returns (lists, swaps, accounting of the result)."""
+    lists = [list(x) for x in lists]
+    cur = comm_accounting_lists(pr, v, placement, fused, cuts, lists)
+    swaps = 0
+    total = sum(len(x) for x in lists)
+    max_rounds = max_rounds if max_rounds > 0 else total
+    while swaps < max_rounds and cur["status"] == 0:
+        best = None
+        for c, cand in enumerate(overlap_candidates(pr, v, placement, fused, cuts, lists)):
+            r = comm_accounting_lists(pr, v, placement, fused, cuts, cand)
+            if r["status"] != 0 or r["makespan"] > cur["makespan"]:
+                continue
+            ov = sum(r["overlap_d"])
+            if ov <= sum(cur["overlap_d"]):
+                continue
+            key = (-ov, r["makespan"], c)
+            if best is None or key < best[0]:
+                best = (key, cand, r)
+        if best is None:
+            break
+        lists, cur = best[1], best[2]
+        swaps += 1
+    return lists, swaps, cur

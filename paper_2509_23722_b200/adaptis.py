@@ -178,6 +178,11 @@ def lib():
             L.adaptis_repair_oom.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
                                              C.POINTER(C.c_uint64), C.c_int32, C.c_void_p,
                                              C.POINTER(_Result), C.POINTER(C.c_int32)]
+            L.adaptis_tune_overlap.restype = st
+            L.adaptis_tune_overlap.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
+                                               C.POINTER(C.c_uint64), C.c_int32, C.c_void_p,
+                                               C.POINTER(_Result), C.POINTER(C.c_int32),
+                                               C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
             L.adaptis_eval_plans.restype = st
             L.adaptis_eval_plans.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_uint64,
                                              C.POINTER(_ResultsSoa), C.POINTER(C.c_int64)]
@@ -517,6 +522,24 @@ class Prepared:
                for d in range(p)]
         return {"lists": rep, "moves": int(nm.value), "status": int(res.status),
                 "makespan": int(res.makespan), "peak_mem": int(res.peak_mem_bytes)}
+
+    def tune_overlap(self, plan, lists, max_swaps: int = 0) -> dict:
+        """adaptis_tune_overlap (R32): the reordered lists and their result."""
+        p = self.m.problem.p
+        arr = make_plans([plan])
+        tasks, offs = self._task_arrays([lists], p)
+        out_tasks = np.zeros_like(tasks)
+        res = _Result()
+        ns = C.c_int32()
+        ob, oa = C.c_int64(), C.c_int64()
+        _check(lib().adaptis_tune_overlap(self.ctx.ptr, self.ptr, arr, tasks.ctypes.data,
+                                          offs.ctypes.data_as(C.POINTER(C.c_uint64)), max_swaps,
+                                          out_tasks.ctypes.data, C.byref(res), C.byref(ns),
+                                          C.byref(ob), C.byref(oa)), self.ctx.ptr)
+        out = [[(int(t["kind"]), int(t["stage"]), int(t["mb"])) for t in out_tasks[int(offs[d]):int(offs[d + 1])]]
+               for d in range(p)]
+        return {"lists": out, "swaps": int(ns.value), "status": int(res.status),
+                "makespan": int(res.makespan), "overlap_before": int(ob.value), "overlap_after": int(oa.value)}
 
     def eval(self, first: int, count: int, device_out: bool = False):
         """Results for [first, first+count): numpy (host) or torch CUDA tensors."""

@@ -1298,6 +1298,116 @@ adaptis_status adaptis_repair_oom(adaptis_ctx* ctx, adaptis_prepared* P, const a
   return ADAPTIS_OK;
 }
 
+// Overlap-aware reordering (reading R32) of an explicit schedule:
+// every round evaluates, in one GPU batch, all schedules that move the nearest
+// later independent task in front of a task whose device idled waiting for its
+// cross-device input, and accepts the one with the largest total OverlapTime
+// among those that keep the makespan and raise the overlap.
+adaptis_status adaptis_tune_overlap(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plan,
+                                    const adaptis_task* tasks, const uint64_t* offsets, int32_t max_swaps,
+                                    adaptis_task* tasks_out, adaptis_result* result, int32_t* n_swaps,
+                                    int64_t* overlap_before, int64_t* overlap_after) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!plan || !tasks || !offsets || !tasks_out || !result || !n_swaps)
+    return fail(ctx, ADAPTIS_EINVAL, "a pointer argument is NULL");
+  if (P->tick == kTickF32) return fail(ctx, ADAPTIS_EINVAL, "FP32 cost mode is not supported for explicit plans");
+  if (plan->policy != ADAPTIS_LIST && plan->policy != ADAPTIS_LIST_FUSED)
+    return fail(ctx, ADAPTIS_EINVAL, "plan.policy = %d is not ADAPTIS_LIST or ADAPTIS_LIST_FUSED", plan->policy);
+  if (plan->S != P->p * plan->v || plan->S < 1 || plan->S > ADAPTIS_MAX_S)
+    return fail(ctx, ADAPTIS_EINVAL, "plan.S = %d != p * v", plan->S);
+  adaptis_status st = validate_lists(ctx, P, plan, tasks, offsets, 1);
+  if (st != ADAPTIS_OK) return st;
+  const int p = P->p, m = P->m, S = plan->S;
+  const bool fused = plan->policy == ADAPTIS_LIST_FUSED;
+  const uint64_t total = offsets[p];
+  if (max_swaps <= 0) max_swaps = (int32_t)std::min<uint64_t>(total, INT32_MAX);
+  std::vector<int> dev(S);
+  for (int s2 = 0; s2 < S; ++s2) dev[s2] = host_dev_of(plan->placement, p, s2);
+  std::vector<adaptis_task> cur(tasks, tasks + total);
+  std::vector<int64_t> mk, rep; std::vector<uint8_t> stt;
+  std::vector<TraceEntry> trace;
+  int cap = 0;
+  auto overlap_of = [&](const std::vector<int64_t>& r, size_t i) {
+    int64_t ov = 0;
+    for (int d = 0; d < p; ++d) ov += r[(i * 5 + 3) * p + d] - r[(i * 5 + 4) * p + d];
+    return ov;
+  };
+  st = run_plans(ctx, P, plan, 1, &mk, nullptr, nullptr, &stt, &rep, nullptr, cur.data(), offsets, &trace, &cap);
+  if (st != ADAPTIS_OK) return st;
+  int64_t cur_mk = mk[0], cur_ov = overlap_of(rep, 0);
+  uint8_t cur_st = stt[0];
+  if (overlap_before) *overlap_before = cur_st == 0 ? cur_ov : 0;
+  const int nk = fused ? 2 : 3;
+  std::vector<int> pos((size_t)nk * S * m);
+  int32_t swaps = 0;
+  while (cur_st == ADAPTIS_CAND_OK && swaps < max_swaps) {
+    for (int d = 0; d < p; ++d)
+      for (uint64_t q = offsets[d]; q < offsets[d + 1]; ++q) {
+        const adaptis_task& t = cur[q];
+        pos[((size_t)t.kind * S + t.stage) * m + t.mb] = (int)(q - offsets[d]);
+      }
+    // the R32 neighbourhood, all candidates concatenated
+    std::vector<adaptis_task> cand;
+    uint64_t nc = 0;
+    for (int d = 0; d < p; ++d) {
+      const uint64_t o = offsets[d];
+      const int len = (int)(offsets[d + 1] - o);
+      for (int i = 0; i < len; ++i) {
+        const adaptis_task& x = cur[o + i];
+        const bool cross = (x.kind == 0 && x.stage > 0 && dev[x.stage - 1] != d) ||
+                           (x.kind == 1 && x.stage + 1 < S && dev[x.stage + 1] != d);
+        if (!cross) continue;
+        const int64_t prev_fin = i == 0 ? 0 : trace[(size_t)d * cap + i - 1].fin;
+        if (trace[(size_t)d * cap + i].start <= prev_fin) continue;  // no idle gap before it
+        for (int q = i + 1; q < len; ++q) {
+          const adaptis_task& y = cur[o + q];
+          if (y.kind > 0 && pos[((size_t)(y.kind - 1) * S + y.stage) * m + y.mb] >= i) continue;
+          const size_t base = cand.size();
+          cand.insert(cand.end(), cur.begin(), cur.end());
+          adaptis_task* c = cand.data() + base + o;
+          const adaptis_task yy = c[q];
+          for (int r2 = q; r2 > i; --r2) c[r2] = c[r2 - 1];
+          c[i] = yy;
+          ++nc;
+          break;
+        }
+      }
+    }
+    if (nc == 0) break;
+    std::vector<adaptis_plan> cplans(nc, *plan);
+    std::vector<uint64_t> coff(nc * (p + 1));
+    for (uint64_t c = 0; c < nc; ++c)
+      for (int d = 0; d <= p; ++d) coff[c * (p + 1) + d] = c * total + offsets[d];
+    std::vector<int64_t> cmk, crep; std::vector<uint8_t> cst;
+    st = run_plans(ctx, P, cplans.data(), nc, &cmk, nullptr, nullptr, &cst, &crep, nullptr, cand.data(),
+                   coff.data());
+    if (st != ADAPTIS_OK) return st;
+    int64_t best = -1, bov = 0, bmk = 0;
+    for (uint64_t c = 0; c < nc; ++c) {
+      if (cst[c] != ADAPTIS_CAND_OK || cmk[c] > cur_mk) continue;
+      const int64_t ov = overlap_of(crep, c);
+      if (ov <= cur_ov) continue;
+      if (best < 0 || ov > bov || (ov == bov && cmk[c] < bmk)) { best = (int64_t)c; bov = ov; bmk = cmk[c]; }
+    }
+    if (best < 0) break;
+    std::copy(cand.begin() + best * total, cand.begin() + (best + 1) * total, cur.begin());
+    ++swaps;
+    st = run_plans(ctx, P, plan, 1, &mk, nullptr, nullptr, &stt, &rep, nullptr, cur.data(), offsets, &trace, &cap);
+    if (st != ADAPTIS_OK) return st;
+    cur_mk = mk[0]; cur_ov = overlap_of(rep, 0); cur_st = stt[0];
+  }
+  std::copy(cur.begin(), cur.end(), tasks_out);
+  *n_swaps = swaps;
+  if (overlap_after) *overlap_after = cur_st == 0 ? cur_ov : 0;
+  memset(result, 0, sizeof(*result));
+  result->makespan = cur_mk;
+  result->status = cur_st;
+  result->makespan_f32 = cur_st == 0 ? (float)cur_mk : INFINITY;
+  result->throughput = (cur_st == 0 && cur_mk > 0 && P->tick_seconds > 0)
+      ? (double)m * (double)P->tokens_per_mb / ((double)cur_mk * P->tick_seconds) : 0.0;
+  return ADAPTIS_OK;
+}
+
 adaptis_status adaptis_eval_indices(adaptis_ctx* ctx, adaptis_prepared* P, const uint64_t* indices,
                                     uint64_t n, const adaptis_results_soa* out) {
   if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");

@@ -247,3 +247,40 @@ def test_repair_oom_cfg3_order(ctx):
     got = prep.repair_oom(plan, lists)
     wl, wm, wr = O.repair_oom(pr, 1, 0, True, cuts, lists)
     assert (got["moves"], got["status"], got["lists"]) == (wm, wr["status"], wl)
+
+
+# ----------------------------------------------------------------- R32 overlap-aware reordering
+@pytest.mark.parametrize("seed", [1, 2])
+def test_tune_overlap_matches_oracle(ctx, seed):
+    rng = W.SplitMix64(3200 + seed)
+    prng = random.Random(seed)
+    moved = 0
+    for t in range(8):
+        p = [2, 3, 4][t % 3]
+        L = 2 * p + 3
+        pr = W.random_problem(rng, L, p, 2 * p, tmax=6, cmax=8, bytes_max=3)
+        prep = ctx.prepare(pr, W.Space([W.Group(1, W.FULL, combo_mask=0xF)]))
+        cuts = sorted(prng.sample(range(1, L), p - 1))
+        for po in (1, 2):
+            fused, lists = realised(pr, 1, 0, po, cuts)
+            if lists is None:
+                continue
+            plan = {"v": 1, "placement": 0, "policy": LIST_FUSED if fused else LIST, "S": p,
+                    "cuts": [0] + cuts + [L]}
+            got = prep.tune_overlap(plan, lists)
+            wl, ws, wa = O.tune_overlap(pr, 1, 0, fused, cuts, lists)
+            assert got["swaps"] == ws and got["lists"] == wl, (t, po)
+            assert got["makespan"] == wa["makespan"] and got["overlap_after"] == sum(wa["overlap_d"])
+            moved += ws
+    assert moved > 0
+
+
+def test_tune_overlap_cfg3_plan(ctx):
+    pr, sp = W.config(3)
+    prep = ctx.prepare(pr, sp)
+    cuts = O.seed_minmax([pr.t_f[i] + pr.t_b[i] + pr.t_w[i] for i in range(len(pr.t_f))], pr.p)[1]
+    fused, lists = realised(pr, 1, 0, 2, cuts)
+    plan = {"v": 1, "placement": 0, "policy": LIST, "S": pr.p, "cuts": [0] + list(cuts) + [len(pr.t_f)]}
+    got = prep.tune_overlap(plan, lists, max_swaps=6)
+    wl, ws, wa = O.tune_overlap(pr, 1, 0, False, cuts, lists, max_rounds=6)
+    assert (got["swaps"], got["makespan"], got["lists"]) == (ws, wa["makespan"], wl)

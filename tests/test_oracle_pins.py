@@ -528,3 +528,47 @@ def test_repair_oom_split_moves_w_with_b():
     assert r["status"] == 0 and moves == 1
     assert lists == [[(0, 0, 0), (0, 0, 1), (1, 0, 1), (2, 0, 1), (0, 0, 2), (1, 0, 0), (2, 0, 0),
                       (1, 0, 2), (2, 0, 2)]]
+
+
+# ----------------------------------------------------------------- R32 overlap-aware reordering
+def _r32_cases():
+    rng = W.SplitMix64(32)
+    for t in range(12):
+        p = [2, 3, 4][t % 3]
+        L = 2 * p + 3
+        pr = W.random_problem(rng, L, p, 2 * p, tmax=6, cmax=8, bytes_max=0)
+        cuts = sorted(random.Random(t).sample(range(1, L), p - 1))
+        for po in (1, 2):
+            r = O.simulate(pr, 1, 0, po, cuts, trace=True)
+            fused = po == 1
+            yield pr, cuts, po, fused, [[(k, s, j) for (k, s, j, _t) in lst if not (fused and k == 2)]
+                                        for lst in r["trace"]]
+
+
+def test_list_accounting_equals_policy_accounting():
+    """R29 on explicit lists (longest-path schedule) equals R29 on the event loop
+    when the lists are the event loop's own realised order."""
+    for pr, cuts, po, fused, lists in _r32_cases():
+        a = O.comm_accounting_lists(pr, 1, 0, fused, cuts, lists)
+        b = O.comm_accounting(pr, 1, 0, po, cuts)
+        for k in ("comm_d", "exposed_d", "overlap_d", "bubble_d", "T_d"):
+            assert a[k] == b[k], k
+
+
+def test_tune_overlap_invariants():
+    """Every accepted move keeps the makespan and raises the total OverlapTime; the
+    result re-simulates; zero latency gives nothing to overlap, hence no move."""
+    moved = 0
+    for pr, cuts, po, fused, lists in _r32_cases():
+        a0 = O.comm_accounting_lists(pr, 1, 0, fused, cuts, lists)
+        nl, swaps, acc = O.tune_overlap(pr, 1, 0, fused, cuts, lists)
+        assert acc["status"] == 0 and acc["makespan"] <= a0["makespan"]
+        assert (swaps == 0) == (sum(acc["overlap_d"]) == sum(a0["overlap_d"]))
+        assert sum(acc["overlap_d"]) >= sum(a0["overlap_d"]) + swaps
+        re = O.comm_accounting_lists(pr, 1, 0, fused, cuts, nl)
+        assert re["makespan"] == acc["makespan"] and re["overlap_d"] == acc["overlap_d"]
+        moved += swaps
+        pr0 = W.Problem(t_f=pr.t_f, t_b=pr.t_b, t_w=pr.t_w, act=pr.act, stash=pr.stash, weight=pr.weight,
+                        grad=pr.grad, comm=[0] * len(pr.t_f), p=pr.p, m=pr.m)
+        assert O.tune_overlap(pr0, 1, 0, fused, cuts, lists)[1] == 0
+    assert moved > 20
