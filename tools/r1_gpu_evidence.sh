@@ -1,6 +1,7 @@
 set -u
 mkdir -p gpurun_out/r1f
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r1f/pytest_gpu.txt 2>&1; tail -2 gpurun_out/r1f/pytest_gpu.txt
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/r1f/pytest_gpu.txt 2>&1; tail -2 gpurun_out/r1f/pytest_gpu.txt
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r1f/smoke.txt 2>&1; tail -1 gpurun_out/r1f/smoke.txt
 timeout 600 python bench.py > gpurun_out/r1f/bench_cfg3.json 2> gpurun_out/r1f/bench_cfg3.err; echo "bench3 rc=$?"
 timeout 600 python bench.py --impl reference > gpurun_out/r1f/bench_cfg3_reference.json 2>&1; echo "ref rc=$?"
 timeout 600 python bench.py --config 4 --no-cpu-baseline > gpurun_out/r1f/bench_cfg4.json 2>&1; echo "bench4 rc=$?"
