@@ -395,6 +395,32 @@ ADAPTIS_API adaptis_status adaptis_generate(adaptis_ctx* ctx, const adaptis_prob
                                             const adaptis_gen_options* options,
                                             adaptis_gen_result* out);
 
+/* Executor lowering (AdaPtis §5 Pipeline Executor, Table
+ * `tab:instruction_types`; reading R33; host only, no GPU needed). One
+ * instruction of a device program; comm ops carry the boundary `stage` b
+ * (between stages b and b+1), the micro-batch and the peer device; computes
+ * carry their stage and peer -1. */
+enum { ADAPTIS_OP_C_F = 0, ADAPTIS_OP_C_B = 1, ADAPTIS_OP_C_W = 2, ADAPTIS_OP_S_F = 3,
+       ADAPTIS_OP_S_B = 4, ADAPTIS_OP_R_F = 5, ADAPTIS_OP_R_B = 6, ADAPTIS_OP_W_F = 7,
+       ADAPTIS_OP_W_B = 8 };
+typedef struct { int32_t op, stage, mb, peer; } adaptis_instr;
+#define ADAPTIS_LOWER_REPAIR 1   /* hoist receives until the rendezvous run completes */
+#define ADAPTIS_LOWER_HOIST 2    /* hoist every receive as early as stays deadlock-free */
+/* Lower one explicit schedule (plan policy LIST / LIST_FUSED on p devices, lists
+ * as in adaptis_eval_lists) to per-device instruction programs: R and W before
+ * a compute with a cross-device input, S right after one with a cross-device
+ * output; then, per `flags`, deadlock repair and receive hoisting
+ * under rendezvous semantics (an S and its R proceed together). Writes
+ * the programs to out (capacity `cap`; 4 x the number of tasks always
+ * suffices) with device d at out[out_offsets[d] .. out_offsets[d+1]).
+ * EINVAL (message: adaptis_lower_error()) on invalid input, a too small `out`,
+ * or a deadlock that hoisting receives cannot repair. */
+ADAPTIS_API adaptis_status adaptis_lower(int32_t p, const adaptis_plan* plan, const adaptis_task* tasks,
+                                         const uint64_t* offsets, int32_t flags, adaptis_instr* out,
+                                         uint64_t cap, uint64_t* out_offsets, int32_t* n_repairs,
+                                         int32_t* n_hoists);
+ADAPTIS_API const char*    adaptis_lower_error(void);
+
 /* Message of the last failure on `ctx` (or of the calling thread when ctx is NULL). */
 ADAPTIS_API const char*    adaptis_last_error(const adaptis_ctx* ctx);
 ADAPTIS_API const char*    adaptis_status_str(adaptis_status s);

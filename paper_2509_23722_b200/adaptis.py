@@ -183,6 +183,11 @@ def lib():
                                                C.POINTER(C.c_uint64), C.c_int32, C.c_void_p,
                                                C.POINTER(_Result), C.POINTER(C.c_int32),
                                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+            L.adaptis_lower.restype = st
+            L.adaptis_lower.argtypes = [C.c_int32, C.POINTER(_Plan), C.c_void_p, C.POINTER(C.c_uint64),
+                                        C.c_int32, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+            L.adaptis_lower_error.restype = C.c_char_p
             L.adaptis_eval_plans.restype = st
             L.adaptis_eval_plans.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_uint64,
                                              C.POINTER(_ResultsSoa), C.POINTER(C.c_int64)]
@@ -254,6 +259,29 @@ def make_plans(plans) -> "C.Array":
         for k, c in enumerate(cuts[:S + 1]):
             arr[i].cuts[k] = int(c)
     return arr
+
+
+LOWER_REPAIR, LOWER_HOIST = 1, 2
+
+
+def lower(p: int, plan: dict, lists, repair: bool = True, hoist: bool = True) -> dict:
+    """adaptis_lower (host only, R33): per-device Table-5 instruction programs of
+    an explicit schedule, as lists of (op, stage, mb, peer)."""
+    arr = make_plans([plan])
+    tasks, offs = Prepared._task_arrays([lists], p)
+    total = int(offs[p])
+    cap = 4 * max(total, 1)
+    out = np.zeros(cap, dtype=[("op", "<i4"), ("stage", "<i4"), ("mb", "<i4"), ("peer", "<i4")])
+    ooff = np.zeros(p + 1, np.uint64)
+    nr, nh = C.c_int32(), C.c_int32()
+    flags = (LOWER_REPAIR if repair else 0) | (LOWER_HOIST if hoist else 0)
+    st = lib().adaptis_lower(p, arr, tasks.ctypes.data, offs.ctypes.data_as(C.POINTER(C.c_uint64)), flags,
+                             out.ctypes.data, cap, ooff.ctypes.data_as(C.POINTER(C.c_uint64)),
+                             C.byref(nr), C.byref(nh))
+    if st != OK:
+        raise AdaptisError(st, (lib().adaptis_lower_error() or b"").decode())
+    prog = [[tuple(int(x) for x in out[i]) for i in range(int(ooff[d]), int(ooff[d + 1]))] for d in range(p)]
+    return {"programs": prog, "repairs": int(nr.value), "hoists": int(nh.value)}
 
 
 def space_size(pr: W.Problem, sp: W.Space) -> int:
