@@ -305,7 +305,7 @@ def main():
                 "gpu_launches": launches,
                 "kernel_ms_per_step": total_kern_ms / args.steps,
                 "clocks": clk}
-        line["roofline"] = roofline(seg_ms, seg_tasks, seg_n)
+        line["roofline"] = roofline(seg_ms, seg_tasks, seg_n, args.config)
         line["generator"] = gen
         if not args.no_cpu_baseline and world == 1:
             info, _, _ = cpu_oracle_rate(pr, sp, args.cpu_seconds)
@@ -326,7 +326,20 @@ POLICY = {0: "GPIPE", 1: "ONEF1B", 2: "ZB", 3: "GREEDY"}
 PLACEMENT = {0: "SEQ", 1: "INT", 2: "WAVE"}
 
 
-def roofline(seg_ms, seg_tasks, seg_n):
+def measured_traffic(config_id, kernel):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set
+    full capture (profiles/r1_dominant_traffic.json), when it is this config's
+    same kernel; None otherwise (the contract's null)."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r1_dominant_traffic.json")))
+    except Exception:  # noqa: BLE001
+        return None
+    if t.get("config_id") != config_id or t.get("kernel") != kernel:
+        return None
+    return int(t["dram_read_bytes"]) + int(t["dram_write_bytes"])
+
+
+def roofline(seg_ms, seg_tasks, seg_n, config_id=None):
     """Issue-rate roofline of the dominant kernel: ALU/issue
     bound, no tensor cores, HBM traffic negligible. achieved = algorithmic
     lane-instructions per launch (16 per simulated F/B/W task)
@@ -354,6 +367,11 @@ def roofline(seg_ms, seg_tasks, seg_n):
                kernel_share_of_step=seg_ms[k] / tot_ms, tasks_per_launch=tasks,
                launch_ms=per_launch_ms, all_kernels_achieved=allk, all_kernels_frac=allk / peak,
                note="algorithmic work = 16 SASS lane-instr per simulated task (int64 form, SURVEY §8d)")
+    out["traffic"] = measured_traffic(config_id, out["kernel"])
+    if out["traffic"] is not None:
+        out["traffic_note"] = ("dram read+write bytes per launch, ncu --set full "
+                               "(profiles/r1_dominant_traffic.json): the global GREEDY rings' "
+                               "evictions; algorithmic bytes are ~0 (ALU bound)")
     return out
 
 
