@@ -284,3 +284,42 @@ def test_tune_overlap_cfg3_plan(ctx):
     got = prep.tune_overlap(plan, lists, max_swaps=6)
     wl, ws, wa = O.tune_overlap(pr, 1, 0, False, cuts, lists, max_rounds=6)
     assert (got["swaps"], got["makespan"], got["lists"]) == (ws, wa["makespan"], wl)
+
+
+def test_int64_kernels_for_lists_plans_and_reports(ctx, monkeypatch):
+    """The int64-tick instantiations of the explicit-plan, LIST and TRACE /
+    accounting kernels (selected when the makespan bound exceeds 2^31; forced
+    here) against the oracle, plus an OOM repair through them."""
+    monkeypatch.setenv("ADAPTIS_FORCE_INT64", "1")
+    rng = W.SplitMix64(6464)
+    prng = random.Random(64)
+    for t in range(4):
+        p = [2, 3][t % 2]
+        L = 2 * p + 4
+        pr = W.random_problem(rng, L, p, 2 * p, tmax=8, cmax=4, bytes_max=5)
+        prep = ctx.prepare(pr, W.Space([W.Group(1, W.FULL, combo_mask=0xF)]))
+        items = []
+        for v in (1, 2):
+            cuts = sorted(prng.sample(range(1, L), p * v - 1))
+            for pl, po in combos(v):
+                fused, lists = realised(pr, v, pl, po, cuts)
+                if lists is not None:
+                    items.append((v, pl, fused, cuts, lists))
+                    items.append((v, pl, fused, cuts, perturb(lists, prng, 3.0)))
+        ok, _ = check(prep, pr, items)
+        assert ok > 4
+        plans = [{"v": v, "placement": pl, "policy": po, "S": p * v, "cuts": [0] + c + [L]}
+                 for (v, c) in ((1, sorted(prng.sample(range(1, L), p - 1))),) for pl, po in combos(1)]
+        got = prep.eval_plans(plans, report=True)
+        for i, d in enumerate(plans):
+            want = O.comm_accounting(pr, d["v"], d["placement"], d["policy"], d["cuts"][1:-1])
+            assert got["status"][i] == want["status"]
+            if want["status"] == 0:
+                assert got["makespan"][i] == want["makespan"]
+                assert list(got["exposed_d"][i]) == want["exposed_d"]
+    pr = W.Problem(t_f=[1, 1], t_b=[1, 1], t_w=[1, 1], act=[5, 5], stash=[0, 0], weight=[0, 0],
+                   grad=[0, 0], comm=[0, 0], p=1, m=4, cap=25)
+    prep = ctx.prepare(pr, W.Space([W.Group(1, W.FULL, combo_mask=0xF)]))
+    r = prep.repair_oom({"v": 1, "placement": 0, "policy": LIST_FUSED, "S": 1, "cuts": [0, 2]},
+                        [[(0, 0, j) for j in range(4)] + [(1, 0, j) for j in range(4)]])
+    assert r["moves"] == 2 and r["status"] == 0 and r["makespan"] == 24
