@@ -204,8 +204,9 @@ ADAPTIS_API void           adaptis_ctx_destroy(adaptis_ctx* ctx);
 ADAPTIS_API adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_allreduce_min_fn fn, void* user);
 /* Exact lower-bound pruning for adaptis_search (default off; SURVEY §8d
  * "time-to-best-plan with and without LB pruning"): a candidate is skipped when
- * (max_d busy_d << bits | index) exceeds the best key found so far; since
- * makespan >= max_d busy_d it cannot win, so the winner is unchanged. Skipped
+ * (LB << bits | index) exceeds the best key found so far, with LB = max_d
+ * (forward time of the stages before device d's first stage + busy_d); since
+ * makespan >= LB it cannot win, so the winner is unchanged. Skipped
  * candidates are counted in adaptis_best.n_pruned. Ignored in FP32 cost mode. */
 ADAPTIS_API adaptis_status adaptis_ctx_set_prune(adaptis_ctx* ctx, int enable);
 /* The CUDA stream (cudaStream_t) every kernel of this context is queued on. */

@@ -364,9 +364,17 @@ adaptis_status upload(adaptis_ctx* ctx, const adaptis_problem* pr, adaptis_prepa
 
 adaptis_status ensure_scratch(adaptis_ctx* ctx, size_t words, size_t overflow_cap) {
   if (words > ctx->scratch_words) {
-    if (ctx->d_scratch) cudaFree(ctx->d_scratch);
-    ctx->d_scratch = nullptr;
-    CU(ctx, cudaMalloc(&ctx->d_scratch, words * 8));
+    // grow, keeping the words already there: a pass that continues from the
+    // incumbent key of a previous pass (keep_key) reads word 0 after this
+    unsigned long long* grown = nullptr;
+    CU(ctx, cudaMalloc(&grown, words * 8));
+    if (ctx->d_scratch) {
+      CU(ctx, cudaMemcpyAsync(grown, ctx->d_scratch, ctx->scratch_words * 8, cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+      CU(ctx, cudaStreamSynchronize(ctx->stream));
+      cudaFree(ctx->d_scratch);
+    }
+    ctx->d_scratch = grown;
     ctx->scratch_words = words;
   }
   if (overflow_cap > ctx->overflow_cap) {
@@ -1049,6 +1057,10 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   float ms = 0;
   adaptis_status st;
   bool seeded = false;
+  // scratch for every segment before the first pass, so the passes share one buffer
+  st = ensure_scratch(ctx, kHdr + kSegWords * std::max<size_t>(P->segs.size(), 1),
+                      kOverflowPerSeg * std::max<size_t>(P->segs.size(), 1));
+  if (st != ADAPTIS_OK) return st;
   if (ctx->prune && P->tick != kTickF32) {
     // seed pass: the first indices of every segment (the seed neighbourhood of
     // BALL spaces) give the lower-bound prune a good incumbent early; every rank
@@ -1157,7 +1169,9 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   bool agree;
   if (P->tick == kTickF32) { float f; uint32_t u = (uint32_t)kv; memcpy(&f, &u, 4); agree = f == mkf; }
   else agree = mk == (int64_t)kv;
-  if (!agree) return fail(ctx, ADAPTIS_ECUDA, "winner re-evaluation disagrees with its search key");
+  if (!agree)
+    return fail(ctx, ADAPTIS_ECUDA, "winner re-evaluation disagrees with its search key (index %llu: key makespan %llu, re-evaluated %lld, status %d)",
+                (unsigned long long)idx, (unsigned long long)kv, (long long)mk, (int)stt);
   return ADAPTIS_OK;
 }
 

@@ -709,12 +709,21 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
               for (int k = 0; k < 2 * sl.ring_k; ++k) ring[(size_t)k * RS + g * S + s] = EMPTY;
           }
           __syncwarp();
-          // exact lower-bound prune (search only): makespan >= max_d busy_d, so a
-          // candidate whose (LB << bits | index) exceeds the incumbent key cannot win
+          // exact lower-bound prune (search only): device d starts no task before the
+          // forwards of every stage ahead of its first stage (s0 = its chunk 0) have
+          // run, and then executes busy_d sequentially, so makespan >= max_d
+          // (t_F[0, cuts[s0]) + busy_d); a candidate whose (LB << bits | index)
+          // exceeds the incumbent key cannot win
           if constexpr (!FP) {
             if (sl.prune) {
-              const int64_t lb = seg_max(lane_on ? (int64_t)busy : (int64_t)0, p2);
-              const unsigned long long inc = *(volatile unsigned long long*)sl.key;
+              const int s0 = stage_of(sl.placement, p, 0, d);
+              const int64_t startup = lane_on ? (int64_t)pre[kColTF * (L + 1) + cuts[s0]] : (int64_t)0;
+              const int64_t lb = seg_max(lane_on ? (int64_t)busy + startup : (int64_t)0, p2);
+              // one read of the incumbent per slot: lanes reading it separately could
+              // straddle another warp's atomicMin and split the slot's prune decision
+              unsigned long long inc = 0;
+              if (d == 0) inc = *(volatile unsigned long long*)sl.key;
+              inc = __shfl_sync(FULLMASK, inc, leader);
               if (take && valid && !(flags & F_PREOVER) &
                   ((((unsigned long long)lb << sl.key_bits) | idx) > inc))
                 flags |= F_PRUNED;

@@ -339,3 +339,20 @@ def test_eval_indices_rejects_out_of_range(ctx):
     with pytest.raises(A.AdaptisError) as e:
         prep.eval_indices([0, 244])
     assert e.value.status == A.EINVAL and "indices[1]" in str(e.value)
+
+
+def test_pruned_search_after_smaller_space_keeps_incumbent():
+    """Regression: a pruned search on a space with more segments than the
+    context's previous one grows the scratch between its seed pass and its main
+    pass; the incumbent key must survive (it once became garbage)."""
+    from paper_2509_23722_b200 import adaptis as A
+    c = A.Context(0)
+    try:
+        c.set_prune(True)
+        pr2, sp2 = W.config(2)
+        assert c.search(pr2, sp2)["index"] == 2962620
+        pr3, sp3 = W.config(3)
+        b = c.search(pr3, sp3)
+        assert (b["index"], b["makespan"]) == (85623303, 1138352)
+    finally:
+        c.close()
