@@ -356,3 +356,37 @@ def test_pruned_search_after_smaller_space_keeps_incumbent():
         assert (b["index"], b["makespan"]) == (85623303, 1138352)
     finally:
         c.close()
+
+
+def test_context_reuse_across_calls_and_configs():
+    """One context through a mixed sequence of calls (eval, pruned and unpruned
+    searches of growing and shrinking spaces, index lists, explicit plans, the
+    generator, the int64 and fp32 kernels): every result still matches the
+    known winners or the oracle, so no per-context buffer carries stale state."""
+    from paper_2509_23722_b200 import adaptis as A
+    wins = {1: (228, 56600), 2: (2962620, 440527), 3: (85623303, 1138352), 4: (61471876, 879178)}
+    c = A.Context(0)
+    try:
+        seq = [(1, False), (4, True), (2, False), (3, True), (1, True), (3, False), (2, True)]
+        for i, (cid, prune) in enumerate(seq):
+            pr, sp = W.config(cid)
+            c.set_prune(prune)
+            b = c.search(pr, sp)
+            assert (b["index"], b["makespan"]) == wins[cid], (i, cid, prune)
+            if i % 2 == 0:  # interleave other calls on the same context
+                N = O.space_size(pr, sp)
+                idx = np.random.default_rng(i).integers(0, N, 300).astype(np.uint64)
+                got = c.prepare(pr, sp).eval_indices(idx)
+                _compare(got, O.eval_indices(pr, sp, idx), "reuse eval_indices cfg%d" % cid)
+                g = c.generate(pr)
+                assert g["status"] == 0 and g["makespan"] > 0
+        pr, sp = W.config(1)
+        got, want = _eval_range(c, pr, sp, 0, 244)
+        _compare(got, want, "reuse cfg1 eval")
+        pr.cost_type = 1  # fp32 kernels on the same context
+        r = c.eval_batch(pr, sp, 0, 244)
+        ok = np.asarray(want["status"]) == 0
+        assert np.all(np.abs(np.asarray(r["makespan_f32"])[ok] - np.asarray(want["makespan"])[ok]) <=
+                      1e-5 * np.asarray(want["makespan"])[ok])
+    finally:
+        c.close()
