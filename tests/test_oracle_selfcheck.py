@@ -159,3 +159,75 @@ def test_stuck_greedy_reports_status_3():
                    grad=[0, 0], comm=[0, 0], p=2, m=2, cap=5)
     r = O.simulate(pr, 1, W.SEQ, W.GREEDY, [1])
     assert r["status"] == 3 and r["makespan"] == O.INT64_MAX
+
+
+def test_greedy_trace_satisfies_r14_rule():
+    """An independent checker of R14 ("advances the F first, followed by the
+    B, and finally the W within the memory constraints") on the event loop's
+    GREEDY traces: at every decision of every device, the candidates are the next
+    unissued F of each own stage (only if static + dyn + act + stash fits the
+    cap), every B whose F is done, every pending W; the task started is at
+    max(device free, earliest candidate ready time) and has the smallest (kind,
+    mb, stage) key among the candidates ready by then. Ready times come from the
+    final trace (anything scheduled later is ready strictly later, R17)."""
+    import random as _r
+    rng = W.SplitMix64(1414)
+    checked = 0
+    for t in range(60):
+        p = [1, 2, 3, 4][t % 4]
+        L = 2 * p + 3
+        m = 2 * p
+        cap = W.INT64_MAX if t % 3 else 60 + 9 * t
+        pr = W.random_problem(rng, L, p, m, tmax=7, cmax=4, bytes_max=6, cap=cap)
+        v = 1 + (t % 2)
+        S = p * v
+        cuts = sorted(_r.Random(t).sample(range(1, L), S - 1))
+        for pl in ([0] if v == 1 else [1, 2]):
+            r = O.simulate(pr, v, pl, 3, cuts, trace=True)
+            if r["status"] == 3:
+                continue
+            full = [0] + cuts + [L]
+            ssum = lambda col, s: int(sum(col[full[s]:full[s + 1]]))  # noqa: E731
+            dur = {0: [ssum(pr.t_f, s) for s in range(S)], 1: [ssum(pr.t_b, s) for s in range(S)],
+                   2: [ssum(pr.t_w, s) for s in range(S)]}
+            act = [ssum(pr.act, s) for s in range(S)]
+            sta = [ssum(pr.stash, s) for s in range(S)]
+            wg = [ssum(pr.weight, s) + ssum(pr.grad, s) for s in range(S)]
+            dev = [O.device_of_stage(pl, p, v, s) for s in range(S)]
+            lat = [int(pr.comm[full[s + 1] - 1]) if s + 1 < S and dev[s + 1] != dev[s] else 0 for s in range(S)]
+            fin = {}
+            for lst in r["trace"]:
+                for (k, s, j, st) in lst:
+                    fin[(k, s, j)] = st + dur[k][s]
+
+            def ready(k, s, j):
+                if k == 0:
+                    return 0 if s == 0 else fin[(0, s - 1, j)] + lat[s - 1]
+                if k == 1:
+                    x = fin[(0, s, j)]
+                    return max(x, fin[(1, s + 1, j)] + lat[s]) if s + 1 < S else x
+                return fin[(1, s, j)]
+            for d, lst in enumerate(r["trace"]):
+                own = [s for s in range(S) if dev[s] == d]
+                stat = sum(wg[s] for s in own)
+                done, dyn, free = set(), 0, 0
+                for (k, s, j, st) in lst:
+                    cand = []
+                    for s2 in own:
+                        nf = min([j2 for j2 in range(m) if (0, s2, j2) not in done], default=None)
+                        if nf is not None and stat + dyn + act[s2] + sta[s2] <= pr.cap:
+                            cand.append((0, s2, nf))
+                        for j2 in range(m):
+                            if (0, s2, j2) in done and (1, s2, j2) not in done:
+                                cand.append((1, s2, j2))
+                            if (1, s2, j2) in done and (2, s2, j2) not in done:
+                                cand.append((2, s2, j2))
+                    at = max(free, min(ready(*c) for c in cand))
+                    assert st == at, (t, d, (k, s, j))
+                    best = min((c for c in cand if ready(*c) <= at), key=lambda c: (c[0], c[2], c[1]))
+                    assert best == (k, s, j), (t, d, best, (k, s, j))
+                    done.add((k, s, j))
+                    free = st + dur[k][s]
+                    dyn += act[s] + sta[s] if k == 0 else (-act[s] if k == 1 else -sta[s])
+                    checked += 1
+    assert checked > 3000
