@@ -231,3 +231,83 @@ def test_greedy_trace_satisfies_r14_rule():
                     dyn += act[s] + sta[s] if k == 0 else (-act[s] if k == 1 else -sta[s])
                     checked += 1
     assert checked > 3000
+
+
+def test_zb_trace_satisfies_r13_rule():
+    """An independent checker of R13 ("only reschedules W to fill bubbles")
+    on the event loop's ZB traces: the F/B tasks follow the R9/R10 list; before
+    each of them (ready time r) the oldest pending Ws (B-completion order) run
+    while the F would not fit under the cap, then while free < r; the F/B then
+    starts at max(free, r); leftover Ws run in order at the end."""
+    import random as _r
+    rng = W.SplitMix64(1313)
+    checked = 0
+    for t in range(60):
+        p = [1, 2, 3, 4][t % 4]
+        L = 2 * p + 3
+        m = 2 * p
+        cap = W.INT64_MAX if t % 3 else 60 + 9 * t
+        pr = W.random_problem(rng, L, p, m, tmax=7, cmax=4, bytes_max=6, cap=cap)
+        v = 1 + (t % 2)
+        S = p * v
+        pl = 0 if v == 1 else 1
+        cuts = sorted(_r.Random(t).sample(range(1, L), S - 1))
+        r = O.simulate(pr, v, pl, 2, cuts, trace=True)
+        if r["status"] == 3:
+            continue
+        full = [0] + cuts + [L]
+        ssum = lambda col, s: int(sum(col[full[s]:full[s + 1]]))  # noqa: E731
+        dur = {0: [ssum(pr.t_f, s) for s in range(S)], 1: [ssum(pr.t_b, s) for s in range(S)],
+               2: [ssum(pr.t_w, s) for s in range(S)]}
+        act = [ssum(pr.act, s) for s in range(S)]
+        sta = [ssum(pr.stash, s) for s in range(S)]
+        wg = [ssum(pr.weight, s) + ssum(pr.grad, s) for s in range(S)]
+        dev = [O.device_of_stage(pl, p, v, s) for s in range(S)]
+        lat = [int(pr.comm[full[s + 1] - 1]) if s + 1 < S and dev[s + 1] != dev[s] else 0 for s in range(S)]
+        fin = {(k, s, j): st + dur[k][s] for lst in r["trace"] for (k, s, j, st) in lst}
+
+        def ready(k, s, j):
+            if k == 0:
+                return 0 if s == 0 else fin[(0, s - 1, j)] + lat[s - 1]
+            x = fin[(0, s, j)]
+            return max(x, fin[(1, s + 1, j)] + lat[s]) if s + 1 < S else x
+        for d, lst in enumerate(r["trace"]):
+            fb = [(k, s, j) for (k, s, j, _st) in lst if k < 2]
+            assert fb == [tuple(x) for x in O.fixed_order(pr, v, pl, 2, cuts, d)]
+            stat = sum(wg[s] for s in range(S) if dev[s] == d)
+            pend, free, dyn, i = [], 0, 0, 0
+            for task in fb + [None]:
+                k, s, j = task if task is not None else (None, None, None)
+                # the Ws the rule runs before this F/B (or all leftovers at the end)
+                want = []
+                q = list(pend)
+                f2, dy2 = free, dyn
+                rr = ready(k, s, j) if task is not None else None
+                while q:
+                    if k is None or (k == 0 and stat + dy2 + act[s] + sta[s] > pr.cap) or f2 < rr:
+                        w = q.pop(0)
+                        want.append(w)
+                        f2 += dur[2][w[1]]
+                        dy2 -= sta[w[1]]
+                    else:
+                        break
+                for w in want:
+                    kk, ss, jj, st = lst[i]
+                    assert (kk, ss, jj) == w and st == free, (t, d, w, lst[i])
+                    free = st + dur[2][ss]
+                    dyn -= sta[ss]
+                    pend.remove(w)
+                    i += 1
+                    checked += 1
+                if k is None:
+                    break
+                kk, ss, jj, st = lst[i]
+                assert (kk, ss, jj) == (k, s, j) and st == max(free, rr), (t, d, (k, s, j), lst[i])
+                free = st + dur[k][s]
+                dyn += act[s] + sta[s] if k == 0 else -act[s]
+                if k == 1:
+                    pend.append((2, s, j))
+                i += 1
+                checked += 1
+            assert i == len(lst)
+    assert checked > 3000
