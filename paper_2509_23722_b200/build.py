@@ -26,7 +26,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     stale = not os.path.exists(LIB) or max(os.path.getmtime(f) for f in _inputs()) > os.path.getmtime(LIB)
     if not (force or stale):
         return LIB
-    extra = ["-D%s=%s" % (k, os.environ[k]) for k in ("ADAPTIS_GREEDY_MINB", "ADAPTIS_GREEDY_V4_MINB", "ADAPTIS_FIXED_V4_MINB", "ADAPTIS_GREEDY_COMMITS", "ADAPTIS_DEBUG", "ADAPTIS_KRUN", "ADAPTIS_GREEDY_ALWAYS_DECIDE") if os.environ.get(k)]
+    extra = ["-D%s=%s" % (k, os.environ[k]) for k in ("ADAPTIS_GREEDY_MINB", "ADAPTIS_GREEDY_V4_MINB", "ADAPTIS_FIXED_V4_MINB", "ADAPTIS_GREEDY_COMMITS", "ADAPTIS_DEBUG", "ADAPTIS_KRUN", "ADAPTIS_GREEDY_ALWAYS_DECIDE", "ADAPTIS_TSTAR_REDUX") if os.environ.get(k)]
     inc = ["-I", os.path.join(os.path.dirname(HERE), "include")]
     objdir = os.path.join(CSRC, "obj")
     os.makedirs(objdir, exist_ok=True)

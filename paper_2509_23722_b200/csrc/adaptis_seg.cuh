@@ -50,6 +50,9 @@ constexpr unsigned FULLMASK = 0xffffffffu;
 #define ADAPTIS_KRUN 32
 #endif
 constexpr int kRun = ADAPTIS_KRUN;  // consecutive positions a slot claims (incremental decode)
+#ifndef ADAPTIS_TSTAR_REDUX
+#define ADAPTIS_TSTAR_REDUX 0
+#endif
 #ifndef ADAPTIS_GREEDY_ALWAYS_DECIDE
 #define ADAPTIS_GREEDY_ALWAYS_DECIDE 2  // from this V up, decide() always recomputes
 #endif
@@ -128,12 +131,18 @@ __device__ __forceinline__ X seg_min(X v, int p2) {
     if (o < p2) { X w = __shfl_xor_sync(FULLMASK, v, o); v = w < v ? w : v; }
   return v;
 }
-// segment minimum over the slot's lanes `smask`: one REDUX for 32-bit ticks
-// (every slot passes its own mask), the shuffle ladder otherwise
+// segment minimum over the slot's lanes `smask`: the shuffle ladder. REDUX with
+// per-slot masks (ADAPTIS_TSTAR_REDUX) was measured 3.4 % slower on cfg3, where
+// four 8-lane slots share a warp (11.8 % of GREEDY's stall samples on it)
 template <typename X>
 __device__ __forceinline__ X seg_min_m(X v, int p2, unsigned smask) {
+#if ADAPTIS_TSTAR_REDUX
   if constexpr (std::is_same<X, int>::value) return __reduce_min_sync(smask, v);
   else return seg_min(v, p2);
+#else
+  (void)smask;
+  return seg_min(v, p2);
+#endif
 }
 template <typename X>
 __device__ __forceinline__ X seg_sum(X v, int p2) {
