@@ -302,6 +302,23 @@ ADAPTIS_API adaptis_status adaptis_eval_lists(adaptis_ctx* ctx, adaptis_prepared
                                               const uint64_t* offsets, uint64_t n,
                                               const adaptis_results_soa* out, int64_t* report);
 
+/* adaptis_eval_lists with communication-engine contention (Alg. 1 Step 3,
+ * P:322-328, with SPEC S:206 (a)/(c) and S:232; reading R34 in DESIGN.md).
+ * Same plans, lists, validation and outputs as adaptis_eval_lists, but every
+ * stage edge between different devices with latency > 0 is a transfer that,
+ * once its producer finishes, holds the sender's send engine and the
+ * receiver's receive engine together for its latency; each engine serves
+ * transfers FIFO by (eligible time, mb, stage, F before B). Memory and the
+ * stuck / over-cap status are those of the lists (R16, R26, R30). `report`
+ * rows 3-4 (comm_d, exposed_d) use the transfers' actual [start, arrival)
+ * intervals. EOVERFLOW if the serial bound (m x all task ticks + 2m x all
+ * latencies) reaches 2^40 ticks; EINVAL if the per-plan scratch
+ * (n x 5 x max S x m x 8 B) exceeds 2 GiB. Not in FP32 cost mode. */
+ADAPTIS_API adaptis_status adaptis_eval_lists_contended(adaptis_ctx* ctx, adaptis_prepared* prep,
+                                                        const adaptis_plan* plans, const adaptis_task* tasks,
+                                                        const uint64_t* offsets, uint64_t n,
+                                                        const adaptis_results_soa* out, int64_t* report);
+
 /* OOM repair ("advances the execution of the latest B and W to ahead of
  * this time to free up memory, continuing this process until all potential OOM
  * errors are resolved"; reading R31) of one explicit schedule (policy LIST or

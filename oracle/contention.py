@@ -164,15 +164,27 @@ def simulate_lists_contended(pr, v, placement, fused, cuts, lists, trace=False):
     comm = [0] * p
     exposed = [0] * p
     for d in range(p):
-        busy_t = set()
+        # sweep over the interval endpoints: count open transfers and open
+        # compute intervals, add the length where a transfer and no compute is open
+        ev = []
         for (a, b, _x) in task_iv[d]:
-            busy_t.update(range(a, b))
-        xt = set()
+            ev += [(a, 0, 1), (b, 0, -1)]
         for (src, dst, a, b, _x) in xfer_iv:
             if d in (src, dst):
                 comm[d] += b - a
-                xt.update(range(a, min(b, Td[d])))
-        exposed[d] = len(xt - busy_t)
+                ev += [(a, 1, 1), (b, 1, -1)]
+        ev.sort()
+        open_c = open_x = 0
+        prev = 0
+        for (x, kind, delta) in ev:
+            x = min(x, Td[d])
+            if open_x > 0 and open_c == 0 and x > prev:
+                exposed[d] += x - prev
+            prev = max(prev, x)
+            if kind == 0:
+                open_c += delta
+            else:
+                open_x += delta
     status = 2 if max(Md) > pr.cap else 0
     res = {"status": status, "makespan": max(Td) if status == 0 else INT64_MAX,
            "peak_mem": max(Md), "T_d": Td, "busy_d": busy, "M_d": Md,

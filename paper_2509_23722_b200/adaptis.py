@@ -174,6 +174,8 @@ def lib():
             L.adaptis_eval_lists.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
                                              C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(_ResultsSoa),
                                              C.POINTER(C.c_int64)]
+            L.adaptis_eval_lists_contended.restype = st
+            L.adaptis_eval_lists_contended.argtypes = L.adaptis_eval_lists.argtypes
             L.adaptis_repair_oom.restype = st
             L.adaptis_repair_oom.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
                                              C.POINTER(C.c_uint64), C.c_int32, C.c_void_p,
@@ -491,7 +493,12 @@ class Prepared:
             out["bubble_d"] = out["T_d"] - out["busy_d"] - out["exposed_d"]
         return out
 
-    def eval_lists(self, plans, lists, report: bool = False) -> dict:
+    def eval_lists_contended(self, plans, lists, report: bool = False) -> dict:
+        """adaptis_eval_lists_contended: eval_lists with FIFO send / receive
+        engines per device (R34)."""
+        return self.eval_lists(plans, lists, report, _contended=True)
+
+    def eval_lists(self, plans, lists, report: bool = False, _contended: bool = False) -> dict:
         """adaptis_eval_lists: plans (policy LIST = 4 / LIST_FUSED = 5) with explicit
         per-device orders lists[i][d] = [(kind, stage, mb), ...] (R30)."""
         n = len(plans)
@@ -511,7 +518,8 @@ class Prepared:
         out = _host_results(n)
         soa = _soa_from_numpy(out)
         rep = np.zeros((max(n, 1), 5, p), np.int64) if report else None
-        _check(lib().adaptis_eval_lists(self.ctx.ptr, self.ptr, arr, tasks.ctypes.data,
+        fn = lib().adaptis_eval_lists_contended if _contended else lib().adaptis_eval_lists
+        _check(fn(self.ctx.ptr, self.ptr, arr, tasks.ctypes.data,
                                         offs.ctypes.data_as(C.POINTER(C.c_uint64)), n, C.byref(soa),
                                         rep.ctypes.data_as(C.POINTER(C.c_int64)) if report else None),
                self.ctx.ptr)

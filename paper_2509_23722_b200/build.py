@@ -8,7 +8,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libadaptis.so")
 # one translation unit per policy for the segment kernels, compiled in parallel
 SOURCES = ["adaptis_inst_greedy.cu", "adaptis_inst_zb.cu", "adaptis_inst_onef1b.cu", "adaptis_inst_list.cu",
-           "adaptis_inst_gpipe.cu", "adaptis_host.cu", "adaptis_kernels.cu", "adaptis_executor.cu"]
+           "adaptis_inst_gpipe.cu", "adaptis_host.cu", "adaptis_kernels.cu", "adaptis_executor.cu",
+           "adaptis_contend.cu"]
 HEADERS = ["adaptis_internal.h", "adaptis_decode.cuh", "adaptis_seg.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

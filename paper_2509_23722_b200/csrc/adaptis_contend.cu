@@ -1,0 +1,371 @@
+// adaptis_contend.cu — Alg. 1 Step 3 on explicit per-device task
+// lists (R30) with communication-engine contention (SPEC S:206 (a)/(c),
+// S:232; reading R34 in DESIGN.md).
+//
+// One warp per plan, lane d = pipeline device d (p <= 32). Each device has a
+// compute engine, a send engine and a receive engine. A transfer (a stage edge
+// between devices with latency > 0) is eligible at its producer's finish and
+// holds the sender's send engine and the receiver's receive engine together,
+// starting at max(eligible, send free, receive free); every engine serves
+// transfers in (eligible, mb, stage, F < B) order.
+//
+// Rounds (bounded lag, the contention analogue of Lemma 3): in one round
+//   * every lane whose next listed task has all its inputs commits it (its
+//     start is exact: device free time and arrival times are known);
+//   * a lane's oldest unassigned transfer X (its sends are created in list
+//     order, at strictly increasing finish times) is assigned when its packed
+//     key (eligible << 23 | mb << 7 | stage << 1 | kind) is below every other
+//     lane's lower bound on the key of any transfer it has not assigned yet:
+//     its own oldest pending key; (t + 1) << 23 for a lane whose next task can
+//     start at t; (F + 1) << 23 for a blocked lane, F = the round's minimum over
+//     all lanes of those start times and pending eligibility times (every
+//     uncommitted task starts at >= F, because it waits for a pending transfer
+//     (eligible >= F), for a task not yet run, or for its device).
+//   Then X is next on both of its engines: no transfer with a smaller key can
+//   still appear. Two transfers into one receiver are never both assignable
+//   (each would have to be below the other), so receive engines update without
+//   conflicts. Each round commits a task or assigns the globally smallest
+//   pending transfer, so a round without either means a cyclic wait (STUCK).
+// Per-plan scratch in global memory (L2-resident at the sizes explicit lists
+// have): finish times fin[3][S][m] and output-ready times rdy[2][S][m] (-1 =
+// unknown); a stage edge's output is ready at its arrival when it travels, at
+// the producer's finish otherwise.
+#include <cstdint>
+
+#include "adaptis_internal.h"
+
+namespace adaptis {
+
+namespace {
+
+constexpr int kCWarps = 4;
+constexpr int64_t kUnknown = -1;
+constexpr unsigned long long kKeyInf = ~0ull;
+
+struct ContendArgs {
+  const int64_t* cols;          // [kNumCols][L]
+  const int64_t* comm;          // [L]
+  int L, p, m;
+  int64_t cap;
+  uint64_t n;
+  const adaptis_plan* plans;    // device copies
+  const adaptis_task* tasks;
+  const uint64_t* offsets;      // [n][p + 1]
+  int64_t* scratch;             // [n][stride]
+  uint64_t stride;              // 5 * Smax * m
+  int64_t* out_makespan;
+  int64_t* out_peak;
+  float* out_bubble;
+  uint8_t* out_status;
+  int64_t* report;              // optional [n][5][p]
+  unsigned long long* n_tasks;  // simulated tasks (work counter)
+};
+
+struct StageTab {                 // per warp, in shared memory
+  int64_t dF[ADAPTIS_MAX_S], dB[ADAPTIS_MAX_S], dW[ADAPTIS_MAX_S];
+  int64_t alloc[ADAPTIS_MAX_S], freeB[ADAPTIS_MAX_S], freeW[ADAPTIS_MAX_S], wg[ADAPTIS_MAX_S];
+  int64_t latF[ADAPTIS_MAX_S];    // transfer latency of F(s) -> F(s+1), 0 = not a transfer
+  int64_t latB[ADAPTIS_MAX_S];    // transfer latency of B(s) -> B(s-1), 0 = not a transfer
+  int64_t recv_val[32];
+  int32_t recv_round[32];
+  int8_t dev[ADAPTIS_MAX_S];
+};
+
+__device__ __forceinline__ int place(int placement, int p, int s) {  // R12
+  if (placement == ADAPTIS_SEQ) return s;
+  if (placement == ADAPTIS_INTERLEAVED) return s % p;
+  const int c = s / p, j = s - c * p;
+  return (c & 1) ? p - 1 - j : j;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
+    x = y < x ? y : x;
+  }
+  return x;
+}
+__device__ __forceinline__ int64_t warp_min_i64(int64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t y = __shfl_xor_sync(0xffffffffu, x, o);
+    x = y < x ? y : x;
+  }
+  return x;
+}
+__device__ __forceinline__ int64_t warp_max_i64(int64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t y = __shfl_xor_sync(0xffffffffu, x, o);
+    x = y > x ? y : x;
+  }
+  return x;
+}
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// length of [a, b) outside device d's compute intervals (its list, in order)
+__device__ int64_t outside_compute(int64_t a, int64_t b, const adaptis_task* lst, int len,
+                                   const int64_t* fin, const StageTab& st, int S, int m) {
+  if (b <= a) return 0;
+  // first listed task whose finish is > a (finish times increase along the list)
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const adaptis_task t = lst[mid];
+    if (fin[((size_t)t.kind * S + t.stage) * m + t.mb] > a) hi = mid; else lo = mid + 1;
+  }
+  int64_t cov = 0;
+  for (int i = lo; i < len; ++i) {
+    const adaptis_task t = lst[i];
+    const int64_t f = fin[((size_t)t.kind * S + t.stage) * m + t.mb];
+    const int64_t du = t.kind == 0 ? st.dF[t.stage] : t.kind == 1 ? st.dB[t.stage] : st.dW[t.stage];
+    const int64_t s0 = f - du;
+    if (s0 >= b) break;
+    const int64_t x0 = s0 > a ? s0 : a, x1 = f < b ? f : b;
+    if (x1 > x0) cov += x1 - x0;
+  }
+  return (b - a) - cov;
+}
+
+__global__ void __launch_bounds__(kCWarps * 32) contend_kernel(ContendArgs A) {
+  __shared__ StageTab tabs[kCWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t o = (uint64_t)blockIdx.x * kCWarps + w;
+  if (o >= A.n) return;  // warp-uniform
+  StageTab& st = tabs[w];
+  const adaptis_plan& pl = A.plans[o];
+  const int p = A.p, m = A.m, S = pl.S, L = A.L;
+  const bool fused = pl.policy == ADAPTIS_LIST_FUSED;
+  // ---- a2/a3: stage sums and edge latencies (R3-R6)
+  for (int s = lane; s < S; s += 32) {
+    const int b0 = s == 0 ? 0 : pl.cuts[s], b1 = s == S - 1 ? L : pl.cuts[s + 1];
+    int64_t c[kNumCols] = {0, 0, 0, 0, 0, 0};
+    for (int r = b0; r < b1; ++r)
+#pragma unroll
+      for (int k = 0; k < kNumCols; ++k) c[k] += A.cols[(size_t)k * L + r];
+    st.dF[s] = c[kColTF];
+    st.dB[s] = c[kColTB] + (fused ? c[kColTW] : 0);
+    st.dW[s] = c[kColTW];
+    st.alloc[s] = c[kColAct] + c[kColStash];
+    st.freeB[s] = c[kColAct] + (fused ? c[kColStash] : 0);
+    st.freeW[s] = fused ? 0 : c[kColStash];
+    st.wg[s] = c[kColWG];
+    st.dev[s] = (int8_t)place(pl.placement, p, s);
+  }
+  __syncwarp();
+  for (int s = lane; s < S; s += 32) {
+    const int b0 = s == 0 ? 0 : pl.cuts[s], b1 = s == S - 1 ? L : pl.cuts[s + 1];
+    st.latF[s] = (s + 1 < S && st.dev[s + 1] != st.dev[s]) ? A.comm[b1 - 1] : 0;
+    st.latB[s] = (s > 0 && st.dev[s - 1] != st.dev[s]) ? A.comm[b0 - 1] : 0;
+  }
+  st.recv_round[lane] = -1;
+  int64_t* fin = A.scratch + o * A.stride;           // [3][S][m]
+  int64_t* rdy = fin + (size_t)3 * S * m;            // [2][S][m]
+  for (uint64_t q = lane; q < (uint64_t)5 * S * m; q += 32) fin[q] = kUnknown;
+  __syncwarp();
+  const bool live = lane < p;
+  const uint64_t* off = A.offsets + o * (uint64_t)(p + 1);
+  const uint64_t beg = live ? off[lane] : 0, end = live ? off[lane + 1] : 0;
+  const adaptis_task* lst = A.tasks + beg;
+  const int len = (int)(end - beg);
+  int64_t stat = 0;
+  for (int s = 0; s < S; ++s)
+    if (st.dev[s] == lane) stat += st.wg[s];
+  int ptr = 0, sq = 0;
+  int64_t freet = 0, sfree = 0, rfree = 0, busy = 0, dyn = 0, peak = 0, Td = 0, commd = 0;
+  uint64_t ntask = 0;
+  bool stuck = false;
+  for (int round = 0;; ++round) {
+    // (1) can my next listed task start, and when?
+    int64_t t = INT64_MAX;
+    adaptis_task X{};
+    if (ptr < len) {
+      X = lst[ptr];
+      const size_t jm = (size_t)X.stage * m + X.mb;
+      int64_t r0 = freet;
+      bool ok = true;
+      if (X.kind == 0) {
+        if (X.stage > 0) {
+          const int64_t a = ((volatile int64_t*)rdy)[jm - m];  // F(s-1, j), over the edge
+          ok = a >= 0; r0 = a > r0 ? a : r0;
+        }
+      } else if (X.kind == 1) {
+        const int64_t a = ((volatile int64_t*)fin)[jm];       // F(s, j), same device
+        ok = a >= 0; r0 = a > r0 ? a : r0;
+        if (X.stage + 1 < S) {
+          const int64_t b = ((volatile int64_t*)rdy)[(size_t)S * m + jm + m];  // B(s+1, j)
+          ok = ok && b >= 0; r0 = b > r0 ? b : r0;
+        }
+      } else {
+        const int64_t a = ((volatile int64_t*)fin)[(size_t)S * m + jm];  // B(s, j), same device
+        ok = a >= 0; r0 = a > r0 ? a : r0;
+      }
+      if (ok) t = r0;
+    }
+    // (2) my oldest unassigned transfer
+    adaptis_task Y{};
+    int64_t lat = 0;
+    while (sq < ptr) {
+      Y = lst[sq];
+      lat = Y.kind == 0 ? st.latF[Y.stage] : Y.kind == 1 ? st.latB[Y.stage] : 0;
+      if (lat > 0) break;
+      ++sq;
+    }
+    unsigned long long hk = kKeyInf;
+    int64_t he = INT64_MAX;
+    if (sq < ptr) {
+      he = ((volatile int64_t*)fin)[((size_t)Y.kind * S + Y.stage) * m + Y.mb];
+      hk = ((unsigned long long)he << 23) | ((unsigned long long)Y.mb << 7) |
+           ((unsigned long long)Y.stage << 1) | (unsigned long long)Y.kind;
+    }
+    // (3) F: earliest known start or pending eligibility over the warp
+    const int64_t F = warp_min_i64(t < he ? t : he);
+    // (4) my lower bound on the key of any transfer I have not assigned
+    unsigned long long lb;
+    if (sq < ptr) lb = hk;
+    else if (ptr >= len) lb = kKeyInf;
+    else if (t != INT64_MAX) lb = (unsigned long long)(t + 1) << 23;
+    else lb = F == INT64_MAX ? kKeyInf : (unsigned long long)(F + 1) << 23;
+    // (5) minimum over the other lanes: global min, its lane, and the runner-up
+    const unsigned long long m1 = warp_min_u64(lb);
+    const unsigned arg_mask = __ballot_sync(0xffffffffu, lb == m1);
+    const int arg = __ffs(arg_mask) - 1;
+    const unsigned long long m2 = warp_min_u64(lane == arg ? kKeyInf : lb);
+    const unsigned long long other = lane == arg ? m2 : m1;
+    // equality can only be with another lane's bound (head keys are unique), and
+    // no unassigned transfer of that lane can have exactly that key
+    const bool safe = sq < ptr && hk <= other;
+    // (6) assign the safe transfers
+    const int dst = safe ? (int)st.dev[Y.kind == 0 ? Y.stage + 1 : Y.stage - 1] : lane;
+    const int64_t rf = __shfl_sync(0xffffffffu, rfree, dst);
+    if (safe) {
+      const int64_t s0 = he > sfree ? he : sfree;
+      const int64_t start = s0 > rf ? s0 : rf;
+      const int64_t arr = start + lat;
+      rdy[(size_t)(Y.kind == 0 ? 0 : 1) * S * m + (size_t)Y.stage * m + Y.mb] = arr;
+      sfree = arr;
+      commd += lat;
+      st.recv_val[dst] = arr;
+      st.recv_round[dst] = round;
+      ++sq;
+    }
+    // (7) commit my task
+    const bool commit = t != INT64_MAX;
+    if (commit) {
+      const int64_t du = X.kind == 0 ? st.dF[X.stage] : X.kind == 1 ? st.dB[X.stage] : st.dW[X.stage];
+      const int64_t f = t + du;
+      const size_t jm = (size_t)X.stage * m + X.mb;
+      fin[(size_t)X.kind * S * m + jm] = f;
+      freet = f;
+      Td = f;
+      busy += du;
+      if (X.kind == 0) {
+        dyn += st.alloc[X.stage];
+        peak = dyn > peak ? dyn : peak;
+        if (st.latF[X.stage] == 0) rdy[jm] = f;  // same device or zero latency: no transfer
+      } else if (X.kind == 1) {
+        dyn -= st.freeB[X.stage];
+        if (st.latB[X.stage] == 0) rdy[(size_t)S * m + jm] = f;
+      } else {
+        dyn -= st.freeW[X.stage];
+      }
+      ++ptr;
+      ++ntask;
+    }
+    __syncwarp();
+    if (live && st.recv_round[lane] == round) rfree = st.recv_val[lane];
+    const bool progress = __any_sync(0xffffffffu, safe || commit);
+    __syncwarp();
+    if (!progress) {
+      stuck = __any_sync(0xffffffffu, ptr < len);
+      break;
+    }
+  }
+  // ---- a6: per-device report and per-plan metrics
+  const int64_t Md = stat + peak;
+  const int64_t makespan = warp_max_i64(live ? Td : 0);
+  const int64_t peak_all = warp_max_i64(live ? Md : 0);
+  const int64_t busy_all = warp_sum_i64(live ? busy : 0);
+  const bool over = peak_all > A.cap;
+  const uint8_t status = stuck ? ADAPTIS_CAND_STUCK : over ? ADAPTIS_CAND_OVER_CAP : ADAPTIS_CAND_OK;
+  // R29 on the contended schedule: comm_d = latencies of the transfers d sends
+  // or receives; exposed_d = |(sends U receives) within [0, T_d]| outside compute
+  int64_t comm_in = 0, exposed = 0;
+  if (A.report && live && !stuck) {
+    // sends (disjoint, in list order) and receives (disjoint): inclusion-exclusion
+    int64_t ex_s = 0, ex_r = 0, ex_sr = 0;
+    for (int i = 0; i < len; ++i) {
+      const adaptis_task U = lst[i];
+      const size_t jm = (size_t)U.stage * m + U.mb;
+      // my send of U's output
+      const int64_t ls = U.kind == 0 ? st.latF[U.stage] : U.kind == 1 ? st.latB[U.stage] : 0;
+      if (ls > 0) {
+        const int64_t a1 = rdy[(size_t)(U.kind == 0 ? 0 : 1) * S * m + jm];
+        const int64_t a0 = a1 - ls, b0 = a1 < Td ? a1 : Td;
+        ex_s += outside_compute(a0, b0, lst, len, fin, st, S, m);
+      }
+      // my receive of U's cross-device input
+      int64_t lr = 0, r1 = 0;
+      if (U.kind == 0 && U.stage > 0 && st.latF[U.stage - 1] > 0) {
+        lr = st.latF[U.stage - 1]; r1 = rdy[jm - m];
+      } else if (U.kind == 1 && U.stage + 1 < S && st.latB[U.stage + 1] > 0) {
+        lr = st.latB[U.stage + 1]; r1 = rdy[(size_t)S * m + jm + m];
+      }
+      if (lr > 0) {
+        comm_in += lr;
+        const int64_t r0 = r1 - lr, rb = r1 < Td ? r1 : Td;
+        ex_r += outside_compute(r0, rb, lst, len, fin, st, S, m);
+        // overlap of this receive with my sends (both families disjoint)
+        for (int k2 = 0; k2 < len; ++k2) {
+          const adaptis_task V = lst[k2];
+          const int64_t lv = V.kind == 0 ? st.latF[V.stage] : V.kind == 1 ? st.latB[V.stage] : 0;
+          if (lv <= 0) continue;
+          const int64_t v1 = rdy[(size_t)(V.kind == 0 ? 0 : 1) * S * m + (size_t)V.stage * m + V.mb];
+          const int64_t v0 = v1 - lv;
+          const int64_t x0 = v0 > r0 ? v0 : r0;
+          int64_t x1 = v1 < rb ? v1 : rb;
+          if (x1 > x0) ex_sr += outside_compute(x0, x1, lst, len, fin, st, S, m);
+        }
+      }
+    }
+    exposed = ex_s + ex_r - ex_sr;
+  }
+  if (A.report && live) {
+    int64_t* rep = A.report + o * 5 * (uint64_t)p;
+    rep[lane] = stuck ? 0 : Td;
+    rep[p + lane] = busy;
+    rep[2 * p + lane] = Md;
+    rep[3 * p + lane] = stuck ? 0 : commd + comm_in;
+    rep[4 * p + lane] = stuck ? 0 : exposed;
+  }
+  const unsigned long long nt = warp_sum_i64((int64_t)ntask);
+  if (lane == 0) {
+    A.out_status[o] = status;
+    A.out_makespan[o] = status == ADAPTIS_CAND_OK ? makespan : INT64_MAX;
+    A.out_peak[o] = stuck ? 0 : peak_all;
+    A.out_bubble[o] = status == ADAPTIS_CAND_OK
+                          ? (float)(1.0 - (double)busy_all / ((double)p * (double)makespan)) : 0.0f;
+    atomicAdd(A.n_tasks, nt);
+  }
+}
+
+}  // namespace
+
+int launch_contend(const int64_t* cols, const int64_t* comm, int L, int p, int m, int64_t cap, uint64_t n,
+                   const adaptis_plan* plans, const adaptis_task* tasks, const uint64_t* offsets,
+                   int64_t* scratch, uint64_t stride, int64_t* makespan, int64_t* peak, float* bubble,
+                   uint8_t* status, int64_t* report, unsigned long long* n_tasks, void* stream) {
+  if (n == 0) return 0;
+  ContendArgs A{cols, comm, L, p, m, cap, n, plans, tasks, offsets, scratch, stride,
+                makespan, peak, bubble, status, report, n_tasks};
+  const unsigned grid = (unsigned)((n + kCWarps - 1) / kCWarps);
+  contend_kernel<<<grid, kCWarps * 32, 0, (cudaStream_t)stream>>>(A);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace adaptis

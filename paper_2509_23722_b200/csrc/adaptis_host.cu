@@ -1546,6 +1546,121 @@ adaptis_status adaptis_eval_lists(adaptis_ctx* ctx, adaptis_prepared* P, const a
   return eval_plans_common(ctx, P, plans, n, out, report, tasks, offsets);
 }
 
+// R34: explicit lists with communication-engine contention (adaptis_contend.cu)
+adaptis_status adaptis_eval_lists_contended(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plans,
+                                            const adaptis_task* tasks, const uint64_t* offsets, uint64_t n,
+                                            const adaptis_results_soa* out, int64_t* report) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");
+  if (n && (!plans || !tasks || !offsets)) return fail(ctx, ADAPTIS_EINVAL, "plans, tasks or offsets is NULL");
+  if (P->tick == kTickF32) return fail(ctx, ADAPTIS_EINVAL, "FP32 cost mode is not supported for explicit plans");
+  const int p = P->p, m = P->m, L = P->L;
+  int Smax = 1;
+  std::vector<adaptis_plan> hp(plans, plans + n);
+  for (uint64_t i = 0; i < n; ++i) {
+    adaptis_plan& pl = hp[i];
+    if (pl.policy != ADAPTIS_LIST && pl.policy != ADAPTIS_LIST_FUSED)
+      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu].policy = %d is not ADAPTIS_LIST or ADAPTIS_LIST_FUSED",
+                  (unsigned long long)i, pl.policy);
+    const bool ok_pl = pl.v == 1 ? pl.placement == ADAPTIS_SEQ
+                                 : (pl.placement == ADAPTIS_INTERLEAVED || pl.placement == ADAPTIS_WAVE);
+    if (pl.v < 1 || pl.v > ADAPTIS_MAX_V || pl.S != p * pl.v || pl.S > ADAPTIS_MAX_S || pl.S > L ||
+        (pl.v > 1 && m % p != 0) || !ok_pl)
+      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: v = %d, S = %d, placement %d not admitted (R10, R12)",
+                  (unsigned long long)i, pl.v, pl.S, pl.placement);
+    pl.cuts[0] = 0;
+    pl.cuts[pl.S] = (int16_t)L;
+    for (int k = 0; k < pl.S; ++k)
+      if (pl.cuts[k + 1] <= pl.cuts[k])
+        return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: cuts are not strictly increasing in [1, L-1]",
+                    (unsigned long long)i);
+    Smax = std::max(Smax, pl.S);
+  }
+  adaptis_status st = validate_lists(ctx, P, hp.data(), tasks, offsets, n);
+  if (st != ADAPTIS_OK) return st;
+  // packed transfer keys hold eligibility times < 2^40: bound the makespan by
+  // every task and every transfer run back to back
+  {
+    long double bound = 0;
+    for (int l = 0; l < L; ++l)
+      bound += (long double)m * (P->h_cols[(size_t)kColTF * L + l] + P->h_cols[(size_t)kColTB * L + l] +
+                                 P->h_cols[(size_t)kColTW * L + l]) +
+               2.0L * m * P->h_comm[l];
+    if (bound >= (long double)(1ull << 40))
+      return fail(ctx, ADAPTIS_EOVERFLOW, "serial bound %.0Lf ticks >= 2^40 (contention keys)", bound);
+  }
+  const uint64_t stride = (uint64_t)5 * Smax * m;
+  if ((long double)n * stride * 8 > (long double)(1ull << 31))
+    return fail(ctx, ADAPTIS_EINVAL, "%llu plans need %.0Lf B of scratch (> 2 GiB): split the list",
+                (unsigned long long)n, (long double)n * stride * 8);
+  if (n == 0) return ADAPTIS_OK;
+  CU(ctx, cudaSetDevice(ctx->device));
+  const uint64_t ntask = offsets[n * (uint64_t)(p + 1) - 1];
+  adaptis_plan* d_plans = nullptr; adaptis_task* d_tasks = nullptr; uint64_t* d_off = nullptr;
+  int64_t *d_scr = nullptr, *d_mk = nullptr, *d_pk = nullptr, *d_rep = nullptr;
+  float* d_bub = nullptr; uint8_t* d_st = nullptr; unsigned long long* d_nt = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(d_plans); cudaFree(d_tasks); cudaFree(d_off); cudaFree(d_scr); cudaFree(d_mk);
+    cudaFree(d_pk); cudaFree(d_rep); cudaFree(d_bub); cudaFree(d_st); cudaFree(d_nt);
+  };
+#define CUC(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { cleanup(); \
+    return fail(ctx, ADAPTIS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
+  CUC(cudaMalloc(&d_plans, n * sizeof(adaptis_plan)));
+  CUC(cudaMalloc(&d_tasks, std::max<uint64_t>(ntask, 1) * sizeof(adaptis_task)));
+  CUC(cudaMalloc(&d_off, n * (p + 1) * 8));
+  CUC(cudaMalloc(&d_scr, n * stride * 8));
+  CUC(cudaMalloc(&d_mk, n * 8));
+  CUC(cudaMalloc(&d_pk, n * 8));
+  CUC(cudaMalloc(&d_bub, n * 4));
+  CUC(cudaMalloc(&d_st, n));
+  CUC(cudaMalloc(&d_nt, 8));
+  if (report) CUC(cudaMalloc(&d_rep, n * 5 * p * 8));
+  CUC(cudaMemcpyAsync(d_plans, hp.data(), n * sizeof(adaptis_plan), cudaMemcpyHostToDevice, ctx->stream));
+  CUC(cudaMemcpyAsync(d_tasks, tasks, ntask * sizeof(adaptis_task), cudaMemcpyHostToDevice, ctx->stream));
+  CUC(cudaMemcpyAsync(d_off, offsets, n * (p + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CUC(cudaMemsetAsync(d_nt, 0, 8, ctx->stream));
+  CUC(cudaEventRecord(ctx->ev0, ctx->stream));
+  const int e = launch_contend(P->d_cols, P->d_comm, L, p, m, P->cap, n, d_plans, d_tasks, d_off, d_scr, stride,
+                               d_mk, d_pk, d_bub, d_st, d_rep, d_nt, ctx->stream);
+  if (e) { cleanup(); return fail(ctx, ADAPTIS_ECUDA, "contention kernel: %s", cudaGetErrorString((cudaError_t)e)); }
+  CUC(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->launches += 1;
+  std::vector<int64_t> mk(n), pk(n), rep(report ? n * 5 * p : 0);
+  std::vector<float> bub(n);
+  std::vector<uint8_t> stt(n);
+  unsigned long long nt = 0;
+  CUC(cudaMemcpyAsync(mk.data(), d_mk, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUC(cudaMemcpyAsync(pk.data(), d_pk, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUC(cudaMemcpyAsync(bub.data(), d_bub, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CUC(cudaMemcpyAsync(stt.data(), d_st, n, cudaMemcpyDeviceToHost, ctx->stream));
+  CUC(cudaMemcpyAsync(&nt, d_nt, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (report) CUC(cudaMemcpyAsync(rep.data(), d_rep, n * 5 * p * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUC(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  ctx->counters[0] += nt;
+  ctx->last_tasks = nt;
+  ctx->last_info.clear();
+  adaptis_launch_info li{};
+  li.group = -1; li.combo = -1; li.v = hp[0].v; li.placement = hp[0].placement; li.policy = hp[0].policy;
+  li.candidates = n; li.tasks = nt; li.ms = ms;
+  ctx->last_info.push_back(li);
+#undef CUC
+  cleanup();
+  for (uint64_t i = 0; i < n; ++i) {
+    if (out->makespan) out->makespan[i] = mk[i];
+    if (out->peak_mem_bytes) out->peak_mem_bytes[i] = pk[i];
+    if (out->bubble_ratio) out->bubble_ratio[i] = bub[i];
+    if (out->status) out->status[i] = stt[i];
+    if (out->makespan_f32) out->makespan_f32[i] = stt[i] == 0 ? (float)mk[i] : INFINITY;
+  }
+  if (report)
+    for (uint64_t i = 0; i < n; ++i)
+      if (stt[i] == ADAPTIS_CAND_OK || stt[i] == ADAPTIS_CAND_OVER_CAP)
+        memcpy(report + (size_t)i * 5 * p, rep.data() + (size_t)i * 5 * p, (size_t)5 * p * 8);
+  return ADAPTIS_OK;
+}
+
 // Pipeline Generator (reading R28): seeds, then rounds of
 // partition / placement / schedule tuning, each accepted only if it strictly
 // lowers the makespan (rollback otherwise), until a round changes nothing.

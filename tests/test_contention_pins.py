@@ -178,6 +178,14 @@ def test_trace_satisfies_the_defining_equations():
             continue
         _check_equations(pr, v, pl, fused, cuts, lists, r)
         for d in range(pr.p):  # R29 identity with the contended transfers
+            # exposed_d by brute force on the tick grid
+            busy_t, xt = set(), set()
+            for (a, b_, _x) in r["tasks"][d]:
+                busy_t.update(range(a, b_))
+            for (src, dst, a, b_, _x) in r["transfers"]:
+                if d in (src, dst):
+                    xt.update(range(a, min(b_, r["T_d"][d])))
+            assert r["exposed_d"][d] == len(xt - busy_t)
             assert 0 <= r["exposed_d"][d] <= r["comm_d"][d]
             assert r["T_d"][d] - r["busy_d"][d] - r["exposed_d"][d] >= 0
         n += 1
