@@ -61,15 +61,17 @@ struct ContendArgs {
   unsigned long long* n_tasks;  // simulated tasks (work counter)
 };
 
-struct StageTab {                 // per warp, in shared memory
-  int64_t dF[ADAPTIS_MAX_S], dB[ADAPTIS_MAX_S], dW[ADAPTIS_MAX_S];
-  int64_t alloc[ADAPTIS_MAX_S], freeB[ADAPTIS_MAX_S], freeW[ADAPTIS_MAX_S], wg[ADAPTIS_MAX_S];
-  int64_t latF[ADAPTIS_MAX_S];    // transfer latency of F(s) -> F(s+1), 0 = not a transfer
-  int64_t latB[ADAPTIS_MAX_S];    // transfer latency of B(s) -> B(s-1), 0 = not a transfer
-  int64_t recv_val[32];
-  int32_t recv_round[32];
-  int8_t dev[ADAPTIS_MAX_S];
+// per-slot stage table in dynamic shared memory: kTabCols int64 arrays of Sm
+// entries, then Sm device ids (int8)
+constexpr int kTabCols = 9;
+enum { kTF = 0, kTB, kTW, kAlloc, kFreeB, kFreeW, kWG, kLatF, kLatB };
+struct Tab {
+  int64_t* t;
+  int Sm;
+  __device__ __forceinline__ int64_t& at(int col, int s) const { return t[col * Sm + s]; }
+  __device__ __forceinline__ int8_t& dev(int s) const { return ((int8_t*)(t + kTabCols * Sm))[s]; }
 };
+__host__ __device__ __forceinline__ int tab_bytes(int Sm) { return (kTabCols * Sm * 8 + Sm + 15) & ~15; }
 
 __device__ __forceinline__ int place(int placement, int p, int s) {  // R12
   if (placement == ADAPTIS_SEQ) return s;
@@ -78,39 +80,43 @@ __device__ __forceinline__ int place(int placement, int p, int s) {  // R12
   return (c & 1) ? p - 1 - j : j;
 }
 
-__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+// reductions over aligned segments of p2 lanes (one candidate slot each)
+__device__ __forceinline__ unsigned long long seg_min_u64(unsigned long long x, int p2) {
+  for (int o = p2 >> 1; o > 0; o >>= 1) {
     const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
     x = y < x ? y : x;
   }
   return x;
 }
-__device__ __forceinline__ int64_t warp_min_i64(int64_t x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+__device__ __forceinline__ int64_t seg_min_i64(int64_t x, int p2) {
+  for (int o = p2 >> 1; o > 0; o >>= 1) {
     const int64_t y = __shfl_xor_sync(0xffffffffu, x, o);
     x = y < x ? y : x;
   }
   return x;
 }
-__device__ __forceinline__ int64_t warp_max_i64(int64_t x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+__device__ __forceinline__ int64_t seg_max_i64(int64_t x, int p2) {
+  for (int o = p2 >> 1; o > 0; o >>= 1) {
     const int64_t y = __shfl_xor_sync(0xffffffffu, x, o);
     x = y > x ? y : x;
   }
   return x;
 }
-__device__ __forceinline__ int64_t warp_sum_i64(int64_t x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+__device__ __forceinline__ int64_t seg_sum_i64(int64_t x, int p2) {
+  for (int o = p2 >> 1; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
 }
 
-// length of [a, b) outside device d's compute intervals (its list, in order)
+__device__ __forceinline__ int64_t dur_of(const Tab& tb, const adaptis_task& t) {
+  return t.kind == 0 ? tb.at(kTF, t.stage) : t.kind == 1 ? tb.at(kTB, t.stage) : tb.at(kTW, t.stage);
+}
+__device__ __forceinline__ int64_t out_lat(const Tab& tb, const adaptis_task& t) {
+  return t.kind == 0 ? tb.at(kLatF, t.stage) : t.kind == 1 ? tb.at(kLatB, t.stage) : 0;
+}
+
+// length of [a, b) outside the device's compute intervals (its list, in order)
 __device__ int64_t outside_compute(int64_t a, int64_t b, const adaptis_task* lst, int len,
-                                   const int64_t* fin, const StageTab& st, int S, int m) {
+                                   const int64_t* fin, const Tab& tb, int S, int m) {
   if (b <= a) return 0;
   // first listed task whose finish is > a (finish times increase along the list)
   int lo = 0, hi = len;
@@ -123,8 +129,7 @@ __device__ int64_t outside_compute(int64_t a, int64_t b, const adaptis_task* lst
   for (int i = lo; i < len; ++i) {
     const adaptis_task t = lst[i];
     const int64_t f = fin[((size_t)t.kind * S + t.stage) * m + t.mb];
-    const int64_t du = t.kind == 0 ? st.dF[t.stage] : t.kind == 1 ? st.dB[t.stage] : st.dW[t.stage];
-    const int64_t s0 = f - du;
+    const int64_t s0 = f - dur_of(tb, t);
     if (s0 >= b) break;
     const int64_t x0 = s0 > a ? s0 : a, x1 = f < b ? f : b;
     if (x1 > x0) cov += x1 - x0;
@@ -132,59 +137,67 @@ __device__ int64_t outside_compute(int64_t a, int64_t b, const adaptis_task* lst
   return (b - a) - cov;
 }
 
-__global__ void __launch_bounds__(kCWarps * 32) contend_kernel(ContendArgs A) {
-  __shared__ StageTab tabs[kCWarps];
+// G = 32 / p2 plans per warp (p2 = p rounded up to a power of two); lane
+// slot * p2 + d is device d of the slot's plan
+__global__ void __launch_bounds__(kCWarps * 32) contend_kernel(ContendArgs A, int p2, int Sm) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int64_t recv_val[kCWarps][32];
+  __shared__ int32_t recv_round[kCWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint64_t o = (uint64_t)blockIdx.x * kCWarps + w;
-  if (o >= A.n) return;  // warp-uniform
-  StageTab& st = tabs[w];
-  const adaptis_plan& pl = A.plans[o];
-  const int p = A.p, m = A.m, S = pl.S, L = A.L;
+  const int G = 32 / p2, slot = lane / p2, d = lane - slot * p2, base = slot * p2;
+  const unsigned smask = (p2 == 32 ? 0xffffffffu : ((1u << p2) - 1u)) << base;
+  const uint64_t o = ((uint64_t)blockIdx.x * kCWarps + w) * G + slot;
+  if (((uint64_t)blockIdx.x * kCWarps + w) * G >= A.n) return;  // warp-uniform
+  const bool valid = o < A.n;
+  const Tab tb{(int64_t*)(smem + (size_t)(w * G + slot) * tab_bytes(Sm)), Sm};
+  const adaptis_plan& pl = A.plans[valid ? o : 0];
+  const int p = A.p, m = A.m, L = A.L;
+  const int S = valid ? pl.S : 0;
   const bool fused = pl.policy == ADAPTIS_LIST_FUSED;
   // ---- a2/a3: stage sums and edge latencies (R3-R6)
-  for (int s = lane; s < S; s += 32) {
+  for (int s = d; s < S; s += p2) {
     const int b0 = s == 0 ? 0 : pl.cuts[s], b1 = s == S - 1 ? L : pl.cuts[s + 1];
     int64_t c[kNumCols] = {0, 0, 0, 0, 0, 0};
     for (int r = b0; r < b1; ++r)
 #pragma unroll
       for (int k = 0; k < kNumCols; ++k) c[k] += A.cols[(size_t)k * L + r];
-    st.dF[s] = c[kColTF];
-    st.dB[s] = c[kColTB] + (fused ? c[kColTW] : 0);
-    st.dW[s] = c[kColTW];
-    st.alloc[s] = c[kColAct] + c[kColStash];
-    st.freeB[s] = c[kColAct] + (fused ? c[kColStash] : 0);
-    st.freeW[s] = fused ? 0 : c[kColStash];
-    st.wg[s] = c[kColWG];
-    st.dev[s] = (int8_t)place(pl.placement, p, s);
+    tb.at(kTF, s) = c[kColTF];
+    tb.at(kTB, s) = c[kColTB] + (fused ? c[kColTW] : 0);
+    tb.at(kTW, s) = c[kColTW];
+    tb.at(kAlloc, s) = c[kColAct] + c[kColStash];
+    tb.at(kFreeB, s) = c[kColAct] + (fused ? c[kColStash] : 0);
+    tb.at(kFreeW, s) = fused ? 0 : c[kColStash];
+    tb.at(kWG, s) = c[kColWG];
+    tb.dev(s) = (int8_t)place(pl.placement, p, s);
   }
   __syncwarp();
-  for (int s = lane; s < S; s += 32) {
+  for (int s = d; s < S; s += p2) {
     const int b0 = s == 0 ? 0 : pl.cuts[s], b1 = s == S - 1 ? L : pl.cuts[s + 1];
-    st.latF[s] = (s + 1 < S && st.dev[s + 1] != st.dev[s]) ? A.comm[b1 - 1] : 0;
-    st.latB[s] = (s > 0 && st.dev[s - 1] != st.dev[s]) ? A.comm[b0 - 1] : 0;
+    tb.at(kLatF, s) = (s + 1 < S && tb.dev(s + 1) != tb.dev(s)) ? A.comm[b1 - 1] : 0;
+    tb.at(kLatB, s) = (s > 0 && tb.dev(s - 1) != tb.dev(s)) ? A.comm[b0 - 1] : 0;
   }
-  st.recv_round[lane] = -1;
-  int64_t* fin = A.scratch + o * A.stride;           // [3][S][m]
-  int64_t* rdy = fin + (size_t)3 * S * m;            // [2][S][m]
-  for (uint64_t q = lane; q < (uint64_t)5 * S * m; q += 32) fin[q] = kUnknown;
+  recv_round[w][lane] = -1;
+  int64_t* fin = A.scratch + (valid ? o : 0) * A.stride;  // [3][S][m]
+  int64_t* rdy = fin + (size_t)3 * S * m;                  // [2][S][m]
+  for (uint64_t q = d; q < (uint64_t)5 * S * m; q += p2) fin[q] = kUnknown;
   __syncwarp();
-  const bool live = lane < p;
-  const uint64_t* off = A.offsets + o * (uint64_t)(p + 1);
-  const uint64_t beg = live ? off[lane] : 0, end = live ? off[lane + 1] : 0;
+  const bool live = valid && d < p;
+  const uint64_t* off = A.offsets + (valid ? o : 0) * (uint64_t)(p + 1);
+  const uint64_t beg = live ? off[d] : 0, end = live ? off[d + 1] : 0;
   const adaptis_task* lst = A.tasks + beg;
   const int len = (int)(end - beg);
   int64_t stat = 0;
   for (int s = 0; s < S; ++s)
-    if (st.dev[s] == lane) stat += st.wg[s];
+    if (tb.dev(s) == d) stat += tb.at(kWG, s);
   int ptr = 0, sq = 0;
   int64_t freet = 0, sfree = 0, rfree = 0, busy = 0, dyn = 0, peak = 0, Td = 0, commd = 0;
   uint64_t ntask = 0;
-  bool stuck = false;
+  bool stuck = false, done = !valid;
   for (int round = 0;; ++round) {
     // (1) can my next listed task start, and when?
     int64_t t = INT64_MAX;
     adaptis_task X{};
-    if (ptr < len) {
+    if (!done && ptr < len) {
       X = lst[ptr];
       const size_t jm = (size_t)X.stage * m + X.mb;
       int64_t r0 = freet;
@@ -212,7 +225,7 @@ __global__ void __launch_bounds__(kCWarps * 32) contend_kernel(ContendArgs A) {
     int64_t lat = 0;
     while (sq < ptr) {
       Y = lst[sq];
-      lat = Y.kind == 0 ? st.latF[Y.stage] : Y.kind == 1 ? st.latB[Y.stage] : 0;
+      lat = out_lat(tb, Y);
       if (lat > 0) break;
       ++sq;
     }
@@ -223,26 +236,26 @@ __global__ void __launch_bounds__(kCWarps * 32) contend_kernel(ContendArgs A) {
       hk = ((unsigned long long)he << 23) | ((unsigned long long)Y.mb << 7) |
            ((unsigned long long)Y.stage << 1) | (unsigned long long)Y.kind;
     }
-    // (3) F: earliest known start or pending eligibility over the warp
-    const int64_t F = warp_min_i64(t < he ? t : he);
+    // (3) F: earliest known start or pending eligibility over the slot
+    const int64_t F = seg_min_i64(t < he ? t : he, p2);
     // (4) my lower bound on the key of any transfer I have not assigned
     unsigned long long lb;
     if (sq < ptr) lb = hk;
-    else if (ptr >= len) lb = kKeyInf;
+    else if (done || ptr >= len) lb = kKeyInf;
     else if (t != INT64_MAX) lb = (unsigned long long)(t + 1) << 23;
     else lb = F == INT64_MAX ? kKeyInf : (unsigned long long)(F + 1) << 23;
-    // (5) minimum over the other lanes: global min, its lane, and the runner-up
-    const unsigned long long m1 = warp_min_u64(lb);
-    const unsigned arg_mask = __ballot_sync(0xffffffffu, lb == m1);
+    // (5) minimum over the slot's other lanes: the min, its lane, the runner-up
+    const unsigned long long m1 = seg_min_u64(lb, p2);
+    const unsigned arg_mask = __ballot_sync(0xffffffffu, lb == m1) & smask;
     const int arg = __ffs(arg_mask) - 1;
-    const unsigned long long m2 = warp_min_u64(lane == arg ? kKeyInf : lb);
+    const unsigned long long m2 = seg_min_u64(lane == arg ? kKeyInf : lb, p2);
     const unsigned long long other = lane == arg ? m2 : m1;
     // equality can only be with another lane's bound (head keys are unique), and
     // no unassigned transfer of that lane can have exactly that key
     const bool safe = sq < ptr && hk <= other;
     // (6) assign the safe transfers
-    const int dst = safe ? (int)st.dev[Y.kind == 0 ? Y.stage + 1 : Y.stage - 1] : lane;
-    const int64_t rf = __shfl_sync(0xffffffffu, rfree, dst);
+    const int dst = safe ? (int)tb.dev(Y.kind == 0 ? Y.stage + 1 : Y.stage - 1) : d;
+    const int64_t rf = __shfl_sync(0xffffffffu, rfree, base + dst);
     if (safe) {
       const int64_t s0 = he > sfree ? he : sfree;
       const int64_t start = s0 > rf ? s0 : rf;
@@ -250,14 +263,14 @@ __global__ void __launch_bounds__(kCWarps * 32) contend_kernel(ContendArgs A) {
       rdy[(size_t)(Y.kind == 0 ? 0 : 1) * S * m + (size_t)Y.stage * m + Y.mb] = arr;
       sfree = arr;
       commd += lat;
-      st.recv_val[dst] = arr;
-      st.recv_round[dst] = round;
+      recv_val[w][base + dst] = arr;
+      recv_round[w][base + dst] = round;
       ++sq;
     }
     // (7) commit my task
     const bool commit = t != INT64_MAX;
     if (commit) {
-      const int64_t du = X.kind == 0 ? st.dF[X.stage] : X.kind == 1 ? st.dB[X.stage] : st.dW[X.stage];
+      const int64_t du = dur_of(tb, X);
       const int64_t f = t + du;
       const size_t jm = (size_t)X.stage * m + X.mb;
       fin[(size_t)X.kind * S * m + jm] = f;
@@ -265,32 +278,38 @@ __global__ void __launch_bounds__(kCWarps * 32) contend_kernel(ContendArgs A) {
       Td = f;
       busy += du;
       if (X.kind == 0) {
-        dyn += st.alloc[X.stage];
+        dyn += tb.at(kAlloc, X.stage);
         peak = dyn > peak ? dyn : peak;
-        if (st.latF[X.stage] == 0) rdy[jm] = f;  // same device or zero latency: no transfer
+        if (tb.at(kLatF, X.stage) == 0) rdy[jm] = f;  // same device or zero latency: no transfer
       } else if (X.kind == 1) {
-        dyn -= st.freeB[X.stage];
-        if (st.latB[X.stage] == 0) rdy[(size_t)S * m + jm] = f;
+        dyn -= tb.at(kFreeB, X.stage);
+        if (tb.at(kLatB, X.stage) == 0) rdy[(size_t)S * m + jm] = f;
       } else {
-        dyn -= st.freeW[X.stage];
+        dyn -= tb.at(kFreeW, X.stage);
       }
       ++ptr;
       ++ntask;
     }
     __syncwarp();
-    if (live && st.recv_round[lane] == round) rfree = st.recv_val[lane];
-    const bool progress = __any_sync(0xffffffffu, safe || commit);
-    __syncwarp();
-    if (!progress) {
-      stuck = __any_sync(0xffffffffu, ptr < len);
-      break;
+    if (live && recv_round[w][lane] == round) rfree = recv_val[w][lane];
+    // a slot without a commit or an assignment is finished (or stuck)
+    const unsigned prog = __ballot_sync(0xffffffffu, safe || commit);
+    const unsigned left = __ballot_sync(0xffffffffu, !done && ptr < len);
+    if (!done && (prog & smask) == 0) {
+      done = true;
+      stuck = (left & smask) != 0;
     }
+    if (__all_sync(0xffffffffu, done)) break;
+    __syncwarp();
   }
   // ---- a6: per-device report and per-plan metrics
   const int64_t Md = stat + peak;
-  const int64_t makespan = warp_max_i64(live ? Td : 0);
-  const int64_t peak_all = warp_max_i64(live ? Md : 0);
-  const int64_t busy_all = warp_sum_i64(live ? busy : 0);
+  const int64_t makespan = seg_max_i64(live ? Td : 0, p2);
+  const int64_t peak_all = seg_max_i64(live ? Md : 0, p2);
+  const int64_t busy_all = seg_sum_i64(live ? busy : 0, p2);
+  const unsigned long long nt = (unsigned long long)seg_sum_i64((int64_t)ntask, 32);
+  if (lane == 0) atomicAdd(A.n_tasks, nt);
+  if (!valid) return;
   const bool over = peak_all > A.cap;
   const uint8_t status = stuck ? ADAPTIS_CAND_STUCK : over ? ADAPTIS_CAND_OVER_CAP : ADAPTIS_CAND_OK;
   // R29 on the contended schedule: comm_d = latencies of the transfers d sends
@@ -302,34 +321,29 @@ __global__ void __launch_bounds__(kCWarps * 32) contend_kernel(ContendArgs A) {
     for (int i = 0; i < len; ++i) {
       const adaptis_task U = lst[i];
       const size_t jm = (size_t)U.stage * m + U.mb;
-      // my send of U's output
-      const int64_t ls = U.kind == 0 ? st.latF[U.stage] : U.kind == 1 ? st.latB[U.stage] : 0;
+      const int64_t ls = out_lat(tb, U);  // my send of U's output
       if (ls > 0) {
         const int64_t a1 = rdy[(size_t)(U.kind == 0 ? 0 : 1) * S * m + jm];
-        const int64_t a0 = a1 - ls, b0 = a1 < Td ? a1 : Td;
-        ex_s += outside_compute(a0, b0, lst, len, fin, st, S, m);
+        ex_s += outside_compute(a1 - ls, a1 < Td ? a1 : Td, lst, len, fin, tb, S, m);
       }
-      // my receive of U's cross-device input
-      int64_t lr = 0, r1 = 0;
-      if (U.kind == 0 && U.stage > 0 && st.latF[U.stage - 1] > 0) {
-        lr = st.latF[U.stage - 1]; r1 = rdy[jm - m];
-      } else if (U.kind == 1 && U.stage + 1 < S && st.latB[U.stage + 1] > 0) {
-        lr = st.latB[U.stage + 1]; r1 = rdy[(size_t)S * m + jm + m];
+      int64_t lr = 0, r1 = 0;             // my receive of U's cross-device input
+      if (U.kind == 0 && U.stage > 0 && tb.at(kLatF, U.stage - 1) > 0) {
+        lr = tb.at(kLatF, U.stage - 1); r1 = rdy[jm - m];
+      } else if (U.kind == 1 && U.stage + 1 < S && tb.at(kLatB, U.stage + 1) > 0) {
+        lr = tb.at(kLatB, U.stage + 1); r1 = rdy[(size_t)S * m + jm + m];
       }
       if (lr > 0) {
         comm_in += lr;
         const int64_t r0 = r1 - lr, rb = r1 < Td ? r1 : Td;
-        ex_r += outside_compute(r0, rb, lst, len, fin, st, S, m);
-        // overlap of this receive with my sends (both families disjoint)
-        for (int k2 = 0; k2 < len; ++k2) {
+        ex_r += outside_compute(r0, rb, lst, len, fin, tb, S, m);
+        for (int k2 = 0; k2 < len; ++k2) {  // overlap of this receive with my sends
           const adaptis_task V = lst[k2];
-          const int64_t lv = V.kind == 0 ? st.latF[V.stage] : V.kind == 1 ? st.latB[V.stage] : 0;
+          const int64_t lv = out_lat(tb, V);
           if (lv <= 0) continue;
           const int64_t v1 = rdy[(size_t)(V.kind == 0 ? 0 : 1) * S * m + (size_t)V.stage * m + V.mb];
           const int64_t v0 = v1 - lv;
-          const int64_t x0 = v0 > r0 ? v0 : r0;
-          int64_t x1 = v1 < rb ? v1 : rb;
-          if (x1 > x0) ex_sr += outside_compute(x0, x1, lst, len, fin, st, S, m);
+          const int64_t x0 = v0 > r0 ? v0 : r0, x1 = v1 < rb ? v1 : rb;
+          if (x1 > x0) ex_sr += outside_compute(x0, x1, lst, len, fin, tb, S, m);
         }
       }
     }
@@ -337,20 +351,18 @@ __global__ void __launch_bounds__(kCWarps * 32) contend_kernel(ContendArgs A) {
   }
   if (A.report && live) {
     int64_t* rep = A.report + o * 5 * (uint64_t)p;
-    rep[lane] = stuck ? 0 : Td;
-    rep[p + lane] = busy;
-    rep[2 * p + lane] = Md;
-    rep[3 * p + lane] = stuck ? 0 : commd + comm_in;
-    rep[4 * p + lane] = stuck ? 0 : exposed;
+    rep[d] = stuck ? 0 : Td;
+    rep[p + d] = busy;
+    rep[2 * p + d] = Md;
+    rep[3 * p + d] = stuck ? 0 : commd + comm_in;
+    rep[4 * p + d] = stuck ? 0 : exposed;
   }
-  const unsigned long long nt = warp_sum_i64((int64_t)ntask);
-  if (lane == 0) {
+  if (d == 0) {
     A.out_status[o] = status;
     A.out_makespan[o] = status == ADAPTIS_CAND_OK ? makespan : INT64_MAX;
     A.out_peak[o] = stuck ? 0 : peak_all;
     A.out_bubble[o] = status == ADAPTIS_CAND_OK
                           ? (float)(1.0 - (double)busy_all / ((double)p * (double)makespan)) : 0.0f;
-    atomicAdd(A.n_tasks, nt);
   }
 }
 
@@ -359,12 +371,21 @@ __global__ void __launch_bounds__(kCWarps * 32) contend_kernel(ContendArgs A) {
 int launch_contend(const int64_t* cols, const int64_t* comm, int L, int p, int m, int64_t cap, uint64_t n,
                    const adaptis_plan* plans, const adaptis_task* tasks, const uint64_t* offsets,
                    int64_t* scratch, uint64_t stride, int64_t* makespan, int64_t* peak, float* bubble,
-                   uint8_t* status, int64_t* report, unsigned long long* n_tasks, void* stream) {
+                   uint8_t* status, int64_t* report, unsigned long long* n_tasks, int Sm, void* stream) {
   if (n == 0) return 0;
   ContendArgs A{cols, comm, L, p, m, cap, n, plans, tasks, offsets, scratch, stride,
                 makespan, peak, bubble, status, report, n_tasks};
-  const unsigned grid = (unsigned)((n + kCWarps - 1) / kCWarps);
-  contend_kernel<<<grid, kCWarps * 32, 0, (cudaStream_t)stream>>>(A);
+  int p2 = 1;
+  while (p2 < p) p2 <<= 1;
+  const int G = 32 / p2;
+  const size_t smem = (size_t)kCWarps * G * tab_bytes(Sm);
+  const uint64_t warps = (n + G - 1) / G;
+  const unsigned grid = (unsigned)((warps + kCWarps - 1) / kCWarps);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(contend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  contend_kernel<<<grid, kCWarps * 32, smem, (cudaStream_t)stream>>>(A, p2, Sm);
   return (int)cudaGetLastError();
 }
 

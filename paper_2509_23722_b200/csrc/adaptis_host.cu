@@ -1621,7 +1621,7 @@ adaptis_status adaptis_eval_lists_contended(adaptis_ctx* ctx, adaptis_prepared* 
   CUC(cudaMemsetAsync(d_nt, 0, 8, ctx->stream));
   CUC(cudaEventRecord(ctx->ev0, ctx->stream));
   const int e = launch_contend(P->d_cols, P->d_comm, L, p, m, P->cap, n, d_plans, d_tasks, d_off, d_scr, stride,
-                               d_mk, d_pk, d_bub, d_st, d_rep, d_nt, ctx->stream);
+                               d_mk, d_pk, d_bub, d_st, d_rep, d_nt, Smax, ctx->stream);
   if (e) { cleanup(); return fail(ctx, ADAPTIS_ECUDA, "contention kernel: %s", cudaGetErrorString((cudaError_t)e)); }
   CUC(cudaEventRecord(ctx->ev1, ctx->stream));
   ctx->launches += 1;

@@ -138,11 +138,12 @@ int launch_comm_account(const TraceEntry* trace, const int* trace_n, int trace_c
 int launch_segment(const DevTables& t, const SegLaunch& s, int num_sms, void* stream,
                    bool fallback, unsigned grid_limit);
 // R34 engine contention on explicit lists (adaptis_contend.cu): one warp per
-// plan; scratch [n][stride] int64 with stride >= 5 * S * m. Returns a cudaError_t.
+// plan slot (32 / p2 plans per warp); scratch [n][stride] int64 with stride >=
+// 5 * S * m; Sm = the largest S of the batch. Returns a cudaError_t.
 int launch_contend(const int64_t* cols, const int64_t* comm, int L, int p, int m, int64_t cap, uint64_t n,
                    const adaptis_plan* plans, const adaptis_task* tasks, const uint64_t* offsets,
                    int64_t* scratch, uint64_t stride, int64_t* makespan, int64_t* peak, float* bubble,
-                   uint8_t* status, int64_t* report, unsigned long long* n_tasks, void* stream);
+                   uint8_t* status, int64_t* report, unsigned long long* n_tasks, int Sm, void* stream);
 int occupancy_ctas_per_sm(const SegLaunch& s, bool fallback);
 size_t smem_bytes(const SegLaunch& s, bool fallback);
 

@@ -110,8 +110,9 @@ def test_contended_wide_pipelines(ctx):
     prng = random.Random(99)
     for p, vs in ((16, (1, 2)), (32, (1,)), (8, (3, 4))):
         L = 4 * p + 3
-        pr = W.random_problem(rng, L, p, p, tmax=5, cmax=9, bytes_max=3)
-        prep = ctx.prepare(pr, W.Space([W.Group(1, W.FULL, combo_mask=0xF)]))
+        pr = W.random_problem(rng, L, p, p, tmax=3, cmax=40, bytes_max=3)
+        # any valid space: explicit plans only reuse the prepared tables
+        prep = ctx.prepare(pr, W.Space([W.Group(1, W.BALL, radius=1, combo_mask=0xF)]))
         items = []
         for v in vs:
             cuts = sorted(prng.sample(range(1, L), p * v - 1))
