@@ -307,6 +307,14 @@ def main():
                 "clocks": clk}
         line["roofline"] = roofline(seg_ms, seg_tasks, seg_n, args.config)
         line["generator"] = gen
+        # §8(f) f1 / R34: explicit cfg3-shaped schedules under send/receive-engine
+        # contention (adaptis_eval_lists_contended), latencies x100 so transfers queue
+        try:
+            sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+            import contend_bench
+            line["contention"] = contend_bench.run(n=8192, reps=3, comm_scale=100, ctx=ctx)
+        except Exception as e:  # reported, never silently replaced
+            line["contention"] = {"error": repr(e)}
         if not args.no_cpu_baseline and world == 1:
             info, _, _ = cpu_oracle_rate(pr, sp, args.cpu_seconds)
             line["cpu_baseline"] = info

@@ -21,15 +21,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_23722_b200 import adaptis as A, workloads as W  # noqa: E402
 
 
-def main():
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
-    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-    comm_scale = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+def run(n=32768, reps=5, comm_scale=1, ctx=None):
     pr, sp = W.config(3, cap=W.INT64_MAX)  # GPipe order keeps all m in flight
     pr.comm = pr.comm * comm_scale         # > 1: a slower link, so transfers queue
     p, m, v, L = pr.p, pr.m, 2, len(pr.t_f)
     S = p * v
-    ctx = A.Context(0)
+    ctx = ctx or A.Context(0)
     prep = ctx.prepare(pr, sp)
     rng = np.random.default_rng(3)
     plans = []
@@ -74,13 +71,20 @@ def main():
     wall.sort()
     ntask = n * len(flat)
     k = ms[len(ms) // 2]
-    print(json.dumps({
+    return {
         "tool": "contend_bench", "config": "cfg3 p=8 m=32 v=2 INTERLEAVED LIST", "comm_scale": comm_scale, "plans": n,
         "tasks_per_plan": len(flat), "kernel_ms": round(k, 3),
         "plans_per_s": round(n / (k / 1e3), 1), "tasks_per_s": round(ntask / (k / 1e3), 1),
         "call_wall_ms": round(wall[len(wall) // 2] * 1e3, 2),
         "ok": int((st_c == 0).sum()), "slowed_by_contention": int(((mk_c > mk_u) & (st_c == 0)).sum()),
-        "median_slowdown": float(np.median(mk_c[st_c == 0] / mk_u[st_c == 0])) if (st_c == 0).any() else None}))
+        "median_slowdown": float(np.median(mk_c[st_c == 0] / mk_u[st_c == 0])) if (st_c == 0).any() else None}
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    comm_scale = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+    print(json.dumps(run(n, reps, comm_scale)))
 
 
 if __name__ == "__main__":
