@@ -204,8 +204,12 @@ ADAPTIS_API void           adaptis_ctx_destroy(adaptis_ctx* ctx);
 ADAPTIS_API adaptis_status adaptis_ctx_set_allreduce(adaptis_ctx* ctx, adaptis_allreduce_min_fn fn, void* user);
 /* Exact lower-bound pruning for adaptis_search (default off; SURVEY §8d
  * "time-to-best-plan with and without LB pruning"): a candidate is skipped when
- * (LB << bits | index) exceeds the best key found so far, with LB = max_d
- * (forward time of the stages before device d's first stage + busy_d); since
+ * (LB << bits | index) exceeds the best key found so far, with LB = max_d of
+ * head_d + busy_d + tail_d. head_d = t_F of the stages before d's lowest
+ * stage (= d) plus the d edge latencies between them. Fused B/W: tail_d =
+ * (t_B + t_W) of those stages plus the same latencies. Split B/W: the max of
+ * head_d + busy_d and head_d + m (t_F + t_B)_d + t_B of those stages + the
+ * latencies + t_W of stage 0 (derivation in adaptis_seg.cuh). Since
  * makespan >= LB it cannot win, so the winner is unchanged. Skipped
  * candidates are counted in adaptis_best.n_pruned. Ignored in FP32 cost mode. */
 ADAPTIS_API adaptis_status adaptis_ctx_set_prune(adaptis_ctx* ctx, int enable);

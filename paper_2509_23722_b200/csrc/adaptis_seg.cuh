@@ -595,7 +595,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           }
           // ---- a2/a3 aggregation into task records
           T dmin = INF, cmin = INF;
-          BT busy = 0;
+          BT busy = 0, wsum = 0;  // wsum: t_W of the device's stages (prune bound)
           int64_t ac[V];
 #pragma unroll
           for (int c = 0; c < V; ++c) ac[c] = 0;
@@ -613,6 +613,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
               const int64_t sta = pre[kColStash * (L + 1) + b] - pre[kColStash * (L + 1) + a];
               stat += pre[kColWG * (L + 1) + b] - pre[kColWG * (L + 1) + a];
               busy += (BT)m * (cF + cB + cW);
+              wsum += cW;
               T oF = 0, oB = 0;
               if (s < S - 1 && dev_of(sl.placement, p, s + 1) != d) {
                 oF = lat(b - 1);
@@ -718,16 +719,40 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
               for (int k = 0; k < 2 * sl.ring_k; ++k) ring[(size_t)k * RS + g * S + s] = EMPTY;
           }
           __syncwarp();
-          // exact lower-bound prune (search only): device d starts no task before the
-          // forwards of every stage ahead of its first stage (s0 = its chunk 0) have
-          // run, and then executes busy_d sequentially, so makespan >= max_d
-          // (t_F[0, cuts[s0]) + busy_d); a candidate whose (LB << bits | index)
-          // exceeds the incumbent key cannot win
+          // exact lower-bound prune (search only). Device d's lowest stage is s0 = d
+          // (chunk 0 of every placement, R12). Head: d starts no task before F(0..d-1)
+          // of some micro-batch ran and travelled, t_F[0, cuts[d]) + the d edge
+          // latencies. Tail: every F and B of d ends by the end E of its last B at
+          // stage d (an F precedes its B; B(s', j) of a higher stage precedes B(d, j)),
+          // and after E that micro-batch's B still runs down stages d-1..0 with the
+          // same d latencies, then (split) its W at stage 0. So makespan >= max_d of
+          //   fused: head + busy_d + (t_B + t_W)[0, cuts[d]) + lat_d
+          //   split: max(head + busy_d, head + m (F + B)_d + t_B[0, cuts[d]) + lat_d
+          //              + t_W(stage 0)).
+          // A candidate whose (LB << bits | index) exceeds the incumbent key cannot win.
           if constexpr (!FP) {
             if (sl.prune) {
               const int s0 = stage_of(sl.placement, p, 0, d);
-              const int64_t startup = lane_on ? (int64_t)pre[kColTF * (L + 1) + cuts[s0]] : (int64_t)0;
-              const int64_t lb = seg_max(lane_on ? (int64_t)busy + startup : (int64_t)0, p2);
+              int64_t lk = (lane_on && s0 >= 1) ? (int64_t)lat(cuts[s0] - 1) : (int64_t)0;
+              for (int o = 1; o < p2; o <<= 1) {  // segmented inclusive scan: sum of edges 0..d
+                const int64_t y = __shfl_up_sync(FULLMASK, lk, o);
+                if (d >= o) lk += y;
+              }
+              int64_t lbd = 0;
+              if (lane_on) {
+                const int cs = cuts[s0];
+                const int64_t head = (int64_t)pre[kColTF * (L + 1) + cs] + lk;
+                const int64_t bpre = (int64_t)pre[kColTB * (L + 1) + cs];
+                lbd = (int64_t)busy + head;
+                if constexpr (BFUSED) {
+                  lbd += bpre + (int64_t)pre[kColTW * (L + 1) + cs] + lk;
+                } else {
+                  const int64_t w0 = (int64_t)pre[kColTW * (L + 1) + cuts[1]];
+                  const int64_t alt = (int64_t)busy - (int64_t)m * (int64_t)wsum + head + bpre + lk + w0;
+                  lbd = alt > lbd ? alt : lbd;
+                }
+              }
+              const int64_t lb = seg_max(lbd, p2);
               // one read of the incumbent per slot: lanes reading it separately could
               // straddle another warp's atomicMin and split the slot's prune decision
               unsigned long long inc = 0;

@@ -66,7 +66,7 @@ def test_cfg1_unit_exhaustive_and_golden(ctx):
     assert (b["index"], b["makespan"]) == (97, 218)
 
 
-def _random_spaces(seed, n):
+def _random_spaces(seed, n, cmax=5):
     rng = W.SplitMix64(seed)
     out = []
     for t in range(n):
@@ -75,7 +75,7 @@ def _random_spaces(seed, n):
         L = 2 * p + 1 + rng.next() % 6
         capsel = rng.next() % 3
         cap = W.INT64_MAX if capsel == 0 else 30 + rng.next() % 300
-        pr = W.random_problem(rng, L, p, m, tmax=9, cmax=5, bytes_max=9, cap=cap)
+        pr = W.random_problem(rng, L, p, m, tmax=9, cmax=cmax, bytes_max=9, cap=cap)
         groups = [W.Group(1, W.FULL, combo_mask=0xF)]
         if m % p == 0:
             groups.append(W.Group(2, W.BALL, 1 + rng.next() % 3, combo_mask=0x3F))
@@ -284,6 +284,27 @@ def test_pruned_search_same_winner(ctx):
     b = c.search(pr, sp)
     assert b["n_pruned"] > 0.5 * b["n_candidates"]  # the LB prune removes most of cfg2
     c.close()
+
+
+@pytest.mark.parametrize("seed,cmax", [(31, 5), (32, 40), (33, 200)])
+def test_pruned_search_same_winner_as_oracle(ctx, seed, cmax):
+    """The prune bound (head latencies + backward tail, see adaptis_seg.cuh) never
+    exceeds a makespan: pruned GPU search = the oracle's unpruned exhaustive
+    search, including latency-dominated tables where those terms are largest."""
+    from paper_2509_23722_b200 import adaptis as A
+    c = A.Context(0)
+    c.set_prune(True)
+    n_pruned = 0
+    for pr, sp in _random_spaces(seed, 10, cmax=cmax):
+        b = c.search(pr, sp)
+        ob = O.search(pr, sp, prune=False)
+        if ob["index"] == O.UINT64_MAX:
+            assert b["status"] != 0
+            continue
+        assert (b["index"], b["makespan"]) == (ob["index"], ob["makespan"])
+        n_pruned += b["n_pruned"]
+    c.close()
+    assert n_pruned > 0
 
 
 @pytest.mark.parametrize("cid", [3, 4, 5])
