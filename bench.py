@@ -132,6 +132,26 @@ def cpu_oracle_rate(pr, sp, seconds, seed=2025):
                       % (n, pr.name, valid, dt, nth, n1, dt1)}, n, dt
 
 
+def contention_cpu_rate(contend_bench, gpu, seconds=5.0):
+    """The R34 oracle (oracle/contention.py, pure Python, one core) on the first
+    plans of the same contention workload: plans/s, and its makespans must equal
+    the GPU's for those plans."""
+    from oracle.contention import simulate_lists_contended
+    pr, _sp, plans, per_dev = contend_bench.workload(64, gpu["comm_scale"])
+    t0 = time.perf_counter()
+    k = 0
+    ms = []
+    while k < len(plans) and (time.perf_counter() - t0 < seconds or k < 4):
+        pl = plans[k]
+        r = simulate_lists_contended(pr, pl["v"], pl["placement"], False, pl["cuts"][1:-1], per_dev)
+        ms.append(r["makespan"])
+        k += 1
+    dt = time.perf_counter() - t0
+    return {"value": k / dt, "unit": "plans/s", "cores": 1, "kind": "oracle",
+            "sample": "first %d plans of the same workload" % k,
+            "makespans_match_gpu": ms[:4] == gpu["makespans_first"][:4]}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -313,6 +333,8 @@ def main():
             sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
             import contend_bench
             line["contention"] = contend_bench.run(n=8192, reps=3, comm_scale=100, ctx=ctx)
+            if not args.no_cpu_baseline and world == 1:
+                line["contention"]["cpu_baseline"] = contention_cpu_rate(contend_bench, line["contention"])
         except Exception as e:  # reported, never silently replaced
             line["contention"] = {"error": repr(e)}
         if not args.no_cpu_baseline and world == 1:

@@ -21,19 +21,18 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_23722_b200 import adaptis as A, workloads as W  # noqa: E402
 
 
-def run(n=32768, reps=5, comm_scale=1, ctx=None):
+def workload(n, comm_scale=1):
+    """The problem, n plans (random cfg3 partitions, seed 3) and the per-device
+    lists they share."""
     pr, sp = W.config(3, cap=W.INT64_MAX)  # GPipe order keeps all m in flight
     pr.comm = pr.comm * comm_scale         # > 1: a slower link, so transfers queue
     p, m, v, L = pr.p, pr.m, 2, len(pr.t_f)
     S = p * v
-    ctx = ctx or A.Context(0)
-    prep = ctx.prepare(pr, sp)
     rng = np.random.default_rng(3)
     plans = []
     for _ in range(n):
         cuts = np.sort(rng.choice(np.arange(1, L), S - 1, replace=False)).tolist()
         plans.append({"v": v, "placement": 1, "policy": 4, "S": S, "cuts": [0] + cuts + [L]})
-    arr = A.make_plans(plans)
     per_dev = []
     for d in range(p):
         lst = [(0, d, j) for j in range(m)] + [(0, d + p, j) for j in range(m)]
@@ -41,6 +40,14 @@ def run(n=32768, reps=5, comm_scale=1, ctx=None):
             for j in range(m):
                 lst += [(1, s, j), (2, s, j)]
         per_dev.append(lst)
+    return pr, sp, plans, per_dev
+
+
+def run(n=32768, reps=5, comm_scale=1, ctx=None):
+    pr, sp, plans, per_dev = workload(n, comm_scale)
+    ctx = ctx or A.Context(0)
+    prep = ctx.prepare(pr, sp)
+    arr = A.make_plans(plans)
     flat = [t for lst in per_dev for t in lst]
     tasks = np.zeros(len(flat), dtype=[("kind", "<i2"), ("stage", "<i2"), ("mb", "<i4")])
     tasks["kind"] = [t[0] for t in flat]
@@ -72,7 +79,7 @@ def run(n=32768, reps=5, comm_scale=1, ctx=None):
     ntask = n * len(flat)
     k = ms[len(ms) // 2]
     return {
-        "tool": "contend_bench", "config": "cfg3 p=8 m=32 v=2 INTERLEAVED LIST", "comm_scale": comm_scale, "plans": n,
+        "tool": "contend_bench", "makespans_first": [int(x) for x in mk_c[:4]], "config": "cfg3 p=8 m=32 v=2 INTERLEAVED LIST", "comm_scale": comm_scale, "plans": n,
         "tasks_per_plan": len(flat), "kernel_ms": round(k, 3),
         "plans_per_s": round(n / (k / 1e3), 1), "tasks_per_s": round(ntask / (k / 1e3), 1),
         "call_wall_ms": round(wall[len(wall) // 2] * 1e3, 2),
