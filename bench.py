@@ -45,7 +45,24 @@ def parse():
     ap.add_argument("--impl", default="adaptis", choices=["adaptis", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cfg5-steps", type=int, default=1,
+                    help="timed steps of the cfg5 leg (the 8-GPU target config); 0 disables it")
     return ap.parse_args()
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a torchrun environment: re-launch this
+    script under torch.distributed.run with N ranks (one process per GPU, NCCL,
+    127.0.0.1 rendezvous); rank 0 prints the JSON line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=%d" % args.gpus, "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ------------------------------------------------------------------ clocks
@@ -188,6 +205,10 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if world != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -242,10 +263,15 @@ def main():
     launches = ctx.launch_count - launches0
     tot = torch.tensor([sum(step_ms), sum(kern_ms)], dtype=torch.float64, device="cuda:%d" % local)
     inv = torch.tensor([n_invalid], dtype=torch.int64, device="cuda:%d" % local)
+    per_rank = tot.clone().reshape(1, 2)
     if world > 1:
+        per_rank = torch.zeros(world, 2, dtype=torch.float64, device="cuda:%d" % local)
+        dist.all_gather_into_tensor(per_rank, tot.reshape(1, 2))
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
         dist.all_reduce(inv, op=dist.ReduceOp.SUM)
     total_ms, total_kern_ms = float(tot[0]), float(tot[1])
+    # per-rank device time of the timed steps (shard balance, §8e)
+    rank_ms = [float(x) / args.steps for x in per_rank[:, 1].tolist()]
     valid = N - int(inv.item())
 
     # ---- time-to-best-plan with the exact lower-bound prune (same winner; the
@@ -253,6 +279,7 @@ def main():
     ctx.set_prune(True)
     prep.search()
     pr_ms = []
+    bp = None
     for _ in range(max(1, min(args.steps, 3))):
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -283,6 +310,62 @@ def main():
     e2e_ms_step = float(e2.item())
     h2d = 8 * (6 * pr.L + pr.L) + 8 * 160 * 65 + 8 * 4 * 64 * 257 + 2 * 4 * 64 + 8 * (2 + 4 * 16)
     d2h = 8 * (2 + 2 * 16) + 8 + 8 + 4 + 1 + 8 * 3 * pr.p
+
+    # ---- cfg5 leg: the config BASELINE quotes the 8-GPU target on (949.9 M
+    # candidates, p = 16, v <= 4, m = 128); same step definition, device-timed,
+    # max over ranks, one warm-up step (a step is tens of seconds on one GPU)
+    cfg5 = None
+    if args.config != 5 and args.cfg5_steps > 0:
+        pr5, sp5 = W.config(5)
+        prep5 = ctx.prepare(pr5, sp5)
+        b5 = prep5.search()  # warm-up
+        ms5, k5 = [], []
+        for _ in range(args.cfg5_steps):
+            flush.random_(0, 255)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            b5 = prep5.search()
+            e1.record(stream)
+            e1.synchronize()
+            ms5.append(e0.elapsed_time(e1))
+            k5.append(b5["kernel_ms"])
+        t5 = torch.tensor([sum(ms5) / len(ms5), sum(k5) / len(k5)], dtype=torch.float64,
+                          device="cuda:%d" % local)
+        pr5_rank = t5.clone().reshape(1, 2)
+        i5 = torch.tensor([b5["n_invalid"]], dtype=torch.int64, device="cuda:%d" % local)
+        if world > 1:
+            pr5_rank = torch.zeros(world, 2, dtype=torch.float64, device="cuda:%d" % local)
+            dist.all_gather_into_tensor(pr5_rank, t5.reshape(1, 2))
+            dist.all_reduce(t5, op=dist.ReduceOp.MAX)
+            dist.all_reduce(i5, op=dist.ReduceOp.SUM)
+        ctx.set_prune(True)
+        prep5.search()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        bp5 = prep5.search()
+        e1.record(stream)
+        e1.synchronize()
+        ctx.set_prune(False)
+        tp5 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda:%d" % local)
+        if world > 1:
+            dist.all_reduce(tp5, op=dist.ReduceOp.MAX)
+        valid5 = prep5.N - int(i5.item())
+        ms_step5 = float(t5[0])
+        g5 = _golden(5)
+        cfg5 = {"workload": CONFIG_NAMES[5], "steps": args.cfg5_steps, "warmup": 1,
+                "candidates": prep5.N, "valid_candidates": valid5,
+                "value": valid5 / (ms_step5 / 1000.0), "unit": UNIT, "ms_per_step": ms_step5,
+                "time_to_best_plan_pruned_ms": float(tp5.item()),
+                "per_rank_kernel_ms": [float(x) for x in pr5_rank[:, 1].tolist()],
+                "best": {"index": b5["index"], "makespan_ticks": b5["makespan"], "plan": b5["plan"]},
+                "same_winner_pruned": bp5["index"] == b5["index"],
+                "matches_oracle_golden": None if g5 is None else
+                (b5["index"], b5["makespan"]) == (g5["index"], g5["makespan"])}
+        prep5.close()
 
     # ---- the paper's own search (Pipeline Generator, R28) on this GPU:
     # seeds + phase-by-phase tuning, every neighbourhood evaluated by the kernels
@@ -324,8 +407,14 @@ def main():
                         "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches,
                 "kernel_ms_per_step": total_kern_ms / args.steps,
+                "per_rank_kernel_ms": rank_ms,
+                "rank_imbalance": (max(rank_ms) / (sum(rank_ms) / len(rank_ms)) - 1.0) if rank_ms else 0.0,
                 "clocks": clk}
         line["roofline"] = roofline(seg_ms, seg_tasks, seg_n, args.config)
+        g = _golden(args.config)
+        line["best"]["matches_oracle_golden"] = None if g is None else \
+            (best["index"], best["makespan"]) == (g["index"], g["makespan"])
+        line["cfg5"] = cfg5
         line["generator"] = gen
         # §8(f) f1 / R34: explicit cfg3-shaped schedules under send/receive-engine
         # contention (adaptis_eval_lists_contended), latencies x100 so transfers queue
@@ -344,6 +433,16 @@ def main():
     if world > 1:
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()
+
+
+def _golden(cid):
+    """The oracle's exhaustive argmin of a config (tests/golden/argmin_cfgN.json,
+    written by tools/oracle_argmin.py from oracle/ only), or None."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "argmin_cfg%d.json" % cid)) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def _int64(pr):

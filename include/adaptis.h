@@ -298,9 +298,11 @@ ADAPTIS_API adaptis_status adaptis_eval_indices(adaptis_ctx* ctx, adaptis_prepar
  * device d executes tasks[offsets[i*(p+1)+d] .. offsets[i*(p+1)+d+1]) in order:
  * every (F, B[, W]) x own stage x micro-batch exactly once, with F(s,j) before
  * B(s,j) before W(s,j) on the device (else EINVAL naming plan, device and
- * task). Cross-device waits follow the DAG; a cyclic wait gives status
+ * task). The offsets array (n*(p+1) entries) must be non-decreasing over its
+ * whole length, plan after plan (else EINVAL): tasks[0 .. offsets[n*(p+1)-1])
+ * is read. Cross-device waits follow the DAG; a cyclic wait gives status
  * STUCK, a peak above the cap OVER_CAP (split precedence, R26). Outputs as
- * adaptis_eval_plans (report [n][5][p] optional). Not in FP32 cost mode. */
+ * adaptis_eval_plans (report [n][7][p] optional). Not in FP32 cost mode. */
 ADAPTIS_API adaptis_status adaptis_eval_lists(adaptis_ctx* ctx, adaptis_prepared* prep,
                                               const adaptis_plan* plans, const adaptis_task* tasks,
                                               const uint64_t* offsets, uint64_t n,
@@ -314,8 +316,8 @@ ADAPTIS_API adaptis_status adaptis_eval_lists(adaptis_ctx* ctx, adaptis_prepared
  * receiver's receive engine together for its latency; each engine serves
  * transfers FIFO by (eligible time, mb, stage, F before B). Memory and the
  * stuck / over-cap status are those of the lists (R16, R26, R30). `report`
- * rows 3-4 (comm_d, exposed_d) use the transfers' actual [start, arrival)
- * intervals. EOVERFLOW if the serial bound (m x all task ticks + 2m x all
+ * rows 3-6 (comm_d, exposed_d, overlap_d, bubble_d) use the transfers' actual
+ * [start, arrival) intervals. EOVERFLOW if the serial bound (m x all task ticks + 2m x all
  * latencies) reaches 2^40 ticks; EINVAL if the per-plan scratch
  * (n x 5 x max S x m x 8 B) exceeds 2 GiB. Not in FP32 cost mode. */
 ADAPTIS_API adaptis_status adaptis_eval_lists_contended(adaptis_ctx* ctx, adaptis_prepared* prep,
@@ -368,9 +370,11 @@ ADAPTIS_API adaptis_status adaptis_tune_overlap(adaptis_ctx* ctx, adaptis_prepar
  * GPIPE and GREEDY); else EINVAL naming the plan. cuts[0] and cuts[S] are taken
  * as 0 and L; cuts that are not strictly increasing give status 1 (INVALID).
  * Results go to host arrays `out` (n entries each) in plan order; `report`,
- * when non-NULL, is a host array [n][5][p] receiving T_d, busy_d, M_d, comm_d
- * and exposed_d (R29, see adaptis_best) of every plan with status 0 or 2
- * (untouched otherwise); its trace scratch (n * p * 3mv * 24 B) must stay
+ * when non-NULL, is a host array [n][7][p] receiving T_d, busy_d, M_d, comm_d,
+ * exposed_d, overlap_d and bubble_d (R29, see adaptis_best: overlap_d =
+ * comm_d - exposed_d is Alg. 1's OverlapTime(d), bubble_d = T_d - busy_d -
+ * exposed_d its BubbleTime(d)) of every plan with status 0 or 2 (untouched
+ * otherwise); its trace scratch (n * p * 3mv * 24 B) must stay
  * under 2 GiB (EINVAL). Not in FP32 cost mode (EINVAL). The context's GPU
  * evaluates the whole list. */
 ADAPTIS_API adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared* prep,

@@ -115,6 +115,7 @@ static double rows_sum_f(const double* col, int a, int b) {
 #define OMIN min64
 #define ORND(x) (x)
 #define ORC_F64 0
+#define ORC_F32 0
 #define COMM(row) (pr->comm[(row)])
 #include "oracle_sim.inc"
 #undef OT
@@ -142,7 +143,32 @@ static double rows_sum_f(const double* col, int a, int b) {
 #undef OMAX
 #undef OMIN
 #undef ORND
+#undef ORC_F32
+#undef COMM
+
+/* the fp32-cost variant in fp32 time arithmetic (reading R27): the same event
+ * loop with every time value (finish, arrival, decision time) an fp32 number
+ * produced by IEEE round-to-nearest additions, so that every scheduling
+ * decision is taken in the precision the kernel takes it in */
+static float fmaxf_(float a, float b) { return a > b ? a : b; }
+static float fminf_(float a, float b) { return a < b ? a : b; }
+#define OT float
+#define OSUF(x) x##_f32
+#define OTMAX HUGE_VALF
+#define OMAX fmaxf_
+#define OMIN fminf_
+#define ORND(x) llroundf(x)
+#define ORC_F32 1
+#define COMM(row) ((float)pr->costs_f64[3 * (size_t)pr->L + (row)])
+#include "oracle_sim.inc"
+#undef OT
+#undef OSUF
+#undef OTMAX
+#undef OMAX
+#undef OMIN
+#undef ORND
 #undef ORC_F64
+#undef ORC_F32
 #undef COMM
 
 /* ------------------------------------------------------------------------ */
@@ -460,7 +486,9 @@ static void* ev_worker(void* a_) {
   for (uint64_t i = a->tid; i < a->n; i += a->nth) {
     orc_plan pl; orc_result r;
     if (orc_decode(a->pr, a->sp, a->idx[i], &pl) != 0) { a->err = 1; continue; }
-    int rc = a->pr->costs_f64 ? orc_simulate_f64(a->pr, &pl, &r, NULL) : orc_simulate(a->pr, &pl, &r, NULL);
+    int rc = !a->pr->costs_f64 ? orc_simulate(a->pr, &pl, &r, NULL)
+             : a->pr->time_f32 ? orc_simulate_f32(a->pr, &pl, &r, NULL)
+                               : orc_simulate_f64(a->pr, &pl, &r, NULL);
     if (rc != 0) a->err = 1;
     if (a->msf) a->msf[i] = r.status == ORC_OK ? r.makespan_f : HUGE_VAL;
     if (a->ms) a->ms[i] = r.makespan;

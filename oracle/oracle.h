@@ -47,6 +47,8 @@ typedef struct {
   int64_t cap;                              /* M_d^capacity (Eq. 2)                       */
   const double* costs_f64;                  /* optional [4][L] real t_f, t_b, t_w, comm:
                                                selects the fp64 simulator                 */
+  int time_f32;                             /* with costs_f64: time arithmetic in fp32
+                                               (the fp32-cost variant, R27)               */
 } orc_problem;
 
 typedef struct {
@@ -100,6 +102,8 @@ int  orc_fixed_order(const orc_problem* pr, const orc_plan* pl, int d,
 int  orc_simulate(const orc_problem* pr, const orc_plan* pl, orc_result* out, orc_trace* tr);
 /* the same event loop with real-valued times (fp64) on pr->costs_f64 */
 int  orc_simulate_f64(const orc_problem* pr, const orc_plan* pl, orc_result* out, orc_trace* tr);
+/* the same event loop with fp32 times on pr->costs_f64 (values exact in fp32) */
+int  orc_simulate_f32(const orc_problem* pr, const orc_plan* pl, orc_result* out, orc_trace* tr);
 /* Independent checker: longest path over the task DAG (S:141 edges) plus the
  * given per-device list-order edges, by relaxation to a fixpoint. Returns 0,
  * or 1 if the lists contain a cyclic wait. fused: B charged c_B + c_W, no W. */

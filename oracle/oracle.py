@@ -42,7 +42,7 @@ class _Problem(C.Structure):
     _fields_ = [("L", C.c_int)] + [(n, C.POINTER(C.c_int64)) for n in
                                    ("t_f", "t_b", "t_w", "act", "stash", "weight", "grad", "comm")] + \
                [("p", C.c_int), ("m", C.c_int), ("cap", C.c_int64),
-                ("costs_f64", C.POINTER(C.c_double))]
+                ("costs_f64", C.POINTER(C.c_double)), ("time_f32", C.c_int)]
 
 
 class _Plan(C.Structure):
@@ -110,6 +110,7 @@ def lib():
                                            C.POINTER(C.c_double), C.POINTER(C.c_uint8),
                                            C.POINTER(C.c_double)]
             L.orc_simulate_f64.argtypes = L.orc_simulate.argtypes
+            L.orc_simulate_f32.argtypes = L.orc_simulate.argtypes
             L.orc_search.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.c_int, C.c_int,
                                      C.POINTER(_Best)]
             _lib = L
@@ -123,7 +124,7 @@ def _i64p(a):
 class _Ctx:
     """Keeps numpy arrays alive while C structs point into them."""
 
-    def __init__(self, pr, sp=None):
+    def __init__(self, pr, sp=None, precision="f64"):
         self.keep = []
         cols = {}
         for n in ("t_f", "t_b", "t_w", "act", "stash", "weight", "grad", "comm"):
@@ -136,7 +137,12 @@ class _Ctx:
             a = np.ascontiguousarray(np.asarray(pr.costs_f32, dtype=np.float64))
             self.keep.append(a)
             cf = a.ctypes.data_as(C.POINTER(C.c_double))
-        self.pr = _Problem(L=len(pr.t_f), p=pr.p, m=pr.m, cap=int(pr.cap), costs_f64=cf, **cols)
+        if precision not in ("f64", "f32"):
+            raise ValueError(precision)
+        # fp32-cost variant: "f64" = real-arithmetic reference, "f32" = every time
+        # value and decision in fp32, as the kernel computes them (reading R27)
+        self.pr = _Problem(L=len(pr.t_f), p=pr.p, m=pr.m, cap=int(pr.cap), costs_f64=cf,
+                           time_f32=int(precision == "f32"), **cols)
         self.sp = None
         if sp is not None:
             s = _Space()
@@ -168,9 +174,9 @@ def plan_dict(pl):
             "cuts": [pl.cuts[i] for i in range(pl.S + 1)]}
 
 
-def simulate(pr, v, placement, policy, cuts, trace=False):
+def simulate(pr, v, placement, policy, cuts, trace=False, precision="f64"):
     """Alg. 1 for one candidate. cuts = interior cuts. Returns a dict."""
-    ctx = _Ctx(pr)
+    ctx = _Ctx(pr, precision=precision)
     pl = make_plan(v, placement, policy, cuts, L=len(pr.t_f))
     res = _Result()
     tr_p = None
@@ -181,7 +187,8 @@ def simulate(pr, v, placement, policy, cuts, trace=False):
                     stage=arrs[1].ctypes.data_as(C.POINTER(C.c_int)),
                     mb=arrs[2].ctypes.data_as(C.POINTER(C.c_int)), start=_i64p(arrs[3]))
         tr_p = C.pointer(tr)
-    sim = lib().orc_simulate_f64 if ctx.pr.costs_f64 else lib().orc_simulate
+    sim = (lib().orc_simulate if not ctx.pr.costs_f64 else
+           lib().orc_simulate_f32 if ctx.pr.time_f32 else lib().orc_simulate_f64)
     rc = sim(C.byref(ctx.pr), C.byref(pl), C.byref(res), tr_p)
     if rc != 0:
         raise RuntimeError("oracle internal inconsistency")
@@ -286,8 +293,8 @@ def decode(pr, sp, index):
     return plan_dict(pl)
 
 
-def eval_indices(pr, sp, indices, nthreads=None):
-    ctx = _Ctx(pr, sp)
+def eval_indices(pr, sp, indices, nthreads=None, precision="f64"):
+    ctx = _Ctx(pr, sp, precision=precision)
     idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
     n = idx.shape[0]
     ms = np.zeros(n, np.int64); pk = np.zeros(n, np.int64)

@@ -482,15 +482,12 @@ class Prepared:
         arr = make_plans(plans)
         out = _host_results(n)
         soa = _soa_from_numpy(out)
-        rep = np.zeros((max(n, 1), 5, self.m.problem.p), np.int64) if report else None
+        rep = np.zeros((max(n, 1), REPORT_ROWS, self.m.problem.p), np.int64) if report else None
         _check(lib().adaptis_eval_plans(self.ctx.ptr, self.ptr, arr, n, C.byref(soa),
                                         rep.ctypes.data_as(C.POINTER(C.c_int64)) if report else None),
                self.ctx.ptr)
         if report:
-            out["T_d"], out["busy_d"], out["M_d"] = rep[:n, 0], rep[:n, 1], rep[:n, 2]
-            out["comm_d"], out["exposed_d"] = rep[:n, 3], rep[:n, 4]
-            out["overlap_d"] = out["comm_d"] - out["exposed_d"]
-            out["bubble_d"] = out["T_d"] - out["busy_d"] - out["exposed_d"]
+            _unpack_report(out, rep, n)
         return out
 
     def eval_lists_contended(self, plans, lists, report: bool = False) -> dict:
@@ -517,15 +514,14 @@ class Prepared:
             offs[i * (p + 1) + p] = pos
         out = _host_results(n)
         soa = _soa_from_numpy(out)
-        rep = np.zeros((max(n, 1), 5, p), np.int64) if report else None
+        rep = np.zeros((max(n, 1), REPORT_ROWS, p), np.int64) if report else None
         fn = lib().adaptis_eval_lists_contended if _contended else lib().adaptis_eval_lists
         _check(fn(self.ctx.ptr, self.ptr, arr, tasks.ctypes.data,
                                         offs.ctypes.data_as(C.POINTER(C.c_uint64)), n, C.byref(soa),
                                         rep.ctypes.data_as(C.POINTER(C.c_int64)) if report else None),
                self.ctx.ptr)
         if report:
-            out["T_d"], out["busy_d"], out["M_d"] = rep[:n, 0], rep[:n, 1], rep[:n, 2]
-            out["comm_d"], out["exposed_d"] = rep[:n, 3], rep[:n, 4]
+            _unpack_report(out, rep, n)
         return out
 
     @staticmethod
@@ -599,6 +595,15 @@ class Prepared:
         _check(lib().adaptis_eval_prepared(self.ctx.ptr, self.ptr, first, count, C.byref(soa), 0),
                self.ctx.ptr)
         return out
+
+
+REPORT_ROWS = 7  # adaptis.h per-plan report rows
+REPORT_KEYS = ("T_d", "busy_d", "M_d", "comm_d", "exposed_d", "overlap_d", "bubble_d")
+
+
+def _unpack_report(out, rep, n):
+    for r, k in enumerate(REPORT_KEYS):
+        out[k] = rep[:n, r]
 
 
 def _host_results(count):

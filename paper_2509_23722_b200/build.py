@@ -23,11 +23,25 @@ def _inputs():
             [os.path.join(root, "include", "adaptis.h"), __file__])
 
 
+FLAG_VARS = ("ADAPTIS_GREEDY_MINB", "ADAPTIS_GREEDY_V4_MINB", "ADAPTIS_FIXED_V4_MINB", "ADAPTIS_GREEDY_COMMITS",
+             "ADAPTIS_DEBUG", "ADAPTIS_KRUN", "ADAPTIS_GREEDY_ALWAYS_DECIDE", "ADAPTIS_TSTAR_REDUX")
+STAMP = LIB + ".flags"  # the -D flags the library was built with
+
+
+def _extra_flags():
+    return ["-D%s=%s" % (k, os.environ[k]) for k in FLAG_VARS if os.environ.get(k)]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    stale = not os.path.exists(LIB) or max(os.path.getmtime(f) for f in _inputs()) > os.path.getmtime(LIB)
+    extra = _extra_flags()
+    stamp = " ".join(extra)
+    old_stamp = open(STAMP).read() if os.path.exists(STAMP) else ""
+    # stale when a source is newer than the library or the -D flags changed
+    # (an A/B experiment must never measure the same binary twice)
+    stale = (not os.path.exists(LIB) or max(os.path.getmtime(f) for f in _inputs()) > os.path.getmtime(LIB)
+             or (os.path.exists(STAMP) or extra) and old_stamp != stamp)
     if not (force or stale):
         return LIB
-    extra = ["-D%s=%s" % (k, os.environ[k]) for k in ("ADAPTIS_GREEDY_MINB", "ADAPTIS_GREEDY_V4_MINB", "ADAPTIS_FIXED_V4_MINB", "ADAPTIS_GREEDY_COMMITS", "ADAPTIS_DEBUG", "ADAPTIS_KRUN", "ADAPTIS_GREEDY_ALWAYS_DECIDE", "ADAPTIS_TSTAR_REDUX") if os.environ.get(k)]
     inc = ["-I", os.path.join(os.path.dirname(HERE), "include")]
     objdir = os.path.join(CSRC, "obj")
     os.makedirs(objdir, exist_ok=True)
@@ -54,6 +68,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(log_text[-8000:])
         raise RuntimeError("nvcc failed building libadaptis.so (see %s)" % log)
     os.replace(LIB + ".tmp", LIB)
+    with open(STAMP, "w") as f:
+        f.write(stamp)
     if verbose:
         print(log_text[-4000:])
     return LIB

@@ -84,7 +84,7 @@ struct adaptis_ctx {
   uint64_t fallback_cands = 0;
   int prune = 0;
   uint64_t counters[3] = {0, 0, 0};
-  uint64_t last_tasks = 0;
+  uint64_t last_tasks = 0, last_invalid = 0, last_pruned = 0;  // counts of the last run_jobs
   std::vector<cudaEvent_t> seg_events;
   std::vector<adaptis_launch_info> last_info;
   // scratch
@@ -470,10 +470,14 @@ struct Job {
   adaptis_launch_info info;
 };
 
-// Scratch words: [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds
-// [5] pruned, then per job i at kHdr + kSegWords*i: [0] cursor [1] overflow
-// count [2] tasks [3] fallback cursor [4] fallback overflow count.
-constexpr size_t kSegWords = 6;
+// Scratch words: [0] key [1] (unused) [2] (unused) [3] rounds [4] live
+// lane-rounds [5] (unused), then per job i at kHdr + kSegWords*i: [0] cursor
+// [1] overflow count [2] tasks [3] fallback cursor [4] fallback overflow count
+// [5] invalid [6] pruned [7] fallback invalid [8] fallback pruned
+// [9] fallback tasks. Counts are kept per job and per pass so that a fallback
+// that re-runs a whole shard replaces that job's first-pass counts instead of
+// adding to them (every candidate is counted once: invalid, pruned or simulated).
+constexpr size_t kSegWords = 10;
 
 // Launch every job on this context's stream; candidates whose fast-path rings
 // filled up are re-run by the fallback kernel (exact, rings >= m).
@@ -524,10 +528,10 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
     s.overflow_count = reinterpret_cast<unsigned int*>(sw + 1);
     s.overflow_idx = ctx->d_overflow + kOverflowPerSeg * i;
     s.overflow_cap = (unsigned)kOverflowPerSeg;
-    s.n_invalid = W + 1;
+    s.n_invalid = sw + 5;
     s.n_tasks = sw + 2;
     s.n_rounds = W + 3;
-    s.n_pruned = W + 5;
+    s.n_pruned = sw + 6;
     s.prune = (mode_search && ctx->prune && P->tick != kTickF32) ? 1 : 0;
     // GREEDY rings hold all m items (its F-first rule can run m items ahead);
     // they live in global memory when they do not fit the shared-memory budget
@@ -584,6 +588,9 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
     s.cursor = sw + 3;
     s.overflow_count = reinterpret_cast<unsigned int*>(sw + 4);
     s.overflow_cap = 0;
+    s.n_invalid = sw + 7;
+    s.n_pruned = sw + 8;
+    s.n_tasks = sw + 9;
     unsigned grid_limit = 0;
     st = ensure_gring(ctx, P, s, &grid_limit);
     if (st != ADAPTIS_OK) return st;
@@ -602,14 +609,21 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
   ctx->counters[1] += words[3];
   ctx->counters[2] += words[4];
   ctx->last_info.clear();
-  uint64_t tasks = 0;
+  uint64_t tasks = 0, invalid = 0, pruned = 0;
   for (size_t i = 0; i < nseg; ++i) {
     if (!active[i]) continue;
     float fb = 0.0f;
     if (active[i] == 2) CU(ctx, cudaEventElapsedTime(&fb, ctx->seg_events[2 * i], ctx->seg_events[2 * i + 1]));
+    const unsigned long long* jw = words.data() + kHdr + kSegWords * i;
+    // a whole-shard fallback re-counted every candidate of the job: its counts
+    // replace the first pass's; a list fallback only saw the overflowed ones
+    const bool whole = active[i] == 2 && (jw[1] & 0xffffffffu) > kOverflowPerSeg;
+    const uint64_t jt = whole ? jw[9] : jw[2] + jw[9];
+    invalid += whole ? jw[7] : jw[5] + jw[7];
+    pruned += whole ? jw[8] : jw[6] + jw[8];
     adaptis_launch_info li = jobs[i].info;
     li.candidates = jobs[i].s.n_pos;
-    li.tasks = words[kHdr + kSegWords * i + 2];
+    li.tasks = jt;
     li.ms = seg_ms[i] + fb;
     li.fallback = active[i] == 2 ? (int32_t)(words[kHdr + kSegWords * i + 1] & 0xffffffffu) : 0;
     tasks += li.tasks;
@@ -617,6 +631,8 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
   }
   ctx->counters[0] += tasks;
   ctx->last_tasks = tasks;
+  ctx->last_invalid = invalid;
+  ctx->last_pruned = pruned;
   return ADAPTIS_OK;
 }
 
@@ -673,6 +689,20 @@ int host_dev_of(int placement, int p, int s) {  // R12
 }
 
 // R30: every (kind, own stage, mb) exactly once per device, F < B < W per (stage, mb)
+// The public per-plan report (adaptis.h): the kernels' five rows T_d, busy_d,
+// M_d, comm_d, exposed_d, completed by R29's derived terms OverlapTime(d) =
+// comm_d - exposed_d and BubbleTime(d) = T_d - busy_d - exposed_d (Alg. 1
+// Step 3), so that T_d = busy_d + comm_d + bubble_d - overlap_d.
+constexpr int kReportRows = 7;
+void expand_report(const int64_t* rep5, int64_t* out7, int p) {
+  for (int r = 0; r < 5; ++r)
+    for (int d = 0; d < p; ++d) out7[r * p + d] = rep5[r * p + d];
+  for (int d = 0; d < p; ++d) {
+    out7[5 * p + d] = rep5[3 * p + d] - rep5[4 * p + d];
+    out7[6 * p + d] = rep5[d] - rep5[p + d] - rep5[4 * p + d];
+  }
+}
+
 adaptis_status validate_lists(adaptis_ctx* ctx, const adaptis_prepared* P, const adaptis_plan* plans,
                               const adaptis_task* tasks, const uint64_t* offsets, uint64_t n) {
   const int p = P->p, m = P->m;
@@ -682,6 +712,11 @@ adaptis_status validate_lists(adaptis_ctx* ctx, const adaptis_prepared* P, const
     const int nk = fused ? 2 : 3, S = pl.S;
     std::vector<int64_t> pos((size_t)nk * S * m, -1);
     const uint64_t* off = offsets + i * (uint64_t)(p + 1);
+    // the whole offsets array is non-decreasing (plan after plan), so its last
+    // entry bounds every task range: the device copy is sized by it
+    if (i > 0 && off[0] < off[-1])
+      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: offsets start before the end of plans[%llu]",
+                  (unsigned long long)i, (unsigned long long)(i - 1));
     for (int d = 0; d < p; ++d) {
       if (off[d + 1] < off[d])
         return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: offsets of device %d decrease", (unsigned long long)i, d);
@@ -1083,9 +1118,9 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   unsigned long long words[6] = {0, 0, 0, 0, 0, 0};
   CU(ctx, cudaMemcpyAsync(words, ctx->d_scratch, 48, cudaMemcpyDeviceToHost, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
-  out->n_invalid = words[1];
+  out->n_invalid = ctx->last_invalid;
   out->n_tasks = ctx->last_tasks;
-  out->n_pruned = words[5];
+  out->n_pruned = ctx->last_pruned;
   const std::vector<adaptis_launch_info> search_info = ctx->last_info;
   out->kernel_ms = ms;
   out->n_candidates = P->N;
@@ -1515,7 +1550,7 @@ static adaptis_status eval_plans_common(adaptis_ctx* ctx, adaptis_prepared* P, c
   if (report)
     for (uint64_t i = 0; i < n; ++i)
       if (stt[i] == ADAPTIS_CAND_OK || stt[i] == ADAPTIS_CAND_OVER_CAP)
-        memcpy(report + (size_t)i * 5 * P->p, rep.data() + (size_t)i * 5 * P->p, (size_t)5 * P->p * 8);
+        expand_report(rep.data() + (size_t)i * 5 * P->p, report + (size_t)i * kReportRows * P->p, P->p);
   return ADAPTIS_OK;
 }
 
@@ -1657,7 +1692,7 @@ adaptis_status adaptis_eval_lists_contended(adaptis_ctx* ctx, adaptis_prepared* 
   if (report)
     for (uint64_t i = 0; i < n; ++i)
       if (stt[i] == ADAPTIS_CAND_OK || stt[i] == ADAPTIS_CAND_OVER_CAP)
-        memcpy(report + (size_t)i * 5 * p, rep.data() + (size_t)i * 5 * p, (size_t)5 * p * 8);
+        expand_report(rep.data() + (size_t)i * 5 * p, report + (size_t)i * kReportRows * p, p);
   return ADAPTIS_OK;
 }
 

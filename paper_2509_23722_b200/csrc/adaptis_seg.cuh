@@ -88,6 +88,16 @@ struct GAux {      // GREEDY statics of one (lane, chunk); stored as SoA, this f
   int32_t tF, tB;  // consumer (lane << 3 | chunk) of the F / B output, -1: none
   T pF, pB;        // cost of the cross-device predecessor of an unknown F / B head
 };
+// fp32 ticks (R27): the predecessor's duration and its latency are kept apart so
+// that a bound is rounded exactly like the arrival it bounds, fl(fl(t + dur) + lat)
+// (monotone in t), never above it
+template <>
+struct GAux<float> {
+  int64_t gate;
+  int32_t tF, tB;
+  float pF, pB;    // predecessor duration
+  float lF, lB;    // predecessor edge latency
+};
 
 // per-lane state touched only at candidate setup / finalize and at kernel exit,
 // kept in shared memory so that the round loop keeps its registers (48 bytes)
@@ -334,6 +344,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   int32_t* ga_tB = ga_tF + V * 32;
   T* ga_pF = reinterpret_cast<T*>(ga_tB + V * 32);
   T* ga_pB = ga_pF + V * 32;
+  T* ga_lF = ga_pB + V * 32;  // fp32 ticks only (GAux<float>)
+  T* ga_lB = ga_lF + V * 32;
   LaneCold& cold = reinterpret_cast<LaneCold*>(wbase + lay.cold_off)[threadIdx.x & 31];
   cold.idx = 0; cold.slot = 0; cold.busy = 0; cold.key = ~0ull >> 1; cold.invalid = 0; cold.tasks = 0; cold.live = 0;
   cold.pruned = 0;
@@ -370,6 +382,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   T free_t = 0;
   int64_t dyn = 0, peak = 0, stat = 0;
   T window = INF;
+  T w_dm = INF, w_cm = INF;  // fp32 ticks: the window's two terms, added in arrival order
   // fixed orders
   int nF = 0, nB = 0, nW = 0;
   VPos fp, bp, wp;
@@ -435,7 +448,6 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
 
   // collective: write results of the slots with `fl` set (all lanes execute)
   auto finalize = [&](bool fl) {
-    if (fl) { cold.tasks += ctasks; cold.live += clive; ctasks = 0; clive = 0; }
     BT busy;
     if constexpr (FP) busy = __longlong_as_double(cold.busy); else busy = cold.busy;
     const uint64_t idx = cold.idx;
@@ -454,6 +466,9 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
     else if (flags & F_STUCK) status = ADAPTIS_CAND_STUCK;
     else if (anyover) status = ADAPTIS_CAND_OVER_CAP;
     else status = ADAPTIS_CAND_OK;
+    // a candidate whose rings overflowed is re-run by the fallback: its partial
+    // tasks are not counted (each candidate's tasks are counted once)
+    if (fl) { if (status != -2) cold.tasks += ctasks; cold.live += clive; ctasks = 0; clive = 0; }
     if (fl && d == 0) {
       if (status == -2) {
         const unsigned k = atomicAdd(sl.overflow_count, 1u);
@@ -650,17 +665,23 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
               if constexpr (GREEDY) {
                 // Lemma 3 refinement: an unknown head F(s, j) waits for F(s-1, j) on the
                 // device of stage s-1, which lasts c_F(s-1) and then travels oF(s-1)
-                T pf = INF, pb = INF;
+                T pf = INF, pb = INF, lf = 0, lb = 0;
                 bool fl = true, bl = false;
                 if (s > 0 && dev_of(sl.placement, p, s - 1) != d) {
                   const int a0 = cuts[s - 1];
-                  pf = (T)dsum(kColTF, a0, a) + lat(a - 1);
+                  if constexpr (FP) { pf = (T)dsum(kColTF, a0, a); lf = lat(a - 1); }
+                  else pf = (T)dsum(kColTF, a0, a) + lat(a - 1);
                   fl = dev_of(sl.placement, p, s - 1) == (d == 0 ? p - 1 : d - 1);
                 }
                 if (s < S - 1 && dev_of(sl.placement, p, s + 1) != d) {
                   const int b1 = cuts[s + 2];
-                  pb = (T)dsum(kColTB, b, b1) + lat(b - 1);
+                  if constexpr (FP) { pb = (T)dsum(kColTB, b, b1); lb = lat(b - 1); }
+                  else pb = (T)dsum(kColTB, b, b1) + lat(b - 1);
                   bl = dev_of(sl.placement, p, s + 1) == (d == 0 ? p - 1 : d - 1);
+                }
+                if constexpr (FP) {
+                  ga_lF[c * 32 + lane] = lf;
+                  ga_lB[c * 32 + lane] = lb;
                 }
                 // gate is set below, once stat is complete
                 ga_pF[c * 32 + lane] = pf;
@@ -699,6 +720,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             const T dm = seg_min_m(dmin, p2, smask), cm = seg_min_m(cmin, p2, smask);
             if (take) {
               window = (cm == INF) ? INF : dm + cm;
+              w_dm = dm; w_cm = cm;
               gdirty = true;
 #pragma unroll
               tstar = 0;
@@ -962,18 +984,22 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       const T atl = __shfl_sync(FULLMASK, at, nleft);
       const T atr = __shfl_sync(FULLMASK, at, nright);
       T bound = INF;
-      const T tw = sat_add(tstar, window);
+      T tw;
+      if constexpr (FP) tw = sat_add(sat_add(tstar, w_dm), w_cm);  // rounded as an arrival is
+      else tw = sat_add(tstar, window);
       const T nl = atl < tw ? atl : tw;
       const T nr = atr < tw ? atr : tw;
       auto tighten = [&]() {
 #pragma unroll
         for (int c = 0; c < V; ++c) {
           if (g_unk & (1u << c)) {
-            const T x = sat_add((pleft >> c) & 1u ? nl : nr, ga_pF[c * 32 + lane]);
+            T x = sat_add((pleft >> c) & 1u ? nl : nr, ga_pF[c * 32 + lane]);
+            if constexpr (FP) x = sat_add(x, ga_lF[c * 32 + lane]);
             bound = x < bound ? x : bound;
           }
           if (g_unk & (1u << (V + c))) {
-            const T x = sat_add((pleft >> (V + c)) & 1u ? nl : nr, ga_pB[c * 32 + lane]);
+            T x = sat_add((pleft >> (V + c)) & 1u ? nl : nr, ga_pB[c * 32 + lane]);
+            if constexpr (FP) x = sat_add(x, ga_lB[c * 32 + lane]);
             bound = x < bound ? x : bound;
           }
         }

@@ -51,6 +51,10 @@ def check(prep, pr, items):
             assert got["peak_mem"][i] == want["peak_mem"], i
             for key in ("T_d", "busy_d", "M_d", "comm_d", "exposed_d"):
                 assert list(got[key][i]) == want[key], (i, key, list(got[key][i]), want[key])
+            # R29's derived rows come from the ABI report, checked against the definition
+            assert list(got["overlap_d"][i]) == [c - e for c, e in zip(want["comm_d"], want["exposed_d"])]
+            assert list(got["bubble_d"][i]) == [t - b - e for t, b, e in
+                                                zip(want["T_d"], want["busy_d"], want["exposed_d"])]
         n_stuck += want["status"] == 3
     return n_ok, n_stuck, n_slower
 

@@ -220,51 +220,94 @@ def _fp32_problem(pr, seed):
 
 
 def _compare_fp32(got, want, where):
+    """R27: the kernel and the oracle's fp32-time event loop take every time
+    decision in fp32 with the same roundings, so status, peak and the fp32
+    makespan are bit-identical."""
     st_g, st_w = np.asarray(got["status"]), np.asarray(want["status"])
-    ok = (st_w == 0) & (st_g == 0)
-    g = np.asarray(got["makespan_f32"], np.float64)[ok]
-    w = np.asarray(want["makespan_f"])[ok]
-    rel = np.abs(g - w) / w
-    assert ok.sum() >= 0.9 * (st_w == 0).sum(), where + ": status disagreements"
-    assert np.all(rel <= FP32_RTOL), "%s: max rel %.3g at %s" % (where, rel.max(), np.argmax(rel))
-    return int(ok.sum()), float(rel.max() if rel.size else 0.0)
+    bad = np.nonzero(st_g != st_w)[0]
+    assert bad.size == 0, "%s: %d status mismatches, first %s" % (where, bad.size, bad[:10])
+    ok = st_w == 0
+    g = np.asarray(got["makespan_f32"], np.float32)[ok]
+    w = np.asarray(want["makespan_f"]).astype(np.float32)[ok]
+    bad = np.nonzero(g != w)[0]
+    assert bad.size == 0, "%s: %d fp32 makespan mismatches, first gpu %s oracle %s" % (
+        where, bad.size, g[bad[:5]], w[bad[:5]])
+    both = (st_w == 0) | (st_w == 2)
+    assert np.array_equal(np.asarray(got["peak_mem"])[both], np.asarray(want["peak_mem"])[both])
+    return int(ok.sum())
+
+
+def _fp32_vs_real(pr, sp, idx, where):
+    """The fp32-cost variant against real (fp64) arithmetic on the same fp32
+    costs, on the oracle: fixed orders are max-plus recurrences with no
+    time-dependent decision, so they stay within the north star's 1e-5; ZB /
+    GREEDY compare times to decide, and a tie in real arithmetic can round
+    either way in fp32 (R27). Returns the split policies' disagreement counts."""
+    from paper_2509_23722_b200 import adaptis as A
+    a = O.eval_indices(pr, sp, idx, precision="f32")
+    b = O.eval_indices(pr, sp, idx)
+    fixed = np.array([A.decode(pr, sp, int(i))["policy"] in (W.GPIPE, W.ONEF1B) for i in idx])
+    sa, sb = np.asarray(a["status"]), np.asarray(b["status"])
+    assert np.array_equal(sa[fixed], sb[fixed]), where
+    ok = (sa == 0) & (sb == 0)
+    rel = np.abs(np.asarray(a["makespan_f"]) - np.asarray(b["makespan_f"])) / np.asarray(b["makespan_f"])
+    assert np.all(rel[ok & fixed] <= FP32_RTOL), where
+    split = ~fixed
+    n_status = int(np.sum(sa[split] != sb[split]))
+    n_far = int(np.sum(rel[ok & split] > FP32_RTOL))
+    print("%s: split policies: %d of %d status differ from real arithmetic, %d of %d makespans "
+          "beyond 1e-5 (fixed orders: 0 of %d)" % (where, n_status, int(split.sum()), n_far,
+                                                    int((ok & split).sum()), int((ok & fixed).sum())))
+    return n_status, n_far
 
 
 @pytest.mark.parametrize("cid,first,count", [(1, 0, 244), (2, 123456, 4096), (3, 9_173_505, 2048),
                                              (3, 85_357_574, 2048), (3, 115_000_000, 1024),
                                              (5, 100_000_000, 256), (5, 300_000_000, 128)])
-def test_fp32_variant_within_tolerance(ctx, cid, first, count):
-    """Dyadic fractional costs (k/8 ticks): every makespan within 1e-5 of fp64."""
+def test_fp32_variant_bit_exact(ctx, cid, first, count):
+    """Dyadic fractional costs (k/8 ticks): the GPU's fp32 results equal the
+    oracle's fp32 event loop bit for bit, and every fixed-order makespan is
+    within 1e-5 of real arithmetic."""
     pr, sp = W.config(cid)
     prf = _fp32_problem(pr, 100 + cid)
     got = ctx.eval_batch(prf, sp, first, count)
-    want = O.eval_indices(prf, sp, range(first, first + count))
-    n, mx = _compare_fp32(got, want, "cfg%d fp32" % cid)
+    idx = range(first, first + count)
+    n = _compare_fp32(got, O.eval_indices(prf, sp, idx, precision="f32"), "cfg%d fp32" % cid)
     assert n > 0
+    _fp32_vs_real(prf, sp, np.arange(first, first + count, dtype=np.uint64), "cfg%d" % cid)
 
 
 def test_fp32_variant_nondyadic_costs(ctx):
-    """Costs k/7 are not representable in fp32. Fixed orders (no time-dependent
-    decisions) stay within 1e-5; ZB / GREEDY may resolve a real-arithmetic tie
-    differently from fp64 (R27), which must stay rare."""
-    from paper_2509_23722_b200 import adaptis as A
+    """Costs k/7 are not representable in fp32 (every addition rounds). The GPU
+    still equals the oracle's fp32 event loop bit for bit (status included) for
+    every policy; against real arithmetic, fixed orders stay within 1e-5."""
     pr, sp = W.config(1)
     prf = _fp32_problem(pr, 3)
     prf.costs_f32 = W.fractional_costs(pr, W.SplitMix64(3), denom=7)
     N = O.space_size(prf, sp)
     got = ctx.eval_batch(prf, sp, 0, N)
-    want = O.eval_indices(prf, sp, range(N))
-    fixed = np.array([A.decode(pr, sp, i)["policy"] in (W.GPIPE, W.ONEF1B) for i in range(N)])
-    ok = (np.asarray(want["status"]) == 0) & (np.asarray(got["status"]) == 0)
-    rel = np.abs(np.asarray(got["makespan_f32"], np.float64) - want["makespan_f"]) / want["makespan_f"]
-    assert np.all(rel[ok & fixed] <= FP32_RTOL)
-    assert np.mean(rel[ok & ~fixed] <= FP32_RTOL) >= 0.95
+    _compare_fp32(got, O.eval_indices(prf, sp, range(N), precision="f32"), "cfg1 k/7")
+    _fp32_vs_real(prf, sp, np.arange(N, dtype=np.uint64), "cfg1 k/7")
+    for pr2, sp2 in _random_spaces(41, 8):
+        prf2 = _fp32_problem(pr2, 5)
+        prf2.costs_f32 = W.fractional_costs(pr2, W.SplitMix64(5), denom=7)
+        N2 = O.space_size(prf2, sp2)
+        got = ctx.eval_batch(prf2, sp2, 0, N2)
+        _compare_fp32(got, O.eval_indices(prf2, sp2, range(N2), precision="f32"),
+                      "random k/7 p=%d m=%d" % (pr2.p, pr2.m))
 
 
 def test_fp32_search_winner_within_tolerance(ctx):
     pr, sp = W.config(1)
     prf = _fp32_problem(pr, 7)
     b = ctx.search(prf, sp)
+    w32 = O.eval_indices(prf, sp, range(O.space_size(prf, sp)), precision="f32")
+    ok = w32["status"] == 0
+    ms32 = np.asarray(w32["makespan_f"]).astype(np.float32)
+    best32 = ms32[ok].min()
+    # the fp32 argmin is the oracle's fp32 argmin (lowest index among equal makespans)
+    assert b["index"] == int(np.nonzero(ok & (ms32 == best32))[0][0])
+    assert np.float32(b["makespan_f32"]) == best32
     want = O.eval_indices(prf, sp, range(O.space_size(prf, sp)))
     best = np.min(want["makespan_f"][want["status"] == 0])
     assert b["makespan_f32"] <= best * (1 + FP32_RTOL)  # T7: the winner is within 1e-5 of the optimum
@@ -370,11 +413,13 @@ def test_pruned_search_after_smaller_space_keeps_incumbent():
     c = A.Context(0)
     try:
         c.set_prune(True)
+        from test_gpu_goldens import golden_argmin
         pr2, sp2 = W.config(2)
-        assert c.search(pr2, sp2)["index"] == 2962620
+        assert c.search(pr2, sp2)["index"] == golden_argmin(2)["index"]
         pr3, sp3 = W.config(3)
         b = c.search(pr3, sp3)
-        assert (b["index"], b["makespan"]) == (85623303, 1138352)
+        g3 = golden_argmin(3)
+        assert (b["index"], b["makespan"]) == (g3["index"], g3["makespan"])
     finally:
         c.close()
 
@@ -385,7 +430,8 @@ def test_context_reuse_across_calls_and_configs():
     generator, the int64 and fp32 kernels): every result still matches the
     known winners or the oracle, so no per-context buffer carries stale state."""
     from paper_2509_23722_b200 import adaptis as A
-    wins = {1: (228, 56600), 2: (2962620, 440527), 3: (85623303, 1138352), 4: (61471876, 879178)}
+    from test_gpu_goldens import golden_argmin  # oracle-written (tools/oracle_argmin.py)
+    wins = {c: (golden_argmin(c)["index"], golden_argmin(c)["makespan"]) for c in (1, 2, 3, 4)}
     c = A.Context(0)
     try:
         seq = [(1, False), (4, True), (2, False), (3, True), (1, True), (3, False), (2, True)]

@@ -342,6 +342,23 @@ def test_cfg1_unit_advisory_golden():
     evl = O.eval_indices(pr, lit, range(165))
     ties = [i for i in range(165) if evl["makespan"][i] == 218]
     assert ties == g["literal_three_policy"]["tied_indices"]
+    # per-combo optima: the only cross-implementation anchors on WAVE placement
+    # and on the v = 4 ZB / GREEDY combos (SURVEY §8(c) cfg1 golden values)
+    names = {(W.SEQ, 0): "GPIPE", (W.SEQ, 1): "ONEF1B", (W.SEQ, 2): "ZB", (W.SEQ, 3): "GREEDY"}
+    for plc, pn in ((W.INTERLEAVED, "INT"), (W.WAVE, "WAVE")):
+        for pol, qn in ((0, "GPIPE"), (1, "ONEF1B"), (2, "ZB"), (3, "GREEDY")):
+            names[(plc, pol)] = pn + "_" + qn
+    seen = 0
+    for v in (1, 2, 4):
+        for k in range(6):
+            c = O.combo(v, k)
+            if c is None:
+                continue
+            one = W.Space([W.Group(v, W.FULL, combo_mask=1 << k)])
+            bc = O.search(pr, one, prune=False)
+            assert bc["makespan"] == g["per_combo_best"]["v%d" % v][names[c]], (v, c)
+            seen += 1
+    assert seen == 16
 
 
 # ---------------------------------------------------------------- fp64 reference of the fp32 variant
@@ -365,6 +382,59 @@ def test_f64_event_loop_equals_int64_on_integer_costs():
             assert (a["status"], a["makespan"], a["peak_mem"]) == (b["status"], b["makespan"], b["peak_mem"])
             if a["status"] == 0:
                 assert b["makespan_f"] == float(a["makespan"])
+
+
+def test_f32_event_loop_equals_int64_on_integer_costs():
+    """R27: the fp32-time event loop on integer costs (exact in fp32 below 2^24)
+    reproduces the exact int64 one, decisions included, for every policy."""
+    rng = W.SplitMix64(556)
+    for _ in range(120):
+        p = 1 + rng.next() % 4
+        m = p * (1 + rng.next() % 2)
+        L = 2 * p + 1 + rng.next() % 3
+        pr = W.random_problem(rng, L, p, m, bytes_max=6, cap=W.INT64_MAX if rng.next() % 2 else 80)
+        prf = W.Problem(**{c: getattr(pr, c) for c in W.COLUMNS}, p=p, m=m, cap=pr.cap, cost_type=1,
+                        costs_f32=np.stack([pr.t_f, pr.t_b, pr.t_w, pr.comm]).astype(np.float32))
+        v, placement = (2, W.INTERLEAVED) if L >= 2 * p else (1, W.SEQ)
+        cuts = list(range(1, p * v))
+        for pol in range(4):
+            a = O.simulate(pr, v, placement, pol, cuts)
+            b = O.simulate(prf, v, placement, pol, cuts, precision="f32")
+            assert (a["status"], a["makespan"], a["peak_mem"]) == (b["status"], b["makespan"], b["peak_mem"])
+            if a["status"] == 0:
+                assert b["makespan_f"] == float(a["makespan"])
+
+
+@pytest.mark.parametrize("policy", [W.GPIPE, W.ONEF1B, W.ZB, W.GREEDY])
+def test_f32_serial_device_rounds_every_addition(policy):
+    """R27 fp32 arithmetic on one device (p = 1, no latency): the makespan is
+    the fp32 running sum of the task durations in execution order, each stage
+    duration the fp32 rounding of its exact row sum (fused B: of t_B + t_W).
+    On one device every task is ready when the device is free, so the order is
+    the policy's priority order alone; it is taken from the int64 oracle's trace
+    (pinned by the closed forms above) and the sum is done here with numpy
+    float32 additions. Costs near 1e7 make fp32 rounding differ from fp64."""
+    m = 5
+    t = np.array([[1e7 + 0.375, 3.25], [2e7 + 0.125, 1.5], [1.0e7 + 0.625, 0.75], [0, 0]], np.float64)
+    t32 = t.astype(np.float32).astype(np.float64)
+    z = [0, 0]
+    pri = W.Problem(t_f=[3, 1], t_b=[3, 1], t_w=[3, 1], act=z, stash=z, weight=z, grad=z, comm=z, p=1, m=m)
+    prf = W.Problem(t_f=[3, 1], t_b=[3, 1], t_w=[3, 1], act=z, stash=z, weight=z, grad=z, comm=z,
+                    p=1, m=m, cost_type=1, costs_f32=t.astype(np.float32))
+    fused = policy in (W.GPIPE, W.ONEF1B)
+    dur = {0: np.float32(t32[0].sum()),
+           1: np.float32(t32[1].sum() + (t32[2].sum() if fused else 0.0)),
+           2: np.float32(t32[2].sum())}
+    order = O.simulate(pri, 1, W.SEQ, policy, [], trace=True)["trace"][0]
+    assert len(order) == m * (2 if fused else 3)
+    acc = np.float32(0)
+    for (k, _s, _j, _st) in order:
+        acc = np.float32(acc + dur[k])
+    r = O.simulate(prf, 1, W.SEQ, policy, [], precision="f32")
+    assert r["status"] == 0 and r["makespan_f"] == float(acc)
+    exact = O.simulate(prf, 1, W.SEQ, policy, [])["makespan_f"]
+    assert r["makespan_f"] != exact  # fp32 rounding is visible here
+    assert abs(r["makespan_f"] - exact) <= 1e-5 * exact
 
 
 @pytest.mark.parametrize("p,m", [(2, 4), (4, 8)])
@@ -572,3 +642,40 @@ def test_tune_overlap_invariants():
                         grad=pr.grad, comm=[0] * len(pr.t_f), p=pr.p, m=pr.m)
         assert O.tune_overlap(pr0, 1, 0, fused, cuts, lists)[1] == 0
     assert moved > 20
+
+
+def test_tune_overlap_spec_two_device_example():
+    """SPEC S:374 (tune_overlap examples, R32): a two-device instance with
+    comm_time = t_F where a consumer waits right after its producer's transfer.
+    Worked by hand (unit costs, one layer per stage, latency 1, split B/W):
+      dev0 [F00 F01 B00 B01 W00 W01]: F00 [0,1] F01 [1,2] B00 [5,6] (waits for
+        B10's arrival 4+1) B01 [7,8] (waits for B11's arrival 6+1) W00 [8,9] W01 [9,10]
+      dev1 [F10 B10 F11 B11 W10 W11]: [2,3] [3,4] [4,5] [5,6] [6,7] [7,8]
+    makespan 10; exposed (union of incident transfers outside compute, R29)
+    dev0 [2,3] [4,5] [6,7] = 3 of comm 4, dev1 [1,2] = 1 of comm 4: overlap 1 + 3.
+    The R32 neighbours are: B01 before B00 (makespan 11), F11 before F10 (11),
+    and W00 before the waiting B01 (W00 [6,7] hides B11's transfer, makespan 9),
+    so exactly one swap is accepted and the overlap rises by comm_time = 1; in
+    the new schedule the remaining neighbours are both 11 (no further swap).
+    The fully dependent chain (m = 1) has no neighbour at all: no-op."""
+    z = [0, 0]
+    pr = W.Problem(t_f=[1, 1], t_b=[1, 1], t_w=[1, 1], act=z, stash=z, weight=z, grad=z,
+                   comm=[1, 0], p=2, m=2)
+    F, B, Wk = 0, 1, 2
+    lists = [[(F, 0, 0), (F, 0, 1), (B, 0, 0), (B, 0, 1), (Wk, 0, 0), (Wk, 0, 1)],
+             [(F, 1, 0), (B, 1, 0), (F, 1, 1), (B, 1, 1), (Wk, 1, 0), (Wk, 1, 1)]]
+    a0 = O.comm_accounting_lists(pr, 1, W.SEQ, False, [1], lists)
+    assert a0["makespan"] == 10 and a0["T_d"] == [10, 8]
+    assert a0["comm_d"] == [4, 4] and a0["exposed_d"] == [3, 1] and a0["overlap_d"] == [1, 3]
+    nl, swaps, acc = O.tune_overlap(pr, 1, W.SEQ, False, [1], lists)
+    assert swaps == 1
+    assert [list(map(tuple, x)) for x in nl] == [
+        [(F, 0, 0), (F, 0, 1), (B, 0, 0), (Wk, 0, 0), (B, 0, 1), (Wk, 0, 1)], lists[1]]
+    assert acc["makespan"] == 9 and acc["T_d"] == [9, 8]
+    assert acc["exposed_d"] == [2, 1] and acc["overlap_d"] == [2, 3]
+    assert sum(acc["overlap_d"]) == sum(a0["overlap_d"]) + 1  # + comm_time
+    pr1 = W.Problem(t_f=[1, 1], t_b=[1, 1], t_w=[1, 1], act=z, stash=z, weight=z, grad=z,
+                    comm=[1, 0], p=2, m=1)
+    chain = [[(F, 0, 0), (B, 0, 0), (Wk, 0, 0)], [(F, 1, 0), (B, 1, 0), (Wk, 1, 0)]]
+    assert O.overlap_candidates(pr1, 1, W.SEQ, False, [1], chain) == []
+    assert O.tune_overlap(pr1, 1, W.SEQ, False, [1], chain)[1] == 0
