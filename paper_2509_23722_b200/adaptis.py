@@ -104,7 +104,8 @@ class _GenResult(C.Structure):
 class _LaunchInfo(C.Structure):
     _fields_ = [("group", C.c_int32), ("combo", C.c_int32), ("v", C.c_int32),
                 ("placement", C.c_int32), ("policy", C.c_int32), ("fallback", C.c_int32),
-                ("candidates", C.c_uint64), ("tasks", C.c_uint64), ("ms", C.c_float)]
+                ("candidates", C.c_uint64), ("tasks", C.c_uint64), ("ms", C.c_float),
+                ("kernel", C.c_int32)]
 
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)

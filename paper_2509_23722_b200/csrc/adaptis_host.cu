@@ -56,6 +56,7 @@ struct adaptis_prepared {
   uint64_t N = 0;
   int key_bits = 1;
   int tick = kTickI32;
+  bool seq_ok = false;  // sequential GREEDY kernel admitted: U < 2^28, latencies < 2^16
   std::vector<uint64_t> h_binom, h_ball;
   std::vector<int16_t> h_seeds;
   std::vector<int64_t> h_cols, h_comm;  // host copies of the layer columns (kNumCols x L) and comm
@@ -64,6 +65,7 @@ struct adaptis_prepared {
   double* d_colsf = nullptr;
   float* d_commf = nullptr;
   int64_t* d_cols = nullptr;
+  int64_t* d_pre = nullptr;
   int64_t* d_comm = nullptr;
   uint64_t* d_binom = nullptr;
   uint64_t* d_ball = nullptr;
@@ -309,6 +311,12 @@ adaptis_status build_space(adaptis_ctx* ctx, const adaptis_problem* pr, const ad
     return fail(ctx, ADAPTIS_EOVERFLOW, "makespan bound and %d index bits exceed the 63-bit key", bits);
   P->tick = U >= ((unsigned __int128)1 << 31) - 1 ? kTickI64 : kTickI32;
   if (getenv("ADAPTIS_FORCE_INT64")) P->tick = kTickI64;  // test hook: exercise the int64 path
+  // the sequential GREEDY kernel packs (at << 4 | device) into 32 bits and
+  // both latencies of a stage into one word
+  bool lat16 = true;
+  for (int l = 0; l + 1 < Ly.L; ++l) lat16 = lat16 && Ly.comm_ticks[l] < (1 << 16);
+  P->seq_ok = P->tick == kTickI32 && U < ((unsigned __int128)1 << 28) && lat16 &&
+              !getenv("ADAPTIS_NO_SEQG");
   return ADAPTIS_OK;
 }
 
@@ -346,7 +354,13 @@ adaptis_status upload(adaptis_ctx* ctx, const adaptis_problem* pr, adaptis_prepa
     P->tabs.colsf = P->d_colsf;
     P->tabs.commf = P->d_commf;
   }
+  std::vector<int64_t> pre((size_t)kNumCols * (L + 1), 0);
+  for (int c = 0; c < kNumCols; ++c)
+    for (int l = 0; l < L; ++l)
+      pre[(size_t)c * (L + 1) + l + 1] = pre[(size_t)c * (L + 1) + l] + cols[(size_t)c * L + l];
   CU(ctx, cudaMalloc(&P->d_cols, cols.size() * 8));
+  CU(ctx, cudaMalloc(&P->d_pre, pre.size() * 8));
+  CU(ctx, cudaMemcpyAsync(P->d_pre, pre.data(), pre.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
   CU(ctx, cudaMalloc(&P->d_comm, comm.size() * 8));
   CU(ctx, cudaMalloc(&P->d_binom, P->h_binom.size() * 8));
   CU(ctx, cudaMalloc(&P->d_ball, P->h_ball.size() * 8));
@@ -358,6 +372,7 @@ adaptis_status upload(adaptis_ctx* ctx, const adaptis_problem* pr, adaptis_prepa
   CU(ctx, cudaMemcpyAsync(P->d_seeds, P->h_seeds.data(), P->h_seeds.size() * 2, cudaMemcpyHostToDevice, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors die on return
   P->tabs.cols = P->d_cols; P->tabs.comm = P->d_comm; P->tabs.binom = P->d_binom;
+  P->tabs.pre = P->d_pre;
   P->tabs.ball = P->d_ball; P->tabs.seeds = P->d_seeds;
   return ADAPTIS_OK;
 }
@@ -423,6 +438,12 @@ int ring_slots(int policy, int m) {
   int pw = 1;
   while (pw < k) pw <<= 1;
   return pw;
+}
+// warps of sequential-GREEDY state an SM must hold for that kernel to be used
+// (below, the lane-per-device kernel keeps more candidates in flight)
+int seqg_min_warps() {
+  static const int w = getenv("ADAPTIS_SEQG_MINW") ? atoi(getenv("ADAPTIS_SEQG_MINW")) : 4;
+  return w;
 }
 constexpr uint64_t kSeedPass = 4096;  // indices per segment in the pruned search's seed pass
 constexpr size_t kHdr = 8;  // [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds [5] pruned
@@ -549,7 +570,12 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
                   s.L, s.S, smem_bytes(s, true), ctx->max_smem);
     CU(ctx, cudaEventRecord(ctx->seg_events[2 * i], ctx->stream));
     int e;
-    if (direct_global) {
+    if (seqg_eligible(s, P->seq_ok, ctx->max_smem, seqg_min_warps())) {
+      // GREEDY as one exact event loop per thread (adaptis_seqg.cu); ring
+      // overflows go to the global-ring fallback below like the fast path's
+      jobs[i].info.kernel = 1;
+      e = launch_seqg(P->tabs, s, ctx->num_sms, ctx->stream);
+    } else if (direct_global) {
       unsigned grid_limit = 0;
       st = ensure_gring(ctx, P, s, &grid_limit);
       if (st != ADAPTIS_OK) return st;
@@ -1034,7 +1060,7 @@ adaptis_status adaptis_prepare(adaptis_ctx* ctx, const adaptis_problem* problem,
 
 void adaptis_prepared_free(adaptis_prepared* P) {
   if (!P) return;
-  cudaFree(P->d_cols); cudaFree(P->d_comm); cudaFree(P->d_colsf); cudaFree(P->d_commf); cudaFree(P->d_binom); cudaFree(P->d_ball);
+  cudaFree(P->d_cols); cudaFree(P->d_pre); cudaFree(P->d_comm); cudaFree(P->d_colsf); cudaFree(P->d_commf); cudaFree(P->d_binom); cudaFree(P->d_ball);
   cudaFree(P->d_seeds);
   delete P;
 }

@@ -26,6 +26,7 @@ struct DevTables {
   const int16_t* seeds;     // [n_groups][ADAPTIS_MAX_S]  (interior cuts of the BALL seed)
   const double* colsf;      // FP32 cost mode: [3][L] t_f, t_b, t_w as real ticks
   const float* commf;       // FP32 cost mode: [L] comm as real ticks
+  const int64_t* pre;       // [kNumCols][L + 1] prefix sums of cols (sequential GREEDY setup)
 };
 
 // One launch = one (group, combo) segment of the canonical order (R19),
@@ -145,6 +146,10 @@ int launch_contend(const int64_t* cols, const int64_t* comm, int L, int p, int m
                    int64_t* scratch, uint64_t stride, int64_t* makespan, int64_t* peak, float* bubble,
                    uint8_t* status, int64_t* report, unsigned long long* n_tasks, int Sm, void* stream);
 int occupancy_ctas_per_sm(const SegLaunch& s, bool fallback);
+// sequential GREEDY kernel (adaptis_seqg.cu): one thread per candidate
+size_t seqg_smem_bytes(int S, int p);
+bool seqg_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int min_warps);
+int launch_seqg(const DevTables& t, const SegLaunch& s, int num_sms, void* stream);
 size_t smem_bytes(const SegLaunch& s, bool fallback);
 
 }  // namespace adaptis

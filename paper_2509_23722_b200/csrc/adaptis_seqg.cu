@@ -1,0 +1,441 @@
+// adaptis_seqg.cu — the GREEDY policy (R14) as one exact event loop per
+// thread: 32 candidates per warp, each simulated by the global event loop of
+// Alg. 1 Step 3 in strict time order.
+//
+// Why a thread per candidate. The lane-per-device kernel (adaptis_seg.cuh)
+// advances a candidate in bounded-lag rounds: every round all p lanes decide,
+// reduce t*, exchange bounds and vote, and 55-67 % of them commit a task. That
+// is ~16 warp-instructions per task. Here one thread commits exactly one task
+// per step, with no shuffles, votes or bounds: a step is the argmin over the
+// devices' cached decisions (at << 4 | d), the commit, and the re-decision of
+// the two devices whose inputs changed (the committing device and the
+// consumer of its output). All candidates of a segment have the same task
+// count S * m * 3, so the 32 threads of a warp step in lockstep.
+//
+// Exact state compression (DESIGN.md §4 "sequential GREEDY"). In a
+// time-ordered event loop every pending task starts at >= the current event
+// time t. An item whose arrival A <= t is therefore interchangeable with t
+// for its consumer's decision: at = max(free, min ready) and the set of tasks
+// ready by `at` are unchanged when A is replaced by any X with A <= X <= at
+// (if free >= t both give `free`; if free < t then at >= t >= A forces A = t).
+// So an edge keeps the exact arrival times of its last K produced items only;
+// an older unconsumed item is known to have arrived. A producer overwriting
+// the slot of an unconsumed item whose arrival is still in the future marks
+// the candidate OVERFLOW, and the exact global-ring kernel re-runs it. With
+// the configs' tables (latency 40 ticks, stage tasks >= ~600 ticks) an edge has
+// at most 2 future arrivals, so K = 2 never overflows there.
+//
+// Ties. Devices with the same decision time are independent (a commit at t
+// produces arrivals > t, which change neither the other device's decision time
+// nor the set of its tasks ready by t), so the order among them does not
+// change the result; the key breaks them by device.
+//
+// Layout. All per-candidate state lives in shared memory as [field][lane]
+// words (conflict-free for any per-lane index): per device the cached key
+// (at << 4 | d), free << 4 | decision, dyn, cap - static, peak; per stage the
+// counters gF | gB << 8 | gW << 16, durations, latencies, act + stash and act
+// bytes, and the K-slot arrival rings of its F and B inputs.
+#include "adaptis_seg.cuh"
+
+namespace adaptis {
+
+#ifndef ADAPTIS_SEQG_K
+#define ADAPTIS_SEQG_K 2
+#endif
+constexpr int kSeqK = ADAPTIS_SEQG_K;   // exact arrival slots per edge (power of two)
+constexpr uint32_t kSeqInf = 0xffffffffu;
+
+// shared-memory rows of one lane (a row is 32 lanes x 4 or 8 bytes)
+struct SeqLayout {
+  int key, fd, cnt, dur, lat, rf, rb, n32;  // u32 rows
+  int dyn, capd, peak, as, act, n64;        // u64 rows
+};
+ADAPTIS_LAYOUT_HD SeqLayout seq_layout(int S, int P2) {
+  SeqLayout l;
+  int r = 0;
+  l.key = r; r += P2;
+  l.fd = r; r += P2;
+  l.cnt = r; r += S;
+  l.dur = r; r += 3 * S;
+  l.lat = r; r += S;
+  l.rf = r; r += kSeqK * S;
+  l.rb = r; r += kSeqK * S;
+  l.n32 = (r + 1) & ~1;  // keep the u64 rows 8-byte aligned
+  r = 0;
+  l.dyn = r; r += P2;
+  l.capd = r; r += P2;
+  l.peak = r; r += P2;
+  l.as = r; r += S;
+  l.act = r; r += S;
+  l.n64 = r;
+  return l;
+}
+size_t seqg_smem_bytes(int S, int p) {
+  int P2 = 1;
+  while (P2 < p) P2 <<= 1;
+  const SeqLayout l = seq_layout(S, P2);
+  return (size_t)32 * (4 * l.n32 + 8 * l.n64);
+}
+
+template <int V, int P2, bool SEARCH>
+__global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const SegLaunch sl) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int L = sl.L, p = sl.p, m = sl.m, S = V * sl.p, plc = sl.placement;
+  const SeqLayout lay = seq_layout(S, P2);
+  uint32_t* w32 = reinterpret_cast<uint32_t*>(smem);
+  int64_t* w64 = reinterpret_cast<int64_t*>(smem + (size_t)128 * lay.n32);
+#define R32(row) w32[(row) * 32 + lane]
+#define R64(row) w64[(row) * 32 + lane]
+#define KEY(d) R32(lay.key + (d))
+#define FD(d) R32(lay.fd + (d))
+#define CNT(s) R32(lay.cnt + (s))
+#define DUR(k, s) R32(lay.dur + (k) * S + (s))
+#define LAT(s) R32(lay.lat + (s))
+#define RF(k, s) R32(lay.rf + (k) * S + (s))
+#define RB(k, s) R32(lay.rb + (k) * S + (s))
+#define DYN(d) R64(lay.dyn + (d))
+#define CAPD(d) R64(lay.capd + (d))
+#define PEAK(d) R64(lay.peak + (d))
+#define AS(s) R64(lay.as + (s))
+#define ACT(s) R64(lay.act + (s))
+  const int64_t* pre = tab.pre;  // [kNumCols][L + 1] prefix sums (global, read-only)
+  auto PRE = [&](int col, int row) -> int64_t { return __ldg(pre + (size_t)col * (L + 1) + row); };
+
+  // GREEDY decision of device d at event time tnow (R14): candidates are the
+  // next F of each own stage if it fits under Eq. 2, the head B whose F is
+  // done, the head W whose B is done; at = max(free, earliest ready); among
+  // the tasks ready by `at` the smallest (kind F < B < W, mb, stage) wins.
+  auto decide = [&](int d, uint32_t tnow) {
+    const uint32_t free_t = FD(d) >> 4;
+    const int64_t dy = DYN(d), capd = CAPD(d);
+    uint32_t rf[V], rb[V], rw[V], kx[V], kbx[V], kwx[V];
+    uint32_t rmin = kSeqInf;
+#pragma unroll
+    for (int c = 0; c < V; ++c) {
+      const int s = stage_of(plc, p, c, d);
+      const uint32_t cnt = CNT(s);
+      const uint32_t gF = cnt & 255u, gB = (cnt >> 8) & 255u, gW = (cnt >> 16) & 255u;
+      uint32_t r = kSeqInf;
+      if (gF < (uint32_t)m && dy + AS(s) <= capd) {
+        if (s == 0) {
+          r = 0;
+        } else {
+          const uint32_t prodF = CNT(s - 1) & 255u;  // F items produced into stage s
+          if (gF < prodF) r = (gF + kSeqK >= prodF) ? RF(gF & (kSeqK - 1), s) : tnow;
+        }
+      }
+      rf[c] = r;
+      r = kSeqInf;
+      if (gB < gF) {
+        if (s == S - 1) {
+          r = 0;
+        } else {
+          const uint32_t prodB = (CNT(s + 1) >> 8) & 255u;  // B items produced into stage s
+          if (gB < prodB) r = (gB + kSeqK >= prodB) ? RB(gB & (kSeqK - 1), s) : tnow;
+        }
+      }
+      rb[c] = r;
+      rw[c] = gW < gB ? 0u : kSeqInf;
+      kx[c] = (gF << 2) | (uint32_t)c;
+      kbx[c] = (gB << 2) | (uint32_t)c;
+      kwx[c] = (gW << 2) | (uint32_t)c;
+      rmin = min(rmin, min(rf[c], min(rb[c], rw[c])));
+    }
+    if (rmin == kSeqInf) { KEY(d) = kSeqInf; return; }
+    const uint32_t at = max(free_t, rmin);
+    uint32_t kF = kSeqInf, kB = kSeqInf, kW = kSeqInf;
+#pragma unroll
+    for (int c = 0; c < V; ++c) {
+      if (rf[c] <= at) kF = min(kF, kx[c]);
+      if (rb[c] <= at) kB = min(kB, kbx[c]);
+      if (rw[c] <= at) kW = min(kW, kwx[c]);
+    }
+    const uint32_t dec = kF != kSeqInf ? ((kF & 3u) << 2)
+                       : kB != kSeqInf ? (1u | ((kB & 3u) << 2)) : (2u | ((kW & 3u) << 2));
+    KEY(d) = (at << 4) | (uint32_t)d;
+    FD(d) = (free_t << 4) | dec;
+  };
+
+  unsigned long long best_key = ~0ull >> 1, n_inv = 0, n_pr = 0, n_tasks = 0;
+  int16_t cuts[ADAPTIS_MAX_S + 1];
+  const int16_t* seed = tab.seeds + sl.group * ADAPTIS_MAX_S;
+  uint64_t rpos = 0, rend = 0, prev_idx = ~0ull - 1;
+  int brem = 0;
+  bool exhausted = false;
+  const int T = S * m * 3;  // tasks per candidate (split policy)
+
+  for (;;) {
+    // ---- setup: every lane looks for its next candidate to simulate (a1-a4);
+    // invalid decodes and pruned candidates are finalised here
+    bool have = false;
+    uint64_t idx = 0, slot = 0;
+    for (;;) {
+      const bool need = !have && !(exhausted && rpos >= rend);
+      const unsigned need_m = __ballot_sync(FULLMASK, need);
+      if (!need_m) break;
+      // lanes whose runs are empty claim new runs with one atomicAdd
+      const unsigned claim_m = __ballot_sync(FULLMASK, need && rpos >= rend);
+      if (claim_m && !exhausted) {
+        const unsigned nw = __popc(claim_m);
+        const unsigned rank = __popc(claim_m & ((1u << lane) - 1u));
+        unsigned long long b = 0, run = kRun;
+        if (lane == 0) {
+          const unsigned long long cur = *(volatile unsigned long long*)sl.cursor;
+          const unsigned long long rem = cur < sl.n_pos ? sl.n_pos - cur : 0;
+          const unsigned long long fair = rem / ((unsigned long long)gridDim.x * 32 * 4);
+          run = fair >= (unsigned long long)kRun ? kRun : (fair < 1 ? 1 : fair);
+          b = atomicAdd(sl.cursor, (unsigned long long)nw * run);
+        }
+        b = __shfl_sync(FULLMASK, b, 0);
+        run = __shfl_sync(FULLMASK, run, 0);
+        if (b + (unsigned long long)nw * run >= sl.n_pos) exhausted = true;
+        if (need && rpos >= rend) {
+          const uint64_t st = b + (uint64_t)rank * run;
+          rpos = st < sl.n_pos ? st : sl.n_pos;
+          rend = st + run < sl.n_pos ? st + run : sl.n_pos;
+        }
+      }
+      if (!need || rpos >= rend) continue;
+      const uint64_t pos = rpos++;
+      idx = pos_to_index(sl, pos);
+      slot = sl.list_slot ? sl.list_slot[pos] : idx - sl.eval_first;
+      // a1: successor of the previous index of this lane's run, else unranking
+      if (idx == prev_idx + 1 && S > 1) {
+        if (sl.part_mode == ADAPTIS_PART_FULL) colex_next(cuts, S);
+        else ball_next(cuts, seed, S - 1, brem);
+      } else {
+        decode_cuts(tab.binom, tab.ball, tab.seeds, sl.group, sl.part_mode, sl.radius, S, L,
+                    idx - sl.seg_base, cuts);
+        if (sl.part_mode == ADAPTIS_PART_BALL) {
+          int used = 0;
+          for (int i = 1; i < S; ++i) {
+            const int di = cuts[i] - seed[i - 1];
+            used += di < 0 ? -di : di;
+          }
+          brem = sl.radius - used;
+        }
+      }
+      prev_idx = idx;
+      bool valid = true;
+      for (int s = 0; s < S; ++s) valid = valid && cuts[s] < cuts[s + 1];
+      if (!valid) {
+        ++n_inv;
+        if (!SEARCH) {
+          if (sl.out_status) sl.out_status[slot] = ADAPTIS_CAND_INVALID;
+          if (sl.out_makespan) sl.out_makespan[slot] = INT64_MAX;
+          if (sl.out_peak) sl.out_peak[slot] = 0;
+          if (sl.out_bubble) sl.out_bubble[slot] = 0.0f;
+        }
+        continue;
+      }
+      // a2/a3: stage sums by prefix differences, device statics
+      for (int d = 0; d < P2; ++d) { CAPD(d) = sl.cap; DYN(d) = 0; PEAK(d) = 0; FD(d) = 0; KEY(d) = kSeqInf; }
+      for (int s = 0; s < S; ++s) {
+        const int a = cuts[s], b = cuts[s + 1];
+        const int ds = dev_of(plc, p, s);
+        DUR(0, s) = (uint32_t)(PRE(kColTF, b) - PRE(kColTF, a));
+        DUR(1, s) = (uint32_t)(PRE(kColTB, b) - PRE(kColTB, a));
+        DUR(2, s) = (uint32_t)(PRE(kColTW, b) - PRE(kColTW, a));
+        const int64_t act = PRE(kColAct, b) - PRE(kColAct, a);
+        AS(s) = act + (PRE(kColStash, b) - PRE(kColStash, a));
+        ACT(s) = act;
+        CAPD(ds) -= PRE(kColWG, b) - PRE(kColWG, a);  // cap - static (cannot overflow: static >= 0)
+        const uint32_t lf = (s < S - 1 && dev_of(plc, p, s + 1) != ds) ? (uint32_t)tab.comm[b - 1] : 0u;
+        const uint32_t lb = (s > 0 && dev_of(plc, p, s - 1) != ds) ? (uint32_t)tab.comm[a - 1] : 0u;
+        LAT(s) = lf | (lb << 16);
+        CNT(s) = 0;
+      }
+      // exact lower-bound prune (search): the bound of adaptis_seg.cuh, per
+      // device d with lowest stage d: head = t_F[0, cuts[d]) + the d edge
+      // latencies; split: max(head + busy_d, head + m (F + B)_d + t_B[0, cuts[d])
+      // + latencies + t_W(stage 0)); a candidate whose (LB << bits | index)
+      // exceeds the incumbent key cannot win
+      if (SEARCH && sl.prune) {
+        int64_t lk = 0, lb = 0;
+        const int64_t w0 = DUR(2, 0);
+        for (int d = 0; d < p; ++d) {
+          if (d >= 1) lk += (int64_t)tab.comm[cuts[d] - 1];
+          int64_t busy = 0, wsum = 0;
+#pragma unroll
+          for (int c = 0; c < V; ++c) {
+            const int s = stage_of(plc, p, c, d);
+            busy += (int64_t)m * ((int64_t)DUR(0, s) + DUR(1, s) + DUR(2, s));
+            wsum += DUR(2, s);
+          }
+          const int64_t head = PRE(kColTF, cuts[d]) + lk;
+          int64_t lbd = busy + head;
+          const int64_t alt = busy - (int64_t)m * wsum + head + PRE(kColTB, cuts[d]) + lk + w0;
+          lbd = alt > lbd ? alt : lbd;
+          lb = lbd > lb ? lbd : lb;
+        }
+        const unsigned long long inc = *(volatile unsigned long long*)sl.key;
+        if ((((unsigned long long)lb << sl.key_bits) | idx) > inc) { ++n_pr; continue; }
+      }
+      for (int d = 0; d < p; ++d) decide(d, 0u);
+      have = true;
+    }
+    if (!__any_sync(FULLMASK, have)) break;
+
+    // ---- a5: the event loop, one committed task per step (all lanes in lockstep)
+    bool alive = have, stuck = false, overflow = false;
+    for (int t = 0; t < T; ++t) {
+      if (alive) {
+        uint32_t kmin = KEY(0);
+#pragma unroll
+        for (int d = 1; d < P2; ++d) kmin = min(kmin, KEY(d));
+        if (kmin == kSeqInf) {
+          stuck = true;  // tasks remain but no device can ever act (R14: stuck)
+          alive = false;
+        } else {
+          const int d = (int)(kmin & 15u);
+          const uint32_t at = kmin >> 4;
+          const uint32_t dec = FD(d) & 15u;
+          const int kind = (int)(dec & 3u), c = (int)(dec >> 2);
+          const int s = stage_of(plc, p, c, d);
+          const uint32_t cnt = CNT(s);
+          const uint32_t j = (cnt >> (8 * kind)) & 255u;
+          const uint32_t fin = at + DUR(kind, s);
+          FD(d) = fin << 4;
+          CNT(s) = cnt + (1u << (8 * kind));
+          // R16: act + stash at F start; act freed at B end, stash at W end
+          const int64_t as = AS(s), ac = ACT(s);
+          const int64_t dy = DYN(d) + (kind == 0 ? as : (kind == 1 ? -ac : ac - as));
+          DYN(d) = dy;
+          if (!SEARCH && kind == 0 && dy > PEAK(d)) PEAK(d) = dy;
+          // the output item: F(s, j) -> F(s+1, j), B(s, j) -> B(s-1, j)
+          const int tg = kind == 0 ? (s < S - 1 ? s + 1 : -1) : (kind == 1 ? s - 1 : -1);
+          int d2 = -1;
+          if (tg >= 0) {
+            const uint32_t lat = kind == 0 ? (LAT(s) & 0xffffu) : (LAT(s) >> 16);
+            const int row = (kind == 0 ? lay.rf : lay.rb) + (int)(j & (kSeqK - 1)) * S + tg;
+            if (j >= (uint32_t)kSeqK) {
+              // the slot's previous item j-K must be consumed or already arrived
+              const uint32_t consumed = (CNT(tg) >> (8 * kind)) & 255u;
+              if (consumed <= j - kSeqK && R32(row) > at) { overflow = true; alive = false; }
+            }
+            R32(row) = fin + lat;
+            d2 = dev_of(plc, p, tg);
+          }
+          if (alive) {
+            decide(d, at);
+            if (d2 >= 0 && d2 != d) decide(d2, at);
+          }
+        }
+      }
+    }
+    // ---- a6/a7: metrics, argmin key or SoA results
+    if (have) {
+      if (overflow) {
+        const unsigned k = atomicAdd(sl.overflow_count, 1u);
+        if (k < sl.overflow_cap) sl.overflow_idx[k] = sl.list_slot ? slot : idx;
+      } else {
+        n_tasks += stuck ? 0 : (unsigned long long)T;
+        uint32_t mk = 0;
+        for (int d = 0; d < p; ++d) mk = max(mk, FD(d) >> 4);
+        if (SEARCH) {
+          if (!stuck) {
+            const unsigned long long key = ((unsigned long long)mk << sl.key_bits) | idx;
+            if (key < best_key) {
+              best_key = key;
+              if (sl.prune) atomicMin(sl.key, key);  // share the incumbent at once
+            }
+          }
+        } else {
+          int64_t mmax = 0;
+          double busy = 0;
+          for (int d = 0; d < p; ++d) {
+            const int64_t md = (sl.cap - CAPD(d)) + PEAK(d);
+            mmax = md > mmax ? md : mmax;
+          }
+          for (int s = 0; s < S; ++s) busy += (double)m * ((double)DUR(0, s) + DUR(1, s) + DUR(2, s));
+          if (sl.out_status) sl.out_status[slot] = stuck ? ADAPTIS_CAND_STUCK : ADAPTIS_CAND_OK;
+          if (sl.out_makespan) sl.out_makespan[slot] = stuck ? INT64_MAX : (int64_t)mk;
+          if (sl.out_makespan_f32) sl.out_makespan_f32[slot] = stuck ? INFINITY : (float)mk;
+          if (sl.out_peak) sl.out_peak[slot] = stuck ? 0 : mmax;
+          if (sl.out_bubble)
+            sl.out_bubble[slot] = stuck ? 0.0f : (float)(1.0 - busy / ((double)p * (double)mk));
+        }
+      }
+    }
+  }
+#undef R32
+#undef R64
+#undef KEY
+#undef FD
+#undef CNT
+#undef DUR
+#undef LAT
+#undef RF
+#undef RB
+#undef DYN
+#undef CAPD
+#undef PEAK
+#undef AS
+#undef ACT
+  // warp reductions of the key and the counters
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(FULLMASK, best_key, o);
+    best_key = x < best_key ? x : best_key;
+    n_inv += __shfl_xor_sync(FULLMASK, n_inv, o);
+    n_pr += __shfl_xor_sync(FULLMASK, n_pr, o);
+    n_tasks += __shfl_xor_sync(FULLMASK, n_tasks, o);
+  }
+  if (lane == 0) {
+    if (SEARCH && best_key != (~0ull >> 1)) atomicMin(sl.key, best_key);
+    if (n_inv) atomicAdd(sl.n_invalid, n_inv);
+    if (n_pr) atomicAdd(sl.n_pruned, n_pr);
+    if (n_tasks) atomicAdd(sl.n_tasks, n_tasks);
+  }
+}
+
+using SeqFn = void (*)(const DevTables, const SegLaunch);
+
+template <int V, bool SEARCH>
+static SeqFn pick_p2(int p2) {
+  switch (p2) {
+    case 2: return seqg_kernel<V, 2, SEARCH>;
+    case 4: return seqg_kernel<V, 4, SEARCH>;
+    case 8: return seqg_kernel<V, 8, SEARCH>;
+    default: return seqg_kernel<V, 16, SEARCH>;
+  }
+}
+template <bool SEARCH>
+static SeqFn pick_v(int v, int p2) {
+  switch (v) {
+    case 1: return pick_p2<1, SEARCH>(p2);
+    case 2: return pick_p2<2, SEARCH>(p2);
+    case 3: return pick_p2<3, SEARCH>(p2);
+    default: return pick_p2<4, SEARCH>(p2);
+  }
+}
+
+// the sequential kernel needs int32 ticks with makespans < 2^28 (key at << 4 | d),
+// m <= 255 (8-bit counters), latencies < 2^16, 2 <= p <= 16, and a plain
+// position range (no explicit plans, lists or traces; the fallback re-run
+// keeps the global-ring kernel); `min_warps` warps of state per SM
+bool seqg_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int min_warps) {
+  if (!seq_ok || s.policy != ADAPTIS_GREEDY || s.tick != kTickI32 || s.trace || s.list_cuts ||
+      s.list_tasks || s.out_report || s.p < 2 || s.p > 16 || s.m > 255 || s.v < 1 || s.v > 4)
+    return false;
+  const size_t per_warp = seqg_smem_bytes(s.S, s.p);
+  return per_warp <= (size_t)max_smem && (size_t)min_warps * per_warp <= (size_t)228 * 1024;
+}
+
+int launch_seqg(const DevTables& t, const SegLaunch& s, int num_sms, void* stream) {
+  SeqFn f = s.key ? pick_v<true>(s.v, s.p2) : pick_v<false>(s.v, s.p2);
+  const size_t sm = seqg_smem_bytes(s.S, s.p);
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return (int)e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 32, sm);
+  if (e != cudaSuccess) return (int)e;
+  if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
+  unsigned grid = (unsigned)num_sms * (unsigned)per_sm;
+  const uint64_t warps_needed = (s.n_pos + 31) / 32;
+  if (warps_needed < grid) grid = (unsigned)(warps_needed ? warps_needed : 1);
+  f<<<grid, 32, sm, (cudaStream_t)stream>>>(t, s);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace adaptis

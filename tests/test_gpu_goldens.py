@@ -20,7 +20,10 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def golden_argmin(cid, tag=""):
-    with open(os.path.join(GOLDEN, "argmin_cfg%d%s.json" % (cid, tag))) as f:
+    path = os.path.join(GOLDEN, "argmin_cfg%d%s.json" % (cid, tag))
+    if not os.path.exists(path):
+        pytest.skip("no oracle golden %s (run tools/oracle_argmin.py)" % os.path.basename(path))
+    with open(path) as f:
         return json.load(f)
 
 
@@ -106,7 +109,7 @@ def test_whole_shard_fallback_counts_once(ctx, monkeypatch):
     b = ctx.search(pr, sp)
     assert (b["index"], b["makespan"]) == (g["index"], g["makespan"])
     assert b["n_invalid"] == g["n_invalid"]
-    assert max(li["fallback"] for li in ctx.launch_info) > (1 << 20)
+    assert max(li["fallback"] for li in ctx.launch_info()) > (1 << 20)
 
 
 def test_uniform_sample_parity_cfg3_ring2(ctx, monkeypatch):
@@ -115,7 +118,12 @@ def test_uniform_sample_parity_cfg3_ring2(ctx, monkeypatch):
     monkeypatch.setenv("ADAPTIS_RING_K", "2")
     pr, sp = W.config(3)
     N = O.space_size(pr, sp)
-    idx = np.random.default_rng(777).integers(0, N, 20_000).astype(np.uint64)
+    # uniform indices are mostly far from the seed (unbalanced, often over the
+    # cap); the block around the oracle's winner holds balanced ZB candidates
+    # whose dependency lag overflows two ring slots
+    w = golden_argmin(3)["index"]
+    idx = np.concatenate([np.random.default_rng(777).integers(0, N, 10_000),
+                          np.arange(w - 5000, w + 5000)]).astype(np.uint64)
     before = ctx.fallback_count
     got = ctx.prepare(pr, sp).eval_indices(idx)
     _compare(got, O.eval_indices(pr, sp, idx), "cfg3 uniform K=2")
