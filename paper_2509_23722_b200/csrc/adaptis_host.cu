@@ -96,8 +96,17 @@ struct adaptis_ctx {
   size_t overflow_cap = 0;
   int64_t* d_gring = nullptr;
   size_t gring_bytes = 0;
-  int64_t* d_report = nullptr;
+  int64_t* d_report = nullptr;  // winner report rows [5][MAX_P], then the winner's SoA block
+  unsigned char* h_report = nullptr;  // pinned host copy of d_report (one D2H per search)
+  TraceEntry* d_wtrace = nullptr;  // winner traces (R29), grown as needed
+  int* d_wtrace_n = nullptr;
+  size_t wtrace_entries = 0;
 };
+
+// winner report block behind the five report rows: makespan, peak, fp32
+// makespan, bubble, status (one allocation and one D2H per search)
+constexpr size_t kReportBytes = 5 * ADAPTIS_MAX_P * 8;
+constexpr size_t kWinBytes = 32;
 
 namespace {
 
@@ -398,7 +407,9 @@ adaptis_status ensure_scratch(adaptis_ctx* ctx, size_t words, size_t overflow_ca
     CU(ctx, cudaMalloc(&ctx->d_overflow, overflow_cap * 8));
     ctx->overflow_cap = overflow_cap;
   }
-  if (!ctx->d_report) CU(ctx, cudaMalloc(&ctx->d_report, 5 * ADAPTIS_MAX_P * 8));
+  if (!ctx->d_report) CU(ctx, cudaMalloc(&ctx->d_report, kReportBytes + kWinBytes));
+  if (!ctx->h_report) CU(ctx, cudaMallocHost(&ctx->h_report, kReportBytes + kWinBytes));
+  if (!ctx->d_wtrace_n) CU(ctx, cudaMalloc(&ctx->d_wtrace_n, ADAPTIS_MAX_P * sizeof(int)));
   return ADAPTIS_OK;
 }
 
@@ -990,6 +1001,7 @@ void adaptis_ctx_destroy(adaptis_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_scratch); cudaFree(c->d_overflow); cudaFree(c->d_gring); cudaFree(c->d_report);
+  cudaFreeHost(c->h_report); cudaFree(c->d_wtrace); cudaFree(c->d_wtrace_n);
   for (cudaEvent_t e : c->seg_events) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -1172,22 +1184,27 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
   const uint64_t idx = key & ((1ull << P->key_bits) - 1);
   out->index = idx;
   fill_plan(*P, idx, &out->plan, nullptr);
-  // winner report: the same kernel on the single winning index
-  std::vector<int64_t> rep(5 * P->p, 0);
-  int64_t mk = 0, pk = 0; float bub = 0, mkf = 0; uint8_t stt = 0;
-  int64_t *dmk = nullptr, *dpk = nullptr; float *dbub = nullptr, *dmkf = nullptr; uint8_t* dst = nullptr;
-  CU(ctx, cudaMalloc(&dmk, 8)); CU(ctx, cudaMalloc(&dpk, 8)); CU(ctx, cudaMalloc(&dbub, 4));
-  CU(ctx, cudaMalloc(&dst, 1)); CU(ctx, cudaMalloc(&dmkf, 4));
-  CU(ctx, cudaMemsetAsync(ctx->d_report, 0, 5 * ADAPTIS_MAX_P * 8, ctx->stream));
-  adaptis_results_soa so{dmk, dpk, dbub, dst, dmkf};
+  // winner report: the same kernel on the single winning index; its buffers
+  // are the context's (no allocation per search), read back with one D2H
+  unsigned char* wb = reinterpret_cast<unsigned char*>(ctx->d_report) + kReportBytes;
+  CU(ctx, cudaMemsetAsync(ctx->d_report, 0, kReportBytes + kWinBytes, ctx->stream));
+  adaptis_results_soa so{reinterpret_cast<int64_t*>(wb), reinterpret_cast<int64_t*>(wb + 8),
+                         reinterpret_cast<float*>(wb + 20), wb + 24, reinterpret_cast<float*>(wb + 16)};
   // with integer ticks the winner is re-run with its device traces for the
   // communication accounting of R29 (comm, exposed, overlap, bubble per device)
   TraceBuf tb;
   const bool account = P->tick != kTickF32;
   if (account) {
     tb.cap = 3 * P->m * out->plan.v;
-    CU(ctx, cudaMalloc(&tb.trace, (size_t)P->p * tb.cap * sizeof(TraceEntry)));
-    CU(ctx, cudaMalloc(&tb.trace_n, (size_t)P->p * sizeof(int)));
+    const size_t need = (size_t)P->p * tb.cap;
+    if (need > ctx->wtrace_entries) {
+      cudaFree(ctx->d_wtrace);
+      ctx->d_wtrace = nullptr;
+      CU(ctx, cudaMalloc(&ctx->d_wtrace, need * sizeof(TraceEntry)));
+      ctx->wtrace_entries = need;
+    }
+    tb.trace = ctx->d_wtrace;
+    tb.trace_n = ctx->d_wtrace_n;
     CU(ctx, cudaMemsetAsync(tb.trace_n, 0, (size_t)P->p * sizeof(int), ctx->stream));
   }
   st = run_range(ctx, P, idx, idx + 1, false, 0, 1, &so, idx, ctx->d_report, nullptr, false,
@@ -1197,18 +1214,19 @@ adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, ad
     if (e) st = fail(ctx, ADAPTIS_ECUDA, "comm accounting: %s", cudaGetErrorString((cudaError_t)e));
   }
   if (st == ADAPTIS_OK) {
-    CU(ctx, cudaMemcpyAsync(&mk, dmk, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(&pk, dpk, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(&bub, dbub, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(&stt, dst, 1, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(&mkf, dmkf, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(rep.data(), ctx->d_report, rep.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(ctx->h_report, ctx->d_report, kReportBytes + kWinBytes, cudaMemcpyDeviceToHost,
+                            ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
   }
-  cudaFree(dmk); cudaFree(dpk); cudaFree(dbub); cudaFree(dst); cudaFree(dmkf);
-  cudaFree(tb.trace); cudaFree(tb.trace_n);
   ctx->last_info = search_info;  // report the search's launches, not the re-evaluation
   if (st != ADAPTIS_OK) return st;
+  std::vector<int64_t> rep(5 * P->p, 0);
+  for (int r = 0; r < 5; ++r)
+    memcpy(rep.data() + (size_t)r * P->p, ctx->h_report + (size_t)r * P->p * 8, (size_t)P->p * 8);
+  int64_t mk, pk; float bub, mkf; uint8_t stt;
+  const unsigned char* hw = ctx->h_report + kReportBytes;
+  memcpy(&mk, hw, 8); memcpy(&pk, hw + 8, 8); memcpy(&mkf, hw + 16, 4); memcpy(&bub, hw + 20, 4);
+  stt = hw[24];
   out->result.makespan = mk;
   out->result.peak_mem_bytes = pk;
   out->result.bubble_ratio = bub;

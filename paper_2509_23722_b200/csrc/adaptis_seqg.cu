@@ -50,7 +50,7 @@ struct SeqLayout {
   int key, fd, cnt, dur, lat, rf, rb, n32;  // u32 rows
   int dyn, capd, peak, as, act, n64;        // u64 rows
 };
-ADAPTIS_LAYOUT_HD SeqLayout seq_layout(int S, int P2) {
+ADAPTIS_LAYOUT_HD SeqLayout seq_layout(int S, int P2, bool search) {
   SeqLayout l;
   int r = 0;
   l.key = r; r += P2;
@@ -64,41 +64,65 @@ ADAPTIS_LAYOUT_HD SeqLayout seq_layout(int S, int P2) {
   r = 0;
   l.dyn = r; r += P2;
   l.capd = r; r += P2;
-  l.peak = r; r += P2;
+  l.peak = r; r += search ? 0 : P2;  // per-device peaks are reported in eval mode only
   l.as = r; r += S;
   l.act = r; r += S;
   l.n64 = r;
   return l;
 }
-size_t seqg_smem_bytes(int S, int p) {
-  int P2 = 1;
-  while (P2 < p) P2 <<= 1;
-  const SeqLayout l = seq_layout(S, P2);
+size_t seqg_smem_bytes(int S, int p, bool search) {
+  const SeqLayout l = seq_layout(S, p, search);
   return (size_t)32 * (4 * l.n32 + 8 * l.n64);
 }
 
-template <int V, int P2, bool SEARCH>
+// placement of stage s = c * P + j (R12), compile-time P (a power of two)
+template <int PLC, int P>
+__device__ __forceinline__ int sq_stage(int c, int d) {
+  if constexpr (PLC == ADAPTIS_SEQ) return d;
+  else if constexpr (PLC == ADAPTIS_INTERLEAVED) return c * P + d;
+  else return c * P + ((c & 1) ? P - 1 - d : d);
+}
+template <int PLC, int P>
+__device__ __forceinline__ int sq_dev(int s) {
+  if constexpr (PLC == ADAPTIS_SEQ) return s;
+  else if constexpr (PLC == ADAPTIS_INTERLEAVED) return s & (P - 1);
+  else { const int j = s & (P - 1); return ((s / P) & 1) ? P - 1 - j : j; }
+}
+
+template <int V, int P, int PLC, bool SEARCH>
 __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const SegLaunch sl) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int S = V * P;
   const int lane = threadIdx.x & 31;
-  const int L = sl.L, p = sl.p, m = sl.m, S = V * sl.p, plc = sl.placement;
-  const SeqLayout lay = seq_layout(S, P2);
-  uint32_t* w32 = reinterpret_cast<uint32_t*>(smem);
-  int64_t* w64 = reinterpret_cast<int64_t*>(smem + (size_t)128 * lay.n32);
-#define R32(row) w32[(row) * 32 + lane]
-#define R64(row) w64[(row) * 32 + lane]
-#define KEY(d) R32(lay.key + (d))
-#define FD(d) R32(lay.fd + (d))
-#define CNT(s) R32(lay.cnt + (s))
-#define DUR(k, s) R32(lay.dur + (k) * S + (s))
-#define LAT(s) R32(lay.lat + (s))
-#define RF(k, s) R32(lay.rf + (k) * S + (s))
-#define RB(k, s) R32(lay.rb + (k) * S + (s))
-#define DYN(d) R64(lay.dyn + (d))
-#define CAPD(d) R64(lay.capd + (d))
-#define PEAK(d) R64(lay.peak + (d))
-#define AS(s) R64(lay.as + (s))
-#define ACT(s) R64(lay.act + (s))
+  const int L = sl.L, m = sl.m;
+  const SeqLayout lay = seq_layout(S, P, SEARCH);
+  // one pointer per field region (the regions are disjoint)
+  uint32_t* __restrict__ w32 = reinterpret_cast<uint32_t*>(smem);
+  int64_t* __restrict__ w64 = reinterpret_cast<int64_t*>(smem + (size_t)128 * lay.n32);
+  uint32_t* __restrict__ rKEY = w32 + lay.key * 32 + lane;
+  uint32_t* __restrict__ rFD = w32 + lay.fd * 32 + lane;
+  uint32_t* __restrict__ rCNT = w32 + lay.cnt * 32 + lane;
+  uint32_t* __restrict__ rDUR = w32 + lay.dur * 32 + lane;
+  uint32_t* __restrict__ rLAT = w32 + lay.lat * 32 + lane;
+  uint32_t* __restrict__ rRF = w32 + lay.rf * 32 + lane;
+  uint32_t* __restrict__ rRB = w32 + lay.rb * 32 + lane;
+  int64_t* __restrict__ rDYN = w64 + lay.dyn * 32 + lane;
+  int64_t* __restrict__ rCAPD = w64 + lay.capd * 32 + lane;
+  int64_t* __restrict__ rPEAK = w64 + lay.peak * 32 + lane;
+  int64_t* __restrict__ rAS = w64 + lay.as * 32 + lane;
+  int64_t* __restrict__ rACT = w64 + lay.act * 32 + lane;
+#define KEY(d) rKEY[(d) * 32]
+#define FD(d) rFD[(d) * 32]
+#define CNT(s) rCNT[(s) * 32]
+#define DUR(k, s) rDUR[((k) * S + (s)) * 32]
+#define LAT(s) rLAT[(s) * 32]
+#define RF(k, s) rRF[((k) * S + (s)) * 32]
+#define RB(k, s) rRB[((k) * S + (s)) * 32]
+#define DYN(d) rDYN[(d) * 32]
+#define CAPD(d) rCAPD[(d) * 32]
+#define PEAK(d) rPEAK[(d) * 32]
+#define AS(s) rAS[(s) * 32]
+#define ACT(s) rACT[(s) * 32]
   const int64_t* pre = tab.pre;  // [kNumCols][L + 1] prefix sums (global, read-only)
   auto PRE = [&](int col, int row) -> int64_t { return __ldg(pre + (size_t)col * (L + 1) + row); };
 
@@ -106,54 +130,42 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
   // next F of each own stage if it fits under Eq. 2, the head B whose F is
   // done, the head W whose B is done; at = max(free, earliest ready); among
   // the tasks ready by `at` the smallest (kind F < B < W, mb, stage) wins.
+  // Branch-free: every load is in bounds and selected afterwards.
   auto decide = [&](int d, uint32_t tnow) {
     const uint32_t free_t = FD(d) >> 4;
-    const int64_t dy = DYN(d), capd = CAPD(d);
-    uint32_t rf[V], rb[V], rw[V], kx[V], kbx[V], kwx[V];
+    const int64_t room = CAPD(d) - DYN(d);  // F of stage s fits iff act + stash <= room
+    uint32_t rf[V], rb[V], rw[V], gf[V], gb[V], gw[V];
     uint32_t rmin = kSeqInf;
 #pragma unroll
     for (int c = 0; c < V; ++c) {
-      const int s = stage_of(plc, p, c, d);
+      const int s = sq_stage<PLC, P>(c, d);
       const uint32_t cnt = CNT(s);
+      const uint32_t cp = CNT(s > 0 ? s - 1 : 0), cn = CNT(s < S - 1 ? s + 1 : S - 1);
       const uint32_t gF = cnt & 255u, gB = (cnt >> 8) & 255u, gW = (cnt >> 16) & 255u;
-      uint32_t r = kSeqInf;
-      if (gF < (uint32_t)m && dy + AS(s) <= capd) {
-        if (s == 0) {
-          r = 0;
-        } else {
-          const uint32_t prodF = CNT(s - 1) & 255u;  // F items produced into stage s
-          if (gF < prodF) r = (gF + kSeqK >= prodF) ? RF(gF & (kSeqK - 1), s) : tnow;
-        }
-      }
-      rf[c] = r;
-      r = kSeqInf;
-      if (gB < gF) {
-        if (s == S - 1) {
-          r = 0;
-        } else {
-          const uint32_t prodB = (CNT(s + 1) >> 8) & 255u;  // B items produced into stage s
-          if (gB < prodB) r = (gB + kSeqK >= prodB) ? RB(gB & (kSeqK - 1), s) : tnow;
-        }
-      }
-      rb[c] = r;
+      const uint32_t prodF = s == 0 ? 255u : (cp & 255u);          // F items produced into s
+      const uint32_t prodB = s == S - 1 ? 255u : ((cn >> 8) & 255u);  // B items produced into s
+      const uint32_t sF = RF(gF & (kSeqK - 1), s), sB = RB(gB & (kSeqK - 1), s);
+      const uint32_t aF = s == 0 ? 0u : (gF + kSeqK >= prodF ? sF : tnow);
+      const uint32_t aB = s == S - 1 ? 0u : (gB + kSeqK >= prodB ? sB : tnow);
+      const bool okF = gF < (uint32_t)m && gF < prodF && AS(s) <= room;
+      const bool okB = gB < gF && gB < prodB;
+      rf[c] = okF ? aF : kSeqInf;
+      rb[c] = okB ? aB : kSeqInf;
       rw[c] = gW < gB ? 0u : kSeqInf;
-      kx[c] = (gF << 2) | (uint32_t)c;
-      kbx[c] = (gB << 2) | (uint32_t)c;
-      kwx[c] = (gW << 2) | (uint32_t)c;
+      gf[c] = gF; gb[c] = gB; gw[c] = gW;
       rmin = min(rmin, min(rf[c], min(rb[c], rw[c])));
     }
-    if (rmin == kSeqInf) { KEY(d) = kSeqInf; return; }
     const uint32_t at = max(free_t, rmin);
     uint32_t kF = kSeqInf, kB = kSeqInf, kW = kSeqInf;
 #pragma unroll
     for (int c = 0; c < V; ++c) {
-      if (rf[c] <= at) kF = min(kF, kx[c]);
-      if (rb[c] <= at) kB = min(kB, kbx[c]);
-      if (rw[c] <= at) kW = min(kW, kwx[c]);
+      kF = rf[c] <= at ? min(kF, (gf[c] << 2) | (uint32_t)c) : kF;
+      kB = rb[c] <= at ? min(kB, (gb[c] << 2) | (uint32_t)c) : kB;
+      kW = rw[c] <= at ? min(kW, (gw[c] << 2) | (uint32_t)c) : kW;
     }
     const uint32_t dec = kF != kSeqInf ? ((kF & 3u) << 2)
                        : kB != kSeqInf ? (1u | ((kB & 3u) << 2)) : (2u | ((kW & 3u) << 2));
-    KEY(d) = (at << 4) | (uint32_t)d;
+    KEY(d) = rmin == kSeqInf ? kSeqInf : ((at << 4) | (uint32_t)d);
     FD(d) = (free_t << 4) | dec;
   };
 
@@ -230,10 +242,14 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
         continue;
       }
       // a2/a3: stage sums by prefix differences, device statics
-      for (int d = 0; d < P2; ++d) { CAPD(d) = sl.cap; DYN(d) = 0; PEAK(d) = 0; FD(d) = 0; KEY(d) = kSeqInf; }
+#pragma unroll
+      for (int d = 0; d < P; ++d) {
+        CAPD(d) = sl.cap; DYN(d) = 0; FD(d) = 0;
+        if (!SEARCH) PEAK(d) = 0;
+      }
       for (int s = 0; s < S; ++s) {
         const int a = cuts[s], b = cuts[s + 1];
-        const int ds = dev_of(plc, p, s);
+        const int ds = sq_dev<PLC, P>(s);
         DUR(0, s) = (uint32_t)(PRE(kColTF, b) - PRE(kColTF, a));
         DUR(1, s) = (uint32_t)(PRE(kColTB, b) - PRE(kColTB, a));
         DUR(2, s) = (uint32_t)(PRE(kColTW, b) - PRE(kColTW, a));
@@ -241,8 +257,8 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
         AS(s) = act + (PRE(kColStash, b) - PRE(kColStash, a));
         ACT(s) = act;
         CAPD(ds) -= PRE(kColWG, b) - PRE(kColWG, a);  // cap - static (cannot overflow: static >= 0)
-        const uint32_t lf = (s < S - 1 && dev_of(plc, p, s + 1) != ds) ? (uint32_t)tab.comm[b - 1] : 0u;
-        const uint32_t lb = (s > 0 && dev_of(plc, p, s - 1) != ds) ? (uint32_t)tab.comm[a - 1] : 0u;
+        const uint32_t lf = (s < S - 1 && sq_dev<PLC, P>(s + 1) != ds) ? (uint32_t)tab.comm[b - 1] : 0u;
+        const uint32_t lb = (s > 0 && sq_dev<PLC, P>(s - 1) != ds) ? (uint32_t)tab.comm[a - 1] : 0u;
         LAT(s) = lf | (lb << 16);
         CNT(s) = 0;
       }
@@ -254,12 +270,12 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
       if (SEARCH && sl.prune) {
         int64_t lk = 0, lb = 0;
         const int64_t w0 = DUR(2, 0);
-        for (int d = 0; d < p; ++d) {
+        for (int d = 0; d < P; ++d) {
           if (d >= 1) lk += (int64_t)tab.comm[cuts[d] - 1];
           int64_t busy = 0, wsum = 0;
 #pragma unroll
           for (int c = 0; c < V; ++c) {
-            const int s = stage_of(plc, p, c, d);
+            const int s = sq_stage<PLC, P>(c, d);
             busy += (int64_t)m * ((int64_t)DUR(0, s) + DUR(1, s) + DUR(2, s));
             wsum += DUR(2, s);
           }
@@ -272,7 +288,8 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
         const unsigned long long inc = *(volatile unsigned long long*)sl.key;
         if ((((unsigned long long)lb << sl.key_bits) | idx) > inc) { ++n_pr; continue; }
       }
-      for (int d = 0; d < p; ++d) decide(d, 0u);
+#pragma unroll
+      for (int d = 0; d < P; ++d) decide(d, 0u);
       have = true;
     }
     if (!__any_sync(FULLMASK, have)) break;
@@ -283,7 +300,7 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
       if (alive) {
         uint32_t kmin = KEY(0);
 #pragma unroll
-        for (int d = 1; d < P2; ++d) kmin = min(kmin, KEY(d));
+        for (int d = 1; d < P; ++d) kmin = min(kmin, KEY(d));
         if (kmin == kSeqInf) {
           stuck = true;  // tasks remain but no device can ever act (R14: stuck)
           alive = false;
@@ -292,35 +309,34 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
           const uint32_t at = kmin >> 4;
           const uint32_t dec = FD(d) & 15u;
           const int kind = (int)(dec & 3u), c = (int)(dec >> 2);
-          const int s = stage_of(plc, p, c, d);
+          const int s = sq_stage<PLC, P>(c, d);
           const uint32_t cnt = CNT(s);
-          const uint32_t j = (cnt >> (8 * kind)) & 255u;
+          const int sh = 8 * kind;
+          const uint32_t j = (cnt >> sh) & 255u;
           const uint32_t fin = at + DUR(kind, s);
-          FD(d) = fin << 4;
-          CNT(s) = cnt + (1u << (8 * kind));
           // R16: act + stash at F start; act freed at B end, stash at W end
           const int64_t as = AS(s), ac = ACT(s);
           const int64_t dy = DYN(d) + (kind == 0 ? as : (kind == 1 ? -ac : ac - as));
+          // the output item: F(s, j) -> F(s+1, j), B(s, j) -> B(s-1, j)
+          const bool out = kind == 0 ? s < S - 1 : (kind == 1 && s > 0);
+          int tg = kind == 0 ? s + 1 : s - 1;
+          tg = tg < 0 ? 0 : (tg > S - 1 ? S - 1 : tg);
+          const uint32_t latw = LAT(s);
+          const uint32_t lat = kind == 0 ? (latw & 0xffffu) : (latw >> 16);
+          uint32_t* ring = (kind == 0 ? rRF : rRB) + (((int)(j & (kSeqK - 1)) * S + tg) * 32);
+          const uint32_t old = *ring;
+          const uint32_t consumed = (CNT(tg) >> sh) & 255u;
+          // the slot's previous item j-K must be consumed or already arrived
+          const bool ovf = out && j >= (uint32_t)kSeqK && consumed + kSeqK <= j && old > at;
+          FD(d) = fin << 4;
+          CNT(s) = cnt + (1u << sh);
           DYN(d) = dy;
           if (!SEARCH && kind == 0 && dy > PEAK(d)) PEAK(d) = dy;
-          // the output item: F(s, j) -> F(s+1, j), B(s, j) -> B(s-1, j)
-          const int tg = kind == 0 ? (s < S - 1 ? s + 1 : -1) : (kind == 1 ? s - 1 : -1);
-          int d2 = -1;
-          if (tg >= 0) {
-            const uint32_t lat = kind == 0 ? (LAT(s) & 0xffffu) : (LAT(s) >> 16);
-            const int row = (kind == 0 ? lay.rf : lay.rb) + (int)(j & (kSeqK - 1)) * S + tg;
-            if (j >= (uint32_t)kSeqK) {
-              // the slot's previous item j-K must be consumed or already arrived
-              const uint32_t consumed = (CNT(tg) >> (8 * kind)) & 255u;
-              if (consumed <= j - kSeqK && R32(row) > at) { overflow = true; alive = false; }
-            }
-            R32(row) = fin + lat;
-            d2 = dev_of(plc, p, tg);
-          }
-          if (alive) {
-            decide(d, at);
-            if (d2 >= 0 && d2 != d) decide(d2, at);
-          }
+          if (out) *ring = fin + lat;
+          const int d2 = out ? sq_dev<PLC, P>(tg) : d;
+          if (ovf) { overflow = true; alive = false; }
+          decide(d, at);
+          decide(d2, at);  // the consumer (the device itself again when no output)
         }
       }
     }
@@ -332,7 +348,8 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
       } else {
         n_tasks += stuck ? 0 : (unsigned long long)T;
         uint32_t mk = 0;
-        for (int d = 0; d < p; ++d) mk = max(mk, FD(d) >> 4);
+#pragma unroll
+        for (int d = 0; d < P; ++d) mk = max(mk, FD(d) >> 4);
         if (SEARCH) {
           if (!stuck) {
             const unsigned long long key = ((unsigned long long)mk << sl.key_bits) | idx;
@@ -344,7 +361,7 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
         } else {
           int64_t mmax = 0;
           double busy = 0;
-          for (int d = 0; d < p; ++d) {
+          for (int d = 0; d < P; ++d) {
             const int64_t md = (sl.cap - CAPD(d)) + PEAK(d);
             mmax = md > mmax ? md : mmax;
           }
@@ -354,13 +371,11 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
           if (sl.out_makespan_f32) sl.out_makespan_f32[slot] = stuck ? INFINITY : (float)mk;
           if (sl.out_peak) sl.out_peak[slot] = stuck ? 0 : mmax;
           if (sl.out_bubble)
-            sl.out_bubble[slot] = stuck ? 0.0f : (float)(1.0 - busy / ((double)p * (double)mk));
+            sl.out_bubble[slot] = stuck ? 0.0f : (float)(1.0 - busy / ((double)P * (double)mk));
         }
       }
     }
   }
-#undef R32
-#undef R64
 #undef KEY
 #undef FD
 #undef CNT
@@ -391,40 +406,48 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
 
 using SeqFn = void (*)(const DevTables, const SegLaunch);
 
+template <int V, int P, bool SEARCH>
+static SeqFn pick_plc(int plc) {
+  if constexpr (V == 1) return seqg_kernel<1, P, ADAPTIS_SEQ, SEARCH>;
+  else return plc == ADAPTIS_WAVE ? seqg_kernel<V, P, ADAPTIS_WAVE, SEARCH>
+                                  : seqg_kernel<V, P, ADAPTIS_INTERLEAVED, SEARCH>;
+}
 template <int V, bool SEARCH>
-static SeqFn pick_p2(int p2) {
-  switch (p2) {
-    case 2: return seqg_kernel<V, 2, SEARCH>;
-    case 4: return seqg_kernel<V, 4, SEARCH>;
-    case 8: return seqg_kernel<V, 8, SEARCH>;
-    default: return seqg_kernel<V, 16, SEARCH>;
+static SeqFn pick_p(int p, int plc) {
+  switch (p) {
+    case 2: return pick_plc<V, 2, SEARCH>(plc);
+    case 4: return pick_plc<V, 4, SEARCH>(plc);
+    case 8: return pick_plc<V, 8, SEARCH>(plc);
+    default: return pick_plc<V, 16, SEARCH>(plc);
   }
 }
 template <bool SEARCH>
-static SeqFn pick_v(int v, int p2) {
+static SeqFn pick_v(int v, int p, int plc) {
   switch (v) {
-    case 1: return pick_p2<1, SEARCH>(p2);
-    case 2: return pick_p2<2, SEARCH>(p2);
-    case 3: return pick_p2<3, SEARCH>(p2);
-    default: return pick_p2<4, SEARCH>(p2);
+    case 1: return pick_p<1, SEARCH>(p, plc);
+    case 2: return pick_p<2, SEARCH>(p, plc);
+    case 3: return pick_p<3, SEARCH>(p, plc);
+    default: return pick_p<4, SEARCH>(p, plc);
   }
 }
 
 // the sequential kernel needs int32 ticks with makespans < 2^28 (key at << 4 | d),
-// m <= 255 (8-bit counters), latencies < 2^16, 2 <= p <= 16, and a plain
-// position range (no explicit plans, lists or traces; the fallback re-run
-// keeps the global-ring kernel); `min_warps` warps of state per SM
+// m <= 255 (8-bit counters), latencies < 2^16, p in {2, 4, 8, 16} (compile-time
+// placement arithmetic), and a plain position range (no explicit plans,
+// lists or traces; the fallback re-run keeps the global-ring kernel), with
+// `min_warps` warps of state per SM
 bool seqg_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int min_warps) {
   if (!seq_ok || s.policy != ADAPTIS_GREEDY || s.tick != kTickI32 || s.trace || s.list_cuts ||
-      s.list_tasks || s.out_report || s.p < 2 || s.p > 16 || s.m > 255 || s.v < 1 || s.v > 4)
+      s.list_tasks || s.out_report || s.m > 255 || s.v < 1 || s.v > 4 ||
+      (s.p != 2 && s.p != 4 && s.p != 8 && s.p != 16))
     return false;
-  const size_t per_warp = seqg_smem_bytes(s.S, s.p);
+  const size_t per_warp = seqg_smem_bytes(s.S, s.p, s.key != nullptr);
   return per_warp <= (size_t)max_smem && (size_t)min_warps * per_warp <= (size_t)228 * 1024;
 }
 
 int launch_seqg(const DevTables& t, const SegLaunch& s, int num_sms, void* stream) {
-  SeqFn f = s.key ? pick_v<true>(s.v, s.p2) : pick_v<false>(s.v, s.p2);
-  const size_t sm = seqg_smem_bytes(s.S, s.p);
+  SeqFn f = s.key ? pick_v<true>(s.v, s.p, s.placement) : pick_v<false>(s.v, s.p, s.placement);
+  const size_t sm = seqg_smem_bytes(s.S, s.p, s.key != nullptr);
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return (int)e;
   int per_sm = 0;
