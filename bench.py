@@ -254,7 +254,7 @@ def main():
         kern_ms.append(best["kernel_ms"])
         n_invalid = best["n_invalid"]
         for li in ctx.launch_info():
-            k = (li["v"], li["placement"], li["policy"])
+            k = (li["v"], li["placement"], li["policy"], li["kernel"])
             seg_ms[k] = seg_ms.get(k, 0.0) + li["ms"]
             seg_tasks[k] = seg_tasks.get(k, 0) + li["tasks"]
             seg_n[k] = seg_n.get(k, 0) + 1
@@ -455,12 +455,15 @@ POLICY = {0: "GPIPE", 1: "ONEF1B", 2: "ZB", 3: "GREEDY"}
 PLACEMENT = {0: "SEQ", 1: "INT", 2: "WAVE"}
 
 
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r2_dominant_traffic.json")
+
+
 def measured_traffic(config_id, kernel):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set
-    full capture (profiles/r1_dominant_traffic.json), when it is this config's
+    full capture (profiles/r2_dominant_traffic.json), when it is this config's
     same kernel; None otherwise (the contract's null)."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r1_dominant_traffic.json")))
+        t = json.load(open(TRAFFIC_FILE))
     except Exception:  # noqa: BLE001
         return None
     if t.get("config_id") != config_id or t.get("kernel") != kernel:
@@ -491,16 +494,17 @@ def roofline(seg_ms, seg_tasks, seg_n, config_id=None):
     ach = ALG_INSTR_PER_TASK * tasks / (per_launch_ms / 1e3) / 1e12
     tot_ms, tot_tasks = sum(seg_ms.values()), sum(seg_tasks.values())
     allk = ALG_INSTR_PER_TASK * tot_tasks / (tot_ms / 1e3) / 1e12
-    out.update(achieved=ach, frac=ach / peak,
-               kernel="seg_kernel<%s, v=%d> (%s placement)" % (POLICY[k[2]], k[0], PLACEMENT[k[1]]),
+    name = "seqg_kernel<v=%d, %s>" % (k[0], PLACEMENT[k[1]]) if k[3] == 1 else \
+        "seg_kernel<%s, v=%d> (%s placement)" % (POLICY[k[2]], k[0], PLACEMENT[k[1]])
+    out.update(achieved=ach, frac=ach / peak, kernel=name,
                kernel_share_of_step=seg_ms[k] / tot_ms, tasks_per_launch=tasks,
                launch_ms=per_launch_ms, all_kernels_achieved=allk, all_kernels_frac=allk / peak,
                note="algorithmic work = 16 SASS lane-instr per simulated task (int64 form, SURVEY §8d)")
     out["traffic"] = measured_traffic(config_id, out["kernel"])
     if out["traffic"] is not None:
         out["traffic_note"] = ("dram read+write bytes per launch, ncu --set full "
-                               "(profiles/r1_dominant_traffic.json): the global GREEDY rings' "
-                               "evictions; algorithmic bytes are ~0 (ALU bound)")
+                               "(profiles/r2_dominant_traffic.json); algorithmic bytes are ~0 "
+                               "(ALU bound: inputs L2/smem-resident, search writes 8 B per warp)")
     return out
 
 

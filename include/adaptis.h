@@ -382,18 +382,26 @@ ADAPTIS_API adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared
                                               const adaptis_plan* plans, uint64_t n,
                                               const adaptis_results_soa* out, int64_t* report);
 
-/* Pipeline Generator (§4.3; reading R28 in DESIGN.md): seeds from the
- * baseline partitions (S-1F1B equal-layer and Mist min-max, R20), placements
- * (S-1F1B, I-1F1B, Hanayo) and schedules (S-1F1B, ZB) of P:346, then rounds of
- * phase-by-phase tuning with rollback: partition (the exact
- * best of the L1 ball of radius `radius` around the current cuts, one GPU
- * search), placement (grouped stage-device permutations and v changes)
- * and schedule (every policy of R12), each accepted only if it
- * strictly lowers the makespan, until a round changes nothing. */
+/* Pipeline Generator (§4.3; readings R28 / R28' in DESIGN.md): seeds
+ * from the baseline partitions (S-1F1B equal-layer and Mist min-max, R20),
+ * placements (S-1F1B, I-1F1B, Hanayo) and schedules (S-1F1B, ZB) of P:346, then
+ * rounds of phase-by-phase tuning with rollback, each step accepted
+ * only if it strictly lowers the makespan, until a round changes nothing.
+ * ADAPTIS_GEN_BOTTLENECK (R28', default): each round tunes the bottleneck phase
+ * first (the partition when the spread of BubbleTime(d) is at least the
+ * largest stage cost C_s; else placement, schedule, partition); the
+ * partition phase transfers one layer at a time from the stage of the device
+ * with the lowest bubble ratio to that of the highest while it helps,
+ * else takes the best of the L1 ball of radius `radius` (one GPU search);
+ * placement and partition changes re-tune the schedule in tandem (the
+ * best policy R12 admits). ADAPTIS_GEN_ROUND_ROBIN (R28, round 1): partition
+ * (ball), placement, schedule in every round. */
+enum { ADAPTIS_GEN_BOTTLENECK = 0, ADAPTIS_GEN_ROUND_ROBIN = 1 };
 typedef struct {
   uint32_t vs_mask;          /* bit v-1 admits v virtual stages per device; 0 = {1, 2}        */
   int32_t  radius;           /* partition-phase L1 radius, >= 1; 0 = 2                        */
   int32_t  max_rounds;       /* tuning rounds, >= 1; 0 = 32                                   */
+  int32_t  mode;             /* ADAPTIS_GEN_BOTTLENECK (0) or ADAPTIS_GEN_ROUND_ROBIN         */
 } adaptis_gen_options;
 
 #define ADAPTIS_GEN_MAX_STEPS 128

@@ -84,7 +84,8 @@ class _Best(C.Structure):
 
 
 class _GenOptions(C.Structure):
-    _fields_ = [("vs_mask", C.c_uint32), ("radius", C.c_int32), ("max_rounds", C.c_int32)]
+    _fields_ = [("vs_mask", C.c_uint32), ("radius", C.c_int32), ("max_rounds", C.c_int32),
+                ("mode", C.c_int32)]
 
 
 GEN_MAX_STEPS = 128
@@ -421,10 +422,12 @@ class Context:
         st = lib().adaptis_search(self.ptr, C.byref(m.problem), C.byref(m.space), C.byref(b))
         return _best_dict(b, st, self.ptr)
 
-    def generate(self, pr: W.Problem, vs_mask: int = 0, radius: int = 0, max_rounds: int = 0) -> dict:
-        """adaptis_generate: the Pipeline Generator (R28) on this GPU."""
+    def generate(self, pr: W.Problem, vs_mask: int = 0, radius: int = 0, max_rounds: int = 0,
+                 mode: str = "bottleneck") -> dict:
+        """adaptis_generate: the Pipeline Generator (R28' / R28) on this GPU."""
         m = _Marshal(pr)
-        o = _GenOptions(vs_mask=vs_mask, radius=radius, max_rounds=max_rounds)
+        o = _GenOptions(vs_mask=vs_mask, radius=radius, max_rounds=max_rounds,
+                        mode={"bottleneck": 0, "round-robin": 1}[mode])
         r = _GenResult()
         st = lib().adaptis_generate(self.ptr, C.byref(m.problem), C.byref(o), C.byref(r))
         if st not in (OK, EINFEASIBLE):

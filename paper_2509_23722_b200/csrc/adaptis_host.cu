@@ -56,7 +56,7 @@ struct adaptis_prepared {
   uint64_t N = 0;
   int key_bits = 1;
   int tick = kTickI32;
-  bool seq_ok = false;  // sequential GREEDY kernel admitted: U < 2^28, latencies < 2^16
+  bool seq_ok = false;  // sequential kernels admitted: U < 2^28, latencies < 2^16
   std::vector<uint64_t> h_binom, h_ball;
   std::vector<int16_t> h_seeds;
   std::vector<int64_t> h_cols, h_comm;  // host copies of the layer columns (kNumCols x L) and comm
@@ -320,12 +320,12 @@ adaptis_status build_space(adaptis_ctx* ctx, const adaptis_problem* pr, const ad
     return fail(ctx, ADAPTIS_EOVERFLOW, "makespan bound and %d index bits exceed the 63-bit key", bits);
   P->tick = U >= ((unsigned __int128)1 << 31) - 1 ? kTickI64 : kTickI32;
   if (getenv("ADAPTIS_FORCE_INT64")) P->tick = kTickI64;  // test hook: exercise the int64 path
-  // the sequential GREEDY kernel packs (at << 4 | device) into 32 bits and
+  // the sequential kernels pack (at << 4 | device) into 32 bits and
   // both latencies of a stage into one word
   bool lat16 = true;
   for (int l = 0; l + 1 < Ly.L; ++l) lat16 = lat16 && Ly.comm_ticks[l] < (1 << 16);
   P->seq_ok = P->tick == kTickI32 && U < ((unsigned __int128)1 << 28) && lat16 &&
-              !getenv("ADAPTIS_NO_SEQG");
+              !getenv("ADAPTIS_NO_SEQ");
   return ADAPTIS_OK;
 }
 
@@ -450,11 +450,12 @@ int ring_slots(int policy, int m) {
   while (pw < k) pw <<= 1;
   return pw;
 }
-// warps of sequential-GREEDY state an SM must hold for that kernel to be used
-// (below, the lane-per-device kernel keeps more candidates in flight)
-int seqg_min_warps() {
-  static const int w = getenv("ADAPTIS_SEQG_MINW") ? atoi(getenv("ADAPTIS_SEQG_MINW")) : 4;
-  return w;
+// warps of sequential-kernel state an SM must hold for that kernel to be used
+// (below, the lane-per-device kernel keeps more candidates in flight; measured
+// on B200); ADAPTIS_SEQ_MINW overrides, ADAPTIS_NO_SEQ disables
+int seq_min_warps() {
+  const char* e = getenv("ADAPTIS_SEQ_MINW");
+  return e ? atoi(e) : 5;
 }
 constexpr uint64_t kSeedPass = 4096;  // indices per segment in the pruned search's seed pass
 constexpr size_t kHdr = 8;  // [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds [5] pruned
@@ -581,7 +582,7 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
                   s.L, s.S, smem_bytes(s, true), ctx->max_smem);
     CU(ctx, cudaEventRecord(ctx->seg_events[2 * i], ctx->stream));
     int e;
-    if (seqg_eligible(s, P->seq_ok, ctx->max_smem, seqg_min_warps())) {
+    if (seqg_eligible(s, P->seq_ok, ctx->max_smem, seq_min_warps())) {
       // GREEDY as one exact event loop per thread (adaptis_seqg.cu); ring
       // overflows go to the global-ring fallback below like the fast path's
       jobs[i].info.kernel = 1;
@@ -1753,6 +1754,8 @@ adaptis_status adaptis_generate(adaptis_ctx* ctx, const adaptis_problem* problem
   const uint32_t vs_mask = o.vs_mask ? o.vs_mask : 0x3u;
   const int R = o.radius ? o.radius : 2;
   const int max_rounds = o.max_rounds ? o.max_rounds : 32;
+  if (o.mode != ADAPTIS_GEN_BOTTLENECK && o.mode != ADAPTIS_GEN_ROUND_ROBIN)
+    return fail(ctx, ADAPTIS_EINVAL, "options.mode = %d is not ADAPTIS_GEN_BOTTLENECK or ADAPTIS_GEN_ROUND_ROBIN", o.mode);
   if (R < 1 || R > kMaxRadius) return fail(ctx, ADAPTIS_EINVAL, "options.radius = %d not in [1, %d]", R, kMaxRadius);
   if (max_rounds < 1) return fail(ctx, ADAPTIS_EINVAL, "options.max_rounds = %d < 1", max_rounds);
   if (vs_mask & ~0xFu) return fail(ctx, ADAPTIS_EINVAL, "options.vs_mask = 0x%x admits v > 4", vs_mask);
@@ -1843,9 +1846,167 @@ adaptis_status adaptis_generate(adaptis_ctx* ctx, const adaptis_problem* problem
   }
   adaptis_plan cur = seeds[bi];
   push_step(ADAPTIS_GEN_SEED, cur_mk);
-  // ---- tuning rounds (P:350-352)
+  // ---- tuning rounds (P:349-352)
   int rounds = 0;
-  for (; rounds < max_rounds;) {
+  // phase (a) of R28: the exact best of the L1 ball of radius R around the cuts
+  auto ball_phase = [&](bool* improved) -> adaptis_status {
+    adaptis_space sp{};
+    sp.n_groups = 1;
+    int16_t seed[ADAPTIS_MAX_S];
+    for (int i = 1; i < cur.S; ++i) seed[i - 1] = cur.cuts[i];
+    sp.group[0].v = cur.v; sp.group[0].part_mode = ADAPTIS_PART_BALL; sp.group[0].radius = R;
+    sp.group[0].seed_cuts = seed;
+    sp.group[0].combo_mask = 1u << combo_bit(cur.v, cur.placement, cur.policy);
+    adaptis_prepared* Q = nullptr;
+    adaptis_status s2 = adaptis_prepare(ctx, problem, &sp, &Q);
+    if (s2 != ADAPTIS_OK) return s2;
+    adaptis_plan best{}; int64_t bmk = INT64_MAX;
+    s2 = best_of_space(ctx, Q, &best, &bmk, &ms);
+    n_eval += Q->N;
+    adaptis_prepared_free(Q);
+    if (s2 != ADAPTIS_OK && s2 != ADAPTIS_EINFEASIBLE) return s2;
+    if (s2 == ADAPTIS_OK && bmk < cur_mk) {
+      cur = best; cur_mk = bmk; *improved = true;
+      push_step(ADAPTIS_GEN_PARTITION, cur_mk);
+    }
+    return ADAPTIS_OK;
+  };
+  // R28': the schedule re-tuned in tandem: the first admitted policy of
+  // smallest makespan for a partition and placement
+  auto best_policy = [&](adaptis_plan q, adaptis_plan* out_pl, int64_t* out_mk) -> adaptis_status {
+    std::vector<adaptis_plan> list;
+    for (int pol = ADAPTIS_GPIPE; pol <= ADAPTIS_GREEDY; ++pol)
+      if (combo_bit(q.v, q.placement, pol) >= 0) { q.policy = pol; list.push_back(q); }
+    int b; int64_t bm;
+    adaptis_status s2 = eval_best(list, &b, &bm);
+    if (s2 != ADAPTIS_OK) return s2;
+    *out_mk = b >= 0 ? bm : INT64_MAX;
+    if (b >= 0) *out_pl = list[b];
+    return ADAPTIS_OK;
+  };
+  // R28': BubbleTime(d) = T_d - busy_d - exposed_d (R29) and T_d of the current
+  // plan, and the largest stage cost C_s = t_F + t_B + t_W of one micro-batch
+  std::vector<int64_t> bubt(p), Td(p);
+  int64_t maxcs = 0;
+  auto profile = [&]() -> adaptis_status {
+    std::vector<int64_t> mk1, rep1; std::vector<uint8_t> st1;
+    float t = 0;
+    adaptis_status s2 = run_plans(ctx, P, &cur, 1, &mk1, nullptr, nullptr, &st1, &rep1, &t);
+    ms += t;
+    if (s2 != ADAPTIS_OK) return s2;
+    for (int d = 0; d < p; ++d) {
+      Td[d] = rep1[d];
+      bubt[d] = rep1[d] - rep1[p + d] - rep1[4 * p + d];
+    }
+    maxcs = 0;
+    for (int s2i = 0; s2i < cur.S; ++s2i) {
+      int64_t c = 0;
+      for (int l = cur.cuts[s2i]; l < cur.cuts[s2i + 1]; ++l)
+        c += P->h_cols[(size_t)kColTF * L + l] + P->h_cols[(size_t)kColTB * L + l] + P->h_cols[(size_t)kColTW * L + l];
+      maxcs = std::max(maxcs, c);
+    }
+    return ADAPTIS_OK;
+  };
+  auto spread = [&]() {
+    return *std::max_element(bubt.begin(), bubt.end()) - *std::min_element(bubt.begin(), bubt.end());
+  };
+  // R28' partition: one-layer transfers from the stage of the device with
+  // the lowest bubble ratio to that of the highest, while they help and the
+  // BubbleTime spread is >= max C_s; else the ball as the alternative adjustment
+  auto partition_phase = [&](bool* improved) -> adaptis_status {
+    bool acc = false;
+    for (;;) {
+      adaptis_status s2 = profile();
+      if (s2 != ADAPTIS_OK) return s2;
+      if (spread() < maxcs) break;
+      int lo = 0, hi = 0;  // bubble ratios compared exactly (cross products < 2^62)
+      for (int d = 1; d < p; ++d) {
+        if (bubt[d] * Td[lo] < bubt[lo] * Td[d]) lo = d;
+        if (bubt[d] * Td[hi] > bubt[hi] * Td[d]) hi = d;
+      }
+      if (lo == hi) break;
+      int bs = -1, bt = -1, bdist = 1 << 30;  // the closest (src, dst) stage pair, then the lowest
+      for (int a = 0; a < cur.S; ++a) {
+        if (host_dev_of(cur.placement, p, a) != lo) continue;
+        for (int b = 0; b < cur.S; ++b) {
+          if (host_dev_of(cur.placement, p, b) != hi) continue;
+          const int dist = a > b ? a - b : b - a;
+          if (dist < bdist) { bdist = dist; bs = a; bt = b; }
+        }
+      }
+      adaptis_plan q = cur;
+      if (bs < bt) for (int i = bs + 1; i <= bt; ++i) q.cuts[i] -= 1;
+      else for (int i = bt + 1; i <= bs; ++i) q.cuts[i] += 1;
+      bool ok = true;
+      for (int i = 0; i < q.S; ++i) ok = ok && q.cuts[i] < q.cuts[i + 1];
+      if (!ok) break;
+      adaptis_plan bp{}; int64_t bm = INT64_MAX;
+      s2 = best_policy(q, &bp, &bm);
+      if (s2 != ADAPTIS_OK) return s2;
+      if (bm >= cur_mk) break;  // rolled back
+      cur = bp; cur_mk = bm; acc = true;
+      push_step(ADAPTIS_GEN_PARTITION, cur_mk);
+    }
+    if (acc) { *improved = true; return ADAPTIS_OK; }
+    return ball_phase(improved);
+  };
+  // R28' placement: every other admitted (v, placement), cuts kept for
+  // the same v (else the Mist seed), the schedule re-tuned in tandem
+  auto placement_phase = [&](bool* improved) -> adaptis_status {
+    adaptis_plan best{}; int64_t bmk = INT64_MAX;
+    for (int v : vs) {
+      std::vector<int> pls = v == 1 ? std::vector<int>{ADAPTIS_SEQ}
+                                    : std::vector<int>{ADAPTIS_INTERLEAVED, ADAPTIS_WAVE};
+      for (int pl : pls) {
+        if (v == cur.v && pl == cur.placement) continue;
+        adaptis_plan q = make(v, pl, ADAPTIS_GREEDY);
+        if (v == cur.v) memcpy(q.cuts, cur.cuts, sizeof(q.cuts));
+        else mist(p * v, &q);
+        adaptis_plan bp{}; int64_t bm = INT64_MAX;
+        adaptis_status s2 = best_policy(q, &bp, &bm);
+        if (s2 != ADAPTIS_OK) return s2;
+        if (bm < bmk) { bmk = bm; best = bp; }
+      }
+    }
+    if (bmk < cur_mk) {
+      cur = best; cur_mk = bmk; *improved = true;
+      push_step(ADAPTIS_GEN_PLACEMENT, cur_mk);
+    }
+    return ADAPTIS_OK;
+  };
+  auto schedule_phase = [&](bool* improved) -> adaptis_status {
+    std::vector<adaptis_plan> list;
+    for (int pol = ADAPTIS_GPIPE; pol <= ADAPTIS_GREEDY; ++pol) {
+      if (pol == cur.policy || combo_bit(cur.v, cur.placement, pol) < 0) continue;
+      adaptis_plan q = cur;
+      q.policy = pol;
+      list.push_back(q);
+    }
+    if (list.empty()) return ADAPTIS_OK;
+    int b3; int64_t mk3;
+    adaptis_status s2 = eval_best(list, &b3, &mk3);
+    if (s2 != ADAPTIS_OK) return s2;
+    if (b3 >= 0 && mk3 < cur_mk) {
+      cur = list[b3]; cur_mk = mk3; *improved = true;
+      push_step(ADAPTIS_GEN_SCHEDULE, cur_mk);
+    }
+    return ADAPTIS_OK;
+  };
+  for (; o.mode == ADAPTIS_GEN_BOTTLENECK && rounds < max_rounds;) {
+    ++rounds;
+    st = profile();
+    if (st != ADAPTIS_OK) { adaptis_prepared_free(P); return st; }
+    // the bottleneck phase first, then the alternatives; one accepted step per round
+    const bool part_first = spread() >= maxcs;
+    bool improved = false;
+    for (int k = 0; k < 3 && !improved; ++k) {
+      const int ph = part_first ? k : (k + 1) % 3;  // 0 partition, 1 placement, 2 schedule
+      st = ph == 0 ? partition_phase(&improved) : ph == 1 ? placement_phase(&improved) : schedule_phase(&improved);
+      if (st != ADAPTIS_OK) { adaptis_prepared_free(P); return st; }
+    }
+    if (!improved) break;
+  }
+  for (; o.mode == ADAPTIS_GEN_ROUND_ROBIN && rounds < max_rounds;) {
     ++rounds;
     bool improved = false;
     // (a) partition: exact best of the L1 ball of radius R around the cuts

@@ -147,7 +147,6 @@ int launch_contend(const int64_t* cols, const int64_t* comm, int L, int p, int m
                    uint8_t* status, int64_t* report, unsigned long long* n_tasks, int Sm, void* stream);
 int occupancy_ctas_per_sm(const SegLaunch& s, bool fallback);
 // sequential GREEDY kernel (adaptis_seqg.cu): one thread per candidate
-size_t seqg_smem_bytes(int S, int p, bool search);
 bool seqg_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int min_warps);
 int launch_seqg(const DevTables& t, const SegLaunch& s, int num_sms, void* stream);
 size_t smem_bytes(const SegLaunch& s, bool fallback);

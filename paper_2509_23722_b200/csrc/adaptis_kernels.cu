@@ -139,4 +139,3 @@ int launch_segment(const DevTables& t, const SegLaunch& s, int num_sms, void* st
 }
 
 }  // namespace adaptis
-

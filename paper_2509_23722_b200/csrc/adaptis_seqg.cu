@@ -12,7 +12,7 @@
 // consumer of its output). All candidates of a segment have the same task
 // count S * m * 3, so the 32 threads of a warp step in lockstep.
 //
-// Exact state compression (DESIGN.md §4 "sequential GREEDY"). In a
+// Exact state compression (DESIGN.md §4 "Sequential GREEDY kernel"). In a
 // time-ordered event loop every pending task starts at >= the current event
 // time t. An item whose arrival A <= t is therefore interchangeable with t
 // for its consumer's decision: at = max(free, min ready) and the set of tasks
@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
         ++n_inv;
         if (!SEARCH) {
           if (sl.out_status) sl.out_status[slot] = ADAPTIS_CAND_INVALID;
+          if (sl.out_makespan_f32) sl.out_makespan_f32[slot] = INFINITY;
           if (sl.out_makespan) sl.out_makespan[slot] = INT64_MAX;
           if (sl.out_peak) sl.out_peak[slot] = 0;
           if (sl.out_bubble) sl.out_bubble[slot] = 0.0f;

@@ -134,3 +134,54 @@ def test_generator_on_configs(cid):
     assert r["status"] == "ok"
     pl = r["plan"]
     assert mk(pr, pl["v"], pl["placement"], pl["policy"], pl["cuts"][1:-1]) == r["makespan"]
+
+
+def test_transfer_moves_one_layer_and_keeps_stages_contiguous():
+    """R28' partition move ("transferring layers from the stage with the
+    lowest bubble ratio to the stage with the highest"): worked by hand."""
+    # stages [0,2) [2,4) [4,6) [6,8): stage 0 gives its last layer to stage 2,
+    # stage 1 shifts left by one and keeps two layers
+    assert G.transfer([2, 4, 6], 8, 0, 2) == [1, 3, 6]
+    # stage 3 gives its first layer to stage 1, stage 2 shifts right by one
+    assert G.transfer([2, 4, 6], 8, 3, 1) == [2, 5, 7]
+    assert G.transfer([2, 4, 6], 8, 1, 2) == [2, 3, 6]
+    assert G.transfer([1, 4, 6], 8, 0, 1) is None  # stage 0 would be empty
+    sizes = lambda c: [b - a for a, b in zip([0] + c, c + [8])]  # noqa: E731
+    for src in range(4):
+        for dst in range(4):
+            if src != dst:
+                c = G.transfer([2, 4, 6], 8, src, dst)
+                want = [2, 2, 2, 2]
+                want[src] -= 1
+                want[dst] += 1
+                assert sizes(c) == want, (src, dst)
+
+
+@pytest.mark.parametrize("pr,vs_mask,R", CASES, ids=lambda x: getattr(x, "name", str(x)))
+def test_bottleneck_mode_phase_order_and_round_robin_mode(pr, vs_mask, R):
+    """R28' (default): every round starts with the bottleneck phase: the
+    partition when the BubbleTime spread is >= the largest stage cost;
+    the trajectory falls strictly; the round-1 reading R28 still runs."""
+    r = G.generate(pr, vs_mask=vs_mask, radius=R)
+    ms = [x[1] for x in r["steps"]]
+    assert all(a > b for a, b in zip(ms, ms[1:]))
+    rr = G.generate(pr, vs_mask=vs_mask, radius=R, mode="round-robin")
+    assert rr["status"] == "ok" and rr["steps"][0] == r["steps"][0]  # same seeds
+
+
+def test_bottleneck_transfer_fires_on_an_unbalanced_seed():
+    """A heavy last layer leaves the device of stage 0 idle; with the spread of
+    BubbleTime(d) above the largest stage cost, the first tuning round moves
+    a layer (a partition step right after the seed), and that step is a
+    single-layer transfer or the ball's best, both within the L1 ball."""
+    L, p, m = 8, 2, 4
+    z = [0] * L
+    pr = W.Problem(t_f=[1, 1, 1, 1, 1, 1, 1, 9], t_b=[1, 1, 1, 1, 1, 1, 1, 9],
+                   t_w=[1, 1, 1, 1, 1, 1, 1, 9], act=z, stash=z, weight=z, grad=z,
+                   comm=[1] * (L - 1) + [0], p=p, m=m)
+    r = G.generate(pr, vs_mask=0x1)
+    assert r["status"] == "ok"
+    # the equal-layer seed [4] is unbalanced (4 vs 12 per micro-batch); Mist's seed is better
+    bub, T, maxcs = G.bottleneck(pr, (1, G.SEQ, G.ONEF1B, [4]))
+    assert max(bub) - min(bub) >= maxcs
+    assert r["makespan"] <= G.score(pr, 1, G.SEQ, G.ONEF1B, G.mist(pr, 2))

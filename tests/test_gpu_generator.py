@@ -1,6 +1,6 @@
 """GPU parity of the explicit-plan evaluator (adaptis_eval_plans, including the
 R29 communication accounting of its per-device report) and of the
-Pipeline Generator (adaptis_generate, reading R28) against the
+Pipeline Generator (adaptis_generate, readings R28' and R28) against the
 oracle: per-plan results and per-device reports bit-exact against
 oracle.simulate; the generator's whole trajectory (every accepted step, the
 rounds, the plans evaluated) and its final plan identical to
@@ -108,17 +108,19 @@ def same_trajectory(got, want):
     assert got["n_evaluated"] == want["n_evaluated"]
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3, 4])
-def test_generate_random_small(ctx, seed):
-    pr = small_problem(seed, L=10, p=2, m=4)
-    same_trajectory(ctx.generate(pr, radius=2), G.generate(pr, radius=2))
+@pytest.mark.parametrize("mode", ["bottleneck", "round-robin"])
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_generate_random_small(ctx, seed, mode):
+    pr = small_problem(seed, L=10 + seed % 3, p=2 + (seed % 2) * 2, m=4)
+    same_trajectory(ctx.generate(pr, radius=2, mode=mode), G.generate(pr, radius=2, mode=mode))
 
 
+@pytest.mark.parametrize("mode", ["bottleneck", "round-robin"])
 @pytest.mark.parametrize("cid", [1, 2, 3, 4])
-def test_generate_configs(ctx, cid):
+def test_generate_configs(ctx, cid, mode):
     pr, _ = W.config(cid)
-    got = ctx.generate(pr)
-    same_trajectory(got, G.generate(pr))
+    got = ctx.generate(pr, mode=mode)
+    same_trajectory(got, G.generate(pr, mode=mode))
     want = O.simulate(pr, got["plan"]["v"], got["plan"]["placement"], got["plan"]["policy"],
                       got["plan"]["cuts"][1:-1])
     assert got["T_d"] == want["T_d"] and got["M_d"] == want["M_d"]

@@ -71,11 +71,12 @@ def _random_spaces(seed, n):
 
 
 def test_forced_fallback_matches_oracle(ctx, monkeypatch):
-    """ADAPTIS_RING_K=2 makes the fixed-order fast path's shared-memory rings
+    """ADAPTIS_RING_K=2 makes the lane kernels' fixed-order shared-memory rings
     overflow on most candidates, so the exact fallback kernel (global rings of
     depth >= m, re-run from the overflow list) decides them: evaluations and
     searches still equal the oracle, and the fallback really ran."""
     monkeypatch.setenv("ADAPTIS_RING_K", "2")
+    monkeypatch.setenv("ADAPTIS_NO_SEQ", "1")  # the lane-per-device kernels and their rings
     before = ctx.fallback_count
     pr, sp = W.config(1)
     got = ctx.eval_batch(pr, sp, 0, 244)
@@ -104,6 +105,7 @@ def test_whole_shard_fallback_counts_once(ctx, monkeypatch):
     the invalid count is the oracle's exactly: the re-run's counts replace the
     first pass's for that segment instead of adding to them."""
     monkeypatch.setenv("ADAPTIS_RING_K", "2")
+    monkeypatch.setenv("ADAPTIS_NO_SEQ", "1")  # the lane-per-device kernels and their rings
     g = golden_argmin(3)
     pr, sp = W.config(3)
     b = ctx.search(pr, sp)
@@ -116,6 +118,7 @@ def test_uniform_sample_parity_cfg3_ring2(ctx, monkeypatch):
     """Seeded-uniform cfg3 indices through adaptis_eval_indices with the
     fallback forced (list-mode re-run of explicit index positions)."""
     monkeypatch.setenv("ADAPTIS_RING_K", "2")
+    monkeypatch.setenv("ADAPTIS_NO_SEQ", "1")  # the lane-per-device kernels and their rings
     pr, sp = W.config(3)
     N = O.space_size(pr, sp)
     # uniform indices are mostly far from the seed (unbalanced, often over the

@@ -1,7 +1,8 @@
 """The sequential GREEDY kernel (adaptis_seqg.cu: one exact event loop per
 thread) against the oracle, and its dispatch. GREEDY segments with int32
-ticks, 2 <= p <= 16 and m <= 255 run on it; everything it cannot hold exactly
-(K = 2 arrival slots per edge) is re-run by the global-ring kernel."""
+ticks, p in {2, 4, 8, 16}, m <= 255 whose state fits run on it; everything it
+cannot hold exactly (K = 2 arrival slots per edge) is re-run by the
+global-ring kernel."""
 import numpy as np
 import pytest
 
@@ -29,7 +30,7 @@ def _compare(got, want, where=""):
     assert np.all(np.abs(np.asarray(got["bubble"])[ok] - np.asarray(want["bubble"])[ok]) <= 1e-6)
 
 
-def test_seqg_runs_the_greedy_segments(ctx):
+def test_seq_runs_the_greedy_segments(ctx):
     pr, sp = W.config(3)
     idx = np.arange(0, O.space_size(pr, sp), 9973, dtype=np.uint64)  # every segment
     ctx.prepare(pr, sp).eval_indices(idx)
@@ -41,7 +42,7 @@ def test_seqg_runs_the_greedy_segments(ctx):
 
 
 @pytest.mark.parametrize("cid", [3, 4, 5])
-def test_seqg_greedy_blocks_equal_oracle(ctx, cid):
+def test_seq_blocks_equal_oracle(ctx, cid):
     """Every GREEDY (group, combo) segment of the config: the first 1024
     candidates (the seed neighbourhood) and a seeded random block."""
     pr, sp = W.config(cid)
@@ -63,7 +64,7 @@ def test_seqg_greedy_blocks_equal_oracle(ctx, cid):
                     cnt = min(1024 if cid != 5 else 128, N - first)
                     got = ctx.eval_batch(pr, sp, first, cnt)
                     _compare(got, O.eval_indices(pr, sp, range(first, first + cnt)),
-                             "cfg%d GREEDY v=%d combo %d @%d" % (cid, g.v, c, first))
+                             "cfg%d v=%d combo %d @%d" % (cid, g.v, c, first))
                 seen += 1
             k += n_s
         base += n_g
@@ -71,7 +72,7 @@ def test_seqg_greedy_blocks_equal_oracle(ctx, cid):
 
 
 @pytest.mark.parametrize("seed", [11, 12, 13])
-def test_seqg_random_spaces_with_overflow(ctx, seed):
+def test_seq_random_spaces_with_overflow(ctx, seed):
     """Random problems with latencies up to 200 ticks against task durations of
     1-9: many edges hold more than K future arrivals, so candidates overflow and
     are re-run by the exact global-ring kernel; results equal the oracle."""
@@ -88,12 +89,12 @@ def test_seqg_random_spaces_with_overflow(ctx, seed):
     assert ctx.fallback_count > before
 
 
-def test_lane_kernel_still_exact_when_seqg_disabled(monkeypatch):
-    """ADAPTIS_NO_SEQG=1 keeps GREEDY on the lane-per-device kernel (used for
-    int64 / fp32 ticks, p > 16, m > 255 and reports): same winner."""
+def test_lane_kernel_still_exact_when_seq_disabled(monkeypatch):
+    """ADAPTIS_NO_SEQ=1 keeps GREEDY on the lane-per-device kernel (used for
+    int64 / fp32 ticks, other p, m > 255 and reports): same winner."""
     from paper_2509_23722_b200 import adaptis as A
     from test_gpu_goldens import golden_argmin
-    monkeypatch.setenv("ADAPTIS_NO_SEQG", "1")
+    monkeypatch.setenv("ADAPTIS_NO_SEQ", "1")
     c = A.Context(0)
     try:
         pr, sp = W.config(4)
