@@ -382,6 +382,27 @@ ADAPTIS_API adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared
                                               const adaptis_plan* plans, uint64_t n,
                                               const adaptis_results_soa* out, int64_t* report);
 
+/* Memory timeline of one plan (Eq. 2; "identifies potential
+ * OOM time"; SPEC memory_timeline S:213-221; reading R35 in DESIGN.md): per
+ * device, the piecewise-constant memory M_d(t) = static + dynamic bytes as
+ * breakpoints (time, bytes) in event order, starting with (0, static):
+ * act + stash are allocated at an F's start, act freed at its B's end, stash
+ * at its W's end (at the B's end when fused, R16); per-device events are
+ * totally ordered on the device's engine (a free at t precedes an allocation
+ * at t). `plan` is a policy plan (as adaptis_eval_plans) or, with `tasks` and
+ * `offsets` (as adaptis_eval_lists, one plan), an explicit schedule. Device d's
+ * breakpoints go to out[dev_offsets[d] .. dev_offsets[d+1]) (caller arrays:
+ * dev_offsets has p + 1 entries; out holds `cap_points`, at most p (1 + 3 m v)
+ * are written, EINVAL if too small); first_violation[d] is the first time
+ * M_d exceeds the memory cap, -1 if never. A STUCK plan's timeline stops at
+ * the stall. Not in FP32 cost mode. */
+typedef struct { int64_t time, bytes; } adaptis_mem_point;
+ADAPTIS_API adaptis_status adaptis_memory_timeline(adaptis_ctx* ctx, adaptis_prepared* prep,
+                                                   const adaptis_plan* plan, const adaptis_task* tasks,
+                                                   const uint64_t* offsets, adaptis_mem_point* out,
+                                                   uint64_t cap_points, uint64_t* dev_offsets,
+                                                   int64_t* first_violation);
+
 /* Pipeline Generator (§4.3; readings R28 / R28' in DESIGN.md): seeds
  * from the baseline partitions (S-1F1B equal-layer and Mist min-max, R20),
  * placements (S-1F1B, I-1F1B, Hanayo) and schedules (S-1F1B, ZB) of P:346, then

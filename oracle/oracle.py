@@ -618,3 +618,57 @@ def tune_overlap(pr, v, placement, fused, cuts, lists, max_rounds=0):
         lists, cur = best[1], best[2]
         swaps += 1
     return lists, swaps, cur
+
+
+def memory_timeline(pr, v, placement, policy, cuts, lists=None):
+    """Reading R35 (Eq. 2, P:341-343; P:372 "identifies potential OOM time";
+    SPEC memory_timeline S:213-221): per device, the breakpoints (time, bytes)
+    of M_d(t) = static + dynamic bytes in event order, starting at (0,
+    static), with the R16 rules: act + stash allocated at an F's start, act
+    freed at its B's end, stash at its W's end (at the B's end when fused);
+    and the first time M_d exceeds the cap (-1: never). Times come from the
+    event loop's trace (policy plans) or the longest-path starts of explicit
+    lists (R30, policy 4 = LIST, 5 = LIST_FUSED). Plans that do not complete
+    (STUCK) are not covered."""
+    L, p = len(pr.t_f), pr.p
+    full = list(cuts) if (cuts and cuts[0] == 0 and cuts[-1] == L) else [0] + list(cuts) + [L]
+    S = len(full) - 1
+
+    def ssum(col, s):
+        return int(sum(int(x) for x in col[full[s]:full[s + 1]]))
+    fused = policy in (0, 1, 5)
+    dur = {0: [ssum(pr.t_f, s) for s in range(S)],
+           1: [ssum(pr.t_b, s) + (ssum(pr.t_w, s) if fused else 0) for s in range(S)],
+           2: [ssum(pr.t_w, s) for s in range(S)]}
+    act = [ssum(pr.act, s) for s in range(S)]
+    sta = [ssum(pr.stash, s) for s in range(S)]
+    wg = [ssum(pr.weight, s) + ssum(pr.grad, s) for s in range(S)]
+    dev = [device_of_stage(placement, p, v, s) for s in range(S)]
+    if lists is None:
+        r = simulate(pr, v, placement, policy, full[1:-1], trace=True)
+        if r["status"] not in (0, 2):
+            raise ValueError("plan does not complete (status %d)" % r["status"])
+        per_dev = [[(k, s, st) for (k, s, _j, st) in r["trace"][d]] for d in range(p)]
+    else:
+        lp = longest_path(pr, v, placement, full[1:-1], fused, lists)
+        if lp is None:
+            raise ValueError("cyclic wait (stuck)")
+        per_dev = [[(k, s, st) for (k, s, _j), st in zip(lists[d], lp[2][d])] for d in range(p)]
+    points, first = [], []
+    for d in range(p):
+        b = sum(wg[s] for s in range(S) if dev[s] == d)
+        pts = [(0, b)]
+        fv = 0 if b > pr.cap else -1
+        for (k, s, st) in per_dev[d]:
+            if k == 0:
+                t, b = st, b + act[s] + sta[s]
+            elif k == 1:
+                t, b = st + dur[1][s], b - act[s] - (sta[s] if fused else 0)
+            else:
+                t, b = st + dur[2][s], b - sta[s]
+            pts.append((t, b))
+            if fv < 0 and b > pr.cap:
+                fv = t
+        points.append(pts)
+        first.append(fv)
+    return {"points": points, "first_violation": first}

@@ -102,6 +102,10 @@ class _GenResult(C.Structure):
                 ("kernel_ms", C.c_float)]
 
 
+class _MemPoint(C.Structure):
+    _fields_ = [("time", C.c_int64), ("bytes", C.c_int64)]
+
+
 class _LaunchInfo(C.Structure):
     _fields_ = [("group", C.c_int32), ("combo", C.c_int32), ("v", C.c_int32),
                 ("placement", C.c_int32), ("policy", C.c_int32), ("fallback", C.c_int32),
@@ -187,6 +191,10 @@ def lib():
                                                C.POINTER(C.c_uint64), C.c_int32, C.c_void_p,
                                                C.POINTER(_Result), C.POINTER(C.c_int32),
                                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+            L.adaptis_memory_timeline.restype = st
+            L.adaptis_memory_timeline.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
+                                                  C.POINTER(C.c_uint64), C.POINTER(_MemPoint), C.c_uint64,
+                                                  C.POINTER(C.c_uint64), C.POINTER(C.c_int64)]
             L.adaptis_lower.restype = st
             L.adaptis_lower.argtypes = [C.c_int32, C.POINTER(_Plan), C.c_void_p, C.POINTER(C.c_uint64),
                                         C.c_int32, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),
@@ -558,6 +566,26 @@ class Prepared:
                for d in range(p)]
         return {"lists": rep, "moves": int(nm.value), "status": int(res.status),
                 "makespan": int(res.makespan), "peak_mem": int(res.peak_mem_bytes)}
+
+    def memory_timeline(self, plan, lists=None) -> dict:
+        """adaptis_memory_timeline (R35): per device the breakpoints (time, bytes)
+        of static + dynamic memory and the first time above the cap (-1: never)."""
+        p, m = self.m.problem.p, self.m.problem.m
+        arr = make_plans([plan])
+        cap = p * (1 + 3 * m * plan["v"])
+        out = (_MemPoint * cap)()
+        offs = (C.c_uint64 * (p + 1))()
+        first = (C.c_int64 * p)()
+        if lists is not None:
+            tasks, toffs = self._task_arrays([lists], p)
+            st = lib().adaptis_memory_timeline(self.ctx.ptr, self.ptr, arr, tasks.ctypes.data,
+                                               toffs.ctypes.data_as(C.POINTER(C.c_uint64)), out, cap,
+                                               offs, first)
+        else:
+            st = lib().adaptis_memory_timeline(self.ctx.ptr, self.ptr, arr, None, None, out, cap, offs, first)
+        _check(st, self.ctx.ptr)
+        pts = [[(int(out[i].time), int(out[i].bytes)) for i in range(offs[d], offs[d + 1])] for d in range(p)]
+        return {"points": pts, "first_violation": [int(x) for x in first]}
 
     def tune_overlap(self, plan, lists, max_swaps: int = 0) -> dict:
         """adaptis_tune_overlap (R32): the reordered lists and their result."""

@@ -786,14 +786,23 @@ adaptis_status validate_lists(adaptis_ctx* ctx, const adaptis_prepared* P, const
   return ADAPTIS_OK;
 }
 
+// memory timeline request of run_plans (R35): per (plan, device) breakpoints
+struct MemTimelineReq {
+  int pcap = 0;                          // breakpoints per (plan, device)
+  std::vector<adaptis_mem_point> points; // [n][p][pcap]
+  std::vector<int> npts;                 // [n][p]
+  std::vector<int64_t> first;            // [n][p], -1: no violation
+};
+
 adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plans,
                          uint64_t n, std::vector<int64_t>* mk, std::vector<int64_t>* peak,
                          std::vector<float>* bubble, std::vector<uint8_t>* status,
                          std::vector<int64_t>* report, float* kernel_ms,
                          const adaptis_task* tasks = nullptr, const uint64_t* offsets = nullptr,
-                         std::vector<TraceEntry>* trace_out = nullptr, int* trace_cap_out = nullptr) {
+                         std::vector<TraceEntry>* trace_out = nullptr, int* trace_cap_out = nullptr,
+                         MemTimelineReq* mt = nullptr) {
   std::vector<int64_t> rep_local;
-  if (trace_out && !report) report = &rep_local;  // the trace rides on the report launch
+  if ((trace_out || mt) && !report) report = &rep_local;  // the trace rides on the report launch
   for (uint64_t i = 0; i < n; ++i) {
     const adaptis_plan& pl = plans[i];
     if (pl.policy == ADAPTIS_LIST || pl.policy == ADAPTIS_LIST_FUSED) {
@@ -917,6 +926,37 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
   if (account) {
     const int e = launch_comm_account(tb.trace, tb.trace_n, tb.cap, P->p, n, d_rep, ctx->stream);
     if (e) { cleanup(); return fail(ctx, ADAPTIS_ECUDA, "comm accounting: %s", cudaGetErrorString((cudaError_t)e)); }
+  }
+  if (mt && account) {  // R35: the memory timeline from the same traces
+    mt->pcap = 1 + tb.cap;
+    std::vector<int32_t> info(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      const int pol = plans[i].policy;
+      const bool fused = pol == ADAPTIS_GPIPE || pol == ADAPTIS_ONEF1B || pol == ADAPTIS_LIST_FUSED;
+      info[i] = plans[i].v | (plans[i].placement << 4) | ((fused ? 1 : 0) << 8);
+    }
+    const size_t np = (size_t)n * P->p;
+    int32_t* d_info = nullptr; adaptis_mem_point* d_pts = nullptr; int* d_npts = nullptr; int64_t* d_first = nullptr;
+    auto free_mt = [&]() { cudaFree(d_info); cudaFree(d_pts); cudaFree(d_npts); cudaFree(d_first); };
+    cudaError_t ce = cudaMalloc(&d_info, n * 4);
+    if (ce == cudaSuccess) ce = cudaMalloc(&d_pts, np * mt->pcap * sizeof(adaptis_mem_point));
+    if (ce == cudaSuccess) ce = cudaMalloc(&d_npts, np * sizeof(int));
+    if (ce == cudaSuccess) ce = cudaMalloc(&d_first, np * 8);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(d_info, info.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream);
+    if (ce == cudaSuccess)
+      ce = (cudaError_t)launch_mem_timeline(tb.trace, tb.trace_n, tb.cap, P->p, n, d_cuts, d_info, P->d_pre, P->L,
+                                            P->cap, d_pts, mt->pcap, d_npts, d_first, ctx->stream);
+    mt->points.resize(np * mt->pcap);
+    mt->npts.resize(np);
+    mt->first.resize(np);
+    if (ce == cudaSuccess)
+      ce = cudaMemcpyAsync(mt->points.data(), d_pts, np * mt->pcap * sizeof(adaptis_mem_point),
+                           cudaMemcpyDeviceToHost, ctx->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(mt->npts.data(), d_npts, np * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(mt->first.data(), d_first, np * 8, cudaMemcpyDeviceToHost, ctx->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
+    free_mt();
+    if (ce != cudaSuccess) { cleanup(); return fail(ctx, ADAPTIS_ECUDA, "memory timeline: %s", cudaGetErrorString(ce)); }
   }
   CUP(cudaMemcpyAsync(mk->data(), d_mk, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   if (peak) CUP(cudaMemcpyAsync(peak->data(), d_pk, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1606,6 +1646,43 @@ adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared* P, const a
       return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: LIST policies go through adaptis_eval_lists",
                   (unsigned long long)i);
   return eval_plans_common(ctx, P, plans, n, out, report, nullptr, nullptr);
+}
+
+adaptis_status adaptis_memory_timeline(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plan,
+                                       const adaptis_task* tasks, const uint64_t* offsets, adaptis_mem_point* out,
+                                       uint64_t cap_points, uint64_t* dev_offsets, int64_t* first_violation) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!plan || !out || !dev_offsets || !first_violation) return fail(ctx, ADAPTIS_EINVAL, "a pointer argument is NULL");
+  if (P->tick == kTickF32) return fail(ctx, ADAPTIS_EINVAL, "FP32 cost mode is not supported for the memory timeline");
+  const bool lists = plan->policy == ADAPTIS_LIST || plan->policy == ADAPTIS_LIST_FUSED;
+  if (lists != (tasks != nullptr && offsets != nullptr))
+    return fail(ctx, ADAPTIS_EINVAL, "plan.policy = %d: task lists are %s", plan->policy,
+                lists ? "required (LIST policies)" : "only for LIST policies");
+  if (lists) {
+    if (plan->S != P->p * plan->v || plan->S < 1 || plan->S > ADAPTIS_MAX_S)
+      return fail(ctx, ADAPTIS_EINVAL, "plan.S = %d != p * v", plan->S);
+    adaptis_status st = validate_lists(ctx, P, plan, tasks, offsets, 1);
+    if (st != ADAPTIS_OK) return st;
+  }
+  const uint64_t need = (uint64_t)P->p * (1 + 3 * (uint64_t)P->m * plan->v);
+  if (cap_points < need)
+    return fail(ctx, ADAPTIS_EINVAL, "cap_points = %llu < p (1 + 3 m v) = %llu", (unsigned long long)cap_points,
+                (unsigned long long)need);
+  std::vector<int64_t> mk; std::vector<uint8_t> stt;
+  MemTimelineReq mt;
+  adaptis_status st = run_plans(ctx, P, plan, 1, &mk, nullptr, nullptr, &stt, nullptr, nullptr, tasks, offsets,
+                                nullptr, nullptr, &mt);
+  if (st != ADAPTIS_OK) return st;
+  if (stt[0] == ADAPTIS_CAND_INVALID) return fail(ctx, ADAPTIS_EINVAL, "plan cuts are not strictly increasing");
+  uint64_t k = 0;
+  for (int d = 0; d < P->p; ++d) {
+    dev_offsets[d] = k;
+    const int np = mt.npts[d];
+    for (int i = 0; i < np; ++i) out[k++] = mt.points[(size_t)d * mt.pcap + i];
+    first_violation[d] = mt.first[d];
+  }
+  dev_offsets[P->p] = k;
+  return ADAPTIS_OK;
 }
 
 adaptis_status adaptis_eval_lists(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plans,

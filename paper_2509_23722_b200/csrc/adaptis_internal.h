@@ -95,6 +95,8 @@ struct SegLaunch {
 struct TraceEntry {
   int64_t start, fin;
   int32_t oc, tgt;
+  int16_t kind, stage;  // the task (F 0, B 1, W 2; stage index), for the memory timeline
+  int32_t pad;
 };
 
 #ifdef __CUDACC__
@@ -138,6 +140,16 @@ int launch_comm_account(const TraceEntry* trace, const int* trace_n, int trace_c
                         uint64_t n, int64_t* report, void* stream);
 int launch_segment(const DevTables& t, const SegLaunch& s, int num_sms, void* stream,
                    bool fallback, unsigned grid_limit);
+// Memory timeline (Eq. 2; SPEC memory_timeline, R35) of n traced plans:
+// per (plan, device) the breakpoints (time, static + dynamic bytes) in event
+// order, starting at (0, static), at [(o * p + d) * pcap], their count in
+// npts[o * p + d], and the first time the bytes exceed cap (-1: none) in
+// first[o * p + d]. plan_info[o] = v | placement << 4 | fused << 8. Returns a
+// cudaError_t.
+int launch_mem_timeline(const TraceEntry* trace, const int* trace_n, int trace_cap, int p, uint64_t n,
+                        const int16_t* cuts, const int32_t* plan_info, const int64_t* pre, int L,
+                        int64_t cap, adaptis_mem_point* points, int pcap, int* npts, int64_t* first,
+                        void* stream);
 // R34 engine contention on explicit lists (adaptis_contend.cu): one warp per
 // plan slot (32 / p2 plans per warp); scratch [n][stride] int64 with stride >=
 // 5 * S * m; Sm = the largest S of the batch. Returns a cudaError_t.

@@ -138,4 +138,60 @@ int launch_segment(const DevTables& t, const SegLaunch& s, int num_sms, void* st
   return (int)cudaGetLastError();
 }
 
+// ---- memory timeline (R35): one thread per (plan, device) walks the device's
+// trace in execution order; F allocates act + stash at its start, B frees act
+// (+ stash when fused) at its end, W frees stash at its end (R16)
+__global__ void mem_timeline_kernel(const TraceEntry* __restrict__ trace, const int* __restrict__ trace_n,
+                                    int cap_t, int p, uint64_t n, const int16_t* __restrict__ cuts,
+                                    const int32_t* __restrict__ plan_info, const int64_t* __restrict__ pre,
+                                    int L, int64_t cap, adaptis_mem_point* __restrict__ points, int pcap,
+                                    int* __restrict__ npts, int64_t* __restrict__ first) {
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= n * (uint64_t)p) return;
+  const uint64_t o = gid / p;
+  const int d = (int)(gid % p);
+  const int info = plan_info[o];
+  const int v = info & 15, placement = (info >> 4) & 15;
+  const bool fused = (info >> 8) & 1;
+  const int S = p * v;
+  const int16_t* c = cuts + o * (ADAPTIS_MAX_S + 1);
+  auto col = [&](int k, int a, int b) { return pre[(size_t)k * (L + 1) + b] - pre[(size_t)k * (L + 1) + a]; };
+  int64_t stat = 0;
+  for (int s = 0; s < S; ++s)
+    if (dev_of(placement, p, s) == d) stat += col(kColWG, c[s], c[s + 1]);
+  adaptis_mem_point* out = points + gid * (size_t)pcap;
+  int k = 0;
+  int64_t bytes = stat, fv = -1;
+  out[k].time = 0; out[k].bytes = bytes; ++k;
+  if (bytes > cap) fv = 0;
+  const int nt = min(trace_n[gid], cap_t);
+  const TraceEntry* tr = trace + gid * (size_t)cap_t;
+  for (int i = 0; i < nt && k < pcap; ++i) {
+    const TraceEntry e = tr[i];
+    const int s = e.stage;
+    const int64_t act = col(kColAct, c[s], c[s + 1]), sta = col(kColStash, c[s], c[s + 1]);
+    int64_t delta, t;
+    if (e.kind == 0) { delta = act + sta; t = e.start; }
+    else if (e.kind == 1) { delta = -(act + (fused ? sta : 0)); t = e.fin; }
+    else { delta = -sta; t = e.fin; }
+    bytes += delta;
+    out[k].time = t; out[k].bytes = bytes; ++k;
+    if (fv < 0 && bytes > cap) fv = t;
+  }
+  npts[gid] = k;
+  first[gid] = fv;
+}
+
+int launch_mem_timeline(const TraceEntry* trace, const int* trace_n, int trace_cap, int p, uint64_t n,
+                        const int16_t* cuts, const int32_t* plan_info, const int64_t* pre, int L,
+                        int64_t cap, adaptis_mem_point* points, int pcap, int* npts, int64_t* first,
+                        void* stream) {
+  if (n == 0) return 0;
+  const uint64_t threads = n * (uint64_t)p;
+  const unsigned grid = (unsigned)((threads + 127) / 128);
+  mem_timeline_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(trace, trace_n, trace_cap, p, n, cuts, plan_info,
+                                                              pre, L, cap, points, pcap, npts, first);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace adaptis

@@ -414,9 +414,10 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   unsigned wrounds = 0;
   unsigned ctasks = 0, clive = 0;  // this lane's tasks / live rounds since the last flush
   int ntr = 0;                     // TRACE: tasks recorded for the slot's current candidate
-  // TRACE (report mode, R29): append a committed task [start, fin) and its output
-  // transfer (latency oc to device tdev, -1: none) to this candidate's device trace
-  auto trace_task = [&](T start, T fin, T oc, int tdev) {
+  // TRACE (report mode, R29): append a committed task [start, fin) of (kind,
+  // chunk) and its output transfer (latency oc to device tdev, -1: none) to this
+  // candidate's device trace
+  auto trace_task = [&](T start, T fin, T oc, int tdev, int kind, int chunk) {
     if constexpr (TRACE) {
       if (ntr < sl.trace_cap) {
         TraceEntry e;
@@ -424,6 +425,8 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         e.fin = to_ticks(fin);
         e.oc = (int32_t)to_ticks(oc);
         e.tgt = tdev;
+        e.kind = (int16_t)kind;
+        e.stage = (int16_t)stage_of(sl.placement, p, chunk, d);
         sl.trace[((size_t)cold.slot * p + d) * sl.trace_cap + ntr] = e;
       }
       ++ntr;
@@ -831,7 +834,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       __syncwarp();
       if (LISTP && live) {  // phase B of an explicit order (R30): W at free_t, F/B when ready
         if (tk == 2) {
-          trace_task(free_t, free_t + tr.dur, (T)0, -1);
+          trace_task(free_t, free_t + tr.dur, (T)0, -1, 2, tc);
           free_t += tr.dur;
           dyn += DMEM(2, tc);
           ++nF; ++ctasks;
@@ -847,7 +850,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
               const int s1 = tk == 0 ? s0 + 1 : s0 - 1;
               int tdev = (oaddr >= 0 && s1 >= 0 && s1 < S) ? dev_of(sl.placement, p, s1) : -1;
               if (tdev == d) tdev = -1;
-              trace_task(fin - tr.dur, fin, tdev >= 0 ? tr.oc : (T)0, tdev);
+              trace_task(fin - tr.dur, fin, tdev >= 0 ? tr.oc : (T)0, tdev, tk, tc);
             }
             free_t = fin;
             if (oaddr >= 0) ring[oaddr] = fin + tr.oc;
@@ -871,7 +874,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             else runW = r >= 0 && free_t < r;
             if (!runW) break;
             const int c = V - 1 - wp.c;
-            trace_task(free_t, free_t + REC(2, c).dur, (T)0, -1);
+            trace_task(free_t, free_t + REC(2, c).dur, (T)0, -1, 2, c);
             free_t += REC(2, c).dur;
             dyn += DMEM(2, c);
             ++nW; wp.next(p, V); ++ctasks;
@@ -888,7 +891,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             const int s1 = tk == 0 ? s0 + 1 : s0 - 1;
             int tdev = (oaddr >= 0 && s1 >= 0 && s1 < S) ? dev_of(sl.placement, p, s1) : -1;
             if (tdev == d) tdev = -1;
-            trace_task(fin - tr.dur, fin, tdev >= 0 ? tr.oc : (T)0, tdev);
+            trace_task(fin - tr.dur, fin, tdev >= 0 ? tr.oc : (T)0, tdev, tk, tc);
           }
           free_t = fin;
           if (oaddr >= 0) ring[oaddr] = fin + tr.oc;
@@ -1016,7 +1019,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         if constexpr (TRACE) {
           const int tg = ak == 0 ? ga_tF[acx * 32 + lane] : (ak == 1 ? ga_tB[acx * 32 + lane] : -1);
           const int tdev = tg >= 0 ? (tg >> 3) - leader : -1;
-          trace_task(at, fin, (tdev >= 0 && tdev != d) ? rc.oc : (T)0, tdev == d ? -1 : tdev);
+          trace_task(at, fin, (tdev >= 0 && tdev != d) ? rc.oc : (T)0, tdev == d ? -1 : tdev, ak, acx);
         }
         free_t = fin;
         dyn += DMEM(ak, acx);

@@ -679,3 +679,55 @@ def test_tune_overlap_spec_two_device_example():
     chain = [[(F, 0, 0), (B, 0, 0), (Wk, 0, 0)], [(F, 1, 0), (B, 1, 0), (Wk, 1, 0)]]
     assert O.overlap_candidates(pr1, 1, W.SEQ, False, [1], chain) == []
     assert O.tune_overlap(pr1, 1, W.SEQ, False, [1], chain)[1] == 0
+
+
+# ----------------------------------------------------------------- R35 memory timeline
+def test_memory_timeline_spec_examples():
+    """GPipe with nmb = 4 and 1 unit of activation per stage and
+    micro-batch, capacity 3 units above static: the violation is at the start
+    of the 4th F (worked by hand: one device, t_F = 2, F starts at 0, 2, 4, 6);
+    capacity infinite: no violation; fused B frees act + stash at its end."""
+    u = 1 << 20
+    pr = W.Problem(t_f=[2], t_b=[3], t_w=[1], act=[u], stash=[0], weight=[5 * u], grad=[0], comm=[0],
+                   p=1, m=4, cap=5 * u + 3 * u)
+    r = O.memory_timeline(pr, 1, W.SEQ, W.GPIPE, [])
+    pts = r["points"][0]
+    assert pts[:5] == [(0, 5 * u), (0, 6 * u), (2, 7 * u), (4, 8 * u), (6, 9 * u)]
+    assert r["first_violation"] == [6]
+    # GPipe then runs the 4 fused backwards (t_B + t_W = 4 each) from t = 8
+    assert pts[5:] == [(12, 8 * u), (16, 7 * u), (20, 6 * u), (24, 5 * u)]
+    pr.cap = W.INT64_MAX
+    assert O.memory_timeline(pr, 1, W.SEQ, W.GPIPE, [])["first_violation"] == [-1]
+    # split (ZB): B frees act at its end, W frees stash at its end
+    pr2 = W.Problem(t_f=[2], t_b=[3], t_w=[1], act=[2], stash=[1], weight=[0], grad=[0], comm=[0], p=1, m=1)
+    assert O.memory_timeline(pr2, 1, W.SEQ, W.ZB, [])["points"][0] == [(0, 0), (0, 3), (5, 1), (6, 0)]
+
+
+def test_memory_timeline_peak_equals_simulated_peak():
+    """The timeline's maximum is the event loop's per-device M_d, every policy,
+    placement and binding caps; breakpoint times never decrease; memory returns
+    to the static bytes; the first violation is the first breakpoint above the
+    cap."""
+    rng = W.SplitMix64(707)
+    n = 0
+    for _ in range(60):
+        p = 1 + rng.next() % 4
+        m = p * (1 + rng.next() % 2)
+        L = 2 * p + 1 + rng.next() % 3
+        pr = W.random_problem(rng, L, p, m, bytes_max=6, cap=W.INT64_MAX if rng.next() % 2 else 30)
+        v, placement = (2, W.INTERLEAVED) if L >= 2 * p else (1, W.SEQ)
+        cuts = list(range(1, p * v))
+        for pol in range(4):
+            sim = O.simulate(pr, v, placement, pol, cuts)
+            if sim["status"] not in (0, 2):
+                continue
+            r = O.memory_timeline(pr, v, placement, pol, cuts)
+            for d in range(p):
+                pts = r["points"][d]
+                assert max(b for _, b in pts) == sim["M_d"][d]
+                assert all(a[0] <= b[0] for a, b in zip(pts, pts[1:]))
+                assert pts[-1][1] == pts[0][1] == sim["static_d"][d]
+                over = [t for t, b in pts if b > pr.cap]
+                assert r["first_violation"][d] == (over[0] if over else -1)
+            n += 1
+    assert n > 100
