@@ -466,9 +466,10 @@ def measured_traffic(config_id, kernel):
         t = json.load(open(TRAFFIC_FILE))
     except Exception:  # noqa: BLE001
         return None
-    if t.get("config_id") != config_id or t.get("kernel") != kernel:
+    k = t.get("kernels", {}).get(kernel)
+    if t.get("config_id") != config_id or k is None:
         return None
-    return int(t["dram_read_bytes"]) + int(t["dram_write_bytes"])
+    return int(k["dram_read_bytes"]) + int(k["dram_write_bytes"])
 
 
 def roofline(seg_ms, seg_tasks, seg_n, config_id=None):

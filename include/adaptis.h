@@ -382,6 +382,20 @@ ADAPTIS_API adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared
                                               const adaptis_plan* plans, uint64_t n,
                                               const adaptis_results_soa* out, int64_t* report);
 
+/* Realised workload scheduling results of one policy plan ("workload
+ * scheduling results"; the Executor's compute-instruction lists): the
+ * order in which each device executes its tasks under the plan's policy, as
+ * explicit lists in the format of adaptis_eval_lists (reading R30): device d's
+ * tasks are tasks_out[offsets_out[d] .. offsets_out[d+1]) (offsets_out has p + 1
+ * entries; tasks_out holds `cap` entries, at most p * 3 * m * v are written,
+ * EINVAL if too small). Fused policies (GPIPE, ONEF1B) give LIST_FUSED lists
+ * (no W), split ones LIST lists; evaluating them with the matching LIST policy
+ * reproduces the plan's result. EINFEASIBLE if the plan does not complete
+ * (STUCK: no full order exists). Not in FP32 cost mode. */
+ADAPTIS_API adaptis_status adaptis_realize_lists(adaptis_ctx* ctx, adaptis_prepared* prep,
+                                                 const adaptis_plan* plan, adaptis_task* tasks_out,
+                                                 uint64_t cap, uint64_t* offsets_out);
+
 /* Memory timeline of one plan (Eq. 2; "identifies potential
  * OOM time"; SPEC memory_timeline S:213-221; reading R35 in DESIGN.md): per
  * device, the piecewise-constant memory M_d(t) = static + dynamic bytes as

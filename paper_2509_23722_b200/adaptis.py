@@ -191,6 +191,9 @@ def lib():
                                                C.POINTER(C.c_uint64), C.c_int32, C.c_void_p,
                                                C.POINTER(_Result), C.POINTER(C.c_int32),
                                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+            L.adaptis_realize_lists.restype = st
+            L.adaptis_realize_lists.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
+                                                C.c_uint64, C.POINTER(C.c_uint64)]
             L.adaptis_memory_timeline.restype = st
             L.adaptis_memory_timeline.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
                                                   C.POINTER(C.c_uint64), C.POINTER(_MemPoint), C.c_uint64,
@@ -566,6 +569,18 @@ class Prepared:
                for d in range(p)]
         return {"lists": rep, "moves": int(nm.value), "status": int(res.status),
                 "makespan": int(res.makespan), "peak_mem": int(res.peak_mem_bytes)}
+
+    def realize_lists(self, plan) -> list:
+        """adaptis_realize_lists: the plan's realised per-device orders (R30 lists
+        of (kind, stage, mb); fused policies without W)."""
+        p, m = self.m.problem.p, self.m.problem.m
+        arr = make_plans([plan])
+        cap = p * 3 * m * plan["v"]
+        tasks = np.zeros(cap, dtype=[("kind", "<i2"), ("stage", "<i2"), ("mb", "<i4")])
+        offs = (C.c_uint64 * (p + 1))()
+        _check(lib().adaptis_realize_lists(self.ctx.ptr, self.ptr, arr, tasks.ctypes.data, cap, offs),
+               self.ctx.ptr)
+        return [[tuple(int(x) for x in tasks[i]) for i in range(offs[d], offs[d + 1])] for d in range(p)]
 
     def memory_timeline(self, plan, lists=None) -> dict:
         """adaptis_memory_timeline (R35): per device the breakpoints (time, bytes)

@@ -1648,6 +1648,42 @@ adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared* P, const a
   return eval_plans_common(ctx, P, plans, n, out, report, nullptr, nullptr);
 }
 
+adaptis_status adaptis_realize_lists(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plan,
+                                     adaptis_task* tasks_out, uint64_t cap, uint64_t* offsets_out) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!plan || !tasks_out || !offsets_out) return fail(ctx, ADAPTIS_EINVAL, "a pointer argument is NULL");
+  if (P->tick == kTickF32) return fail(ctx, ADAPTIS_EINVAL, "FP32 cost mode is not supported for realised lists");
+  if (plan->policy == ADAPTIS_LIST || plan->policy == ADAPTIS_LIST_FUSED)
+    return fail(ctx, ADAPTIS_EINVAL, "plan.policy = %d: an explicit schedule is already realised", plan->policy);
+  const uint64_t need = (uint64_t)P->p * 3 * (uint64_t)P->m * (plan->v > 0 ? plan->v : 1);
+  if (cap < need)
+    return fail(ctx, ADAPTIS_EINVAL, "cap = %llu < p * 3 * m * v = %llu", (unsigned long long)cap,
+                (unsigned long long)need);
+  std::vector<int64_t> mk; std::vector<uint8_t> stt; std::vector<TraceEntry> tr; int tcap = 0;
+  adaptis_status st = run_plans(ctx, P, plan, 1, &mk, nullptr, nullptr, &stt, nullptr, nullptr, nullptr, nullptr,
+                                &tr, &tcap);
+  if (st != ADAPTIS_OK) return st;
+  if (stt[0] == ADAPTIS_CAND_INVALID) return fail(ctx, ADAPTIS_EINVAL, "plan cuts are not strictly increasing");
+  if (stt[0] == ADAPTIS_CAND_STUCK)
+    return fail(ctx, ADAPTIS_EINFEASIBLE, "the plan's policy gets stuck (R14): no complete order");
+  // status 0 or 2: every device executed all of its m v (2 or 3) tasks, in trace order
+  const int per_dev = (plan->policy == ADAPTIS_GPIPE || plan->policy == ADAPTIS_ONEF1B ? 2 : 3) * P->m * plan->v;
+  if (per_dev > tcap) return fail(ctx, ADAPTIS_ECUDA, "trace capacity %d < %d tasks per device", tcap, per_dev);
+  uint64_t k = 0;
+  for (int d = 0; d < P->p; ++d) {
+    offsets_out[d] = k;
+    for (int i = 0; i < per_dev; ++i) {
+      const TraceEntry& e = tr[(size_t)d * tcap + i];
+      tasks_out[k].kind = e.kind;
+      tasks_out[k].stage = e.stage;
+      tasks_out[k].mb = e.mb;
+      ++k;
+    }
+  }
+  offsets_out[P->p] = k;
+  return ADAPTIS_OK;
+}
+
 adaptis_status adaptis_memory_timeline(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_plan* plan,
                                        const adaptis_task* tasks, const uint64_t* offsets, adaptis_mem_point* out,
                                        uint64_t cap_points, uint64_t* dev_offsets, int64_t* first_violation) {

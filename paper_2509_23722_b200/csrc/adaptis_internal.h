@@ -95,8 +95,8 @@ struct SegLaunch {
 struct TraceEntry {
   int64_t start, fin;
   int32_t oc, tgt;
-  int16_t kind, stage;  // the task (F 0, B 1, W 2; stage index), for the memory timeline
-  int32_t pad;
+  int16_t kind, stage;  // the task (F 0, B 1, W 2; stage index, micro-batch), for the
+  int32_t mb;           // memory timeline and the realised lists
 };
 
 #ifdef __CUDACC__

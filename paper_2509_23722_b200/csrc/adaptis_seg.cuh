@@ -417,7 +417,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
   // TRACE (report mode, R29): append a committed task [start, fin) of (kind,
   // chunk) and its output transfer (latency oc to device tdev, -1: none) to this
   // candidate's device trace
-  auto trace_task = [&](T start, T fin, T oc, int tdev, int kind, int chunk) {
+  auto trace_task = [&](T start, T fin, T oc, int tdev, int kind, int chunk, int mb) {
     if constexpr (TRACE) {
       if (ntr < sl.trace_cap) {
         TraceEntry e;
@@ -427,6 +427,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         e.tgt = tdev;
         e.kind = (int16_t)kind;
         e.stage = (int16_t)stage_of(sl.placement, p, chunk, d);
+        e.mb = mb;
         sl.trace[((size_t)cold.slot * p + d) * sl.trace_cap + ntr] = e;
       }
       ++ntr;
@@ -834,7 +835,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
       __syncwarp();
       if (LISTP && live) {  // phase B of an explicit order (R30): W at free_t, F/B when ready
         if (tk == 2) {
-          trace_task(free_t, free_t + tr.dur, (T)0, -1, 2, tc);
+          trace_task(free_t, free_t + tr.dur, (T)0, -1, 2, tc, tj);
           free_t += tr.dur;
           dyn += DMEM(2, tc);
           ++nF; ++ctasks;
@@ -850,7 +851,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
               const int s1 = tk == 0 ? s0 + 1 : s0 - 1;
               int tdev = (oaddr >= 0 && s1 >= 0 && s1 < S) ? dev_of(sl.placement, p, s1) : -1;
               if (tdev == d) tdev = -1;
-              trace_task(fin - tr.dur, fin, tdev >= 0 ? tr.oc : (T)0, tdev, tk, tc);
+              trace_task(fin - tr.dur, fin, tdev >= 0 ? tr.oc : (T)0, tdev, tk, tc, tj);
             }
             free_t = fin;
             if (oaddr >= 0) ring[oaddr] = fin + tr.oc;
@@ -874,7 +875,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             else runW = r >= 0 && free_t < r;
             if (!runW) break;
             const int c = V - 1 - wp.c;
-            trace_task(free_t, free_t + REC(2, c).dur, (T)0, -1, 2, c);
+            trace_task(free_t, free_t + REC(2, c).dur, (T)0, -1, 2, c, wp.mb());
             free_t += REC(2, c).dur;
             dyn += DMEM(2, c);
             ++nW; wp.next(p, V); ++ctasks;
@@ -891,7 +892,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
             const int s1 = tk == 0 ? s0 + 1 : s0 - 1;
             int tdev = (oaddr >= 0 && s1 >= 0 && s1 < S) ? dev_of(sl.placement, p, s1) : -1;
             if (tdev == d) tdev = -1;
-            trace_task(fin - tr.dur, fin, tdev >= 0 ? tr.oc : (T)0, tdev, tk, tc);
+            trace_task(fin - tr.dur, fin, tdev >= 0 ? tr.oc : (T)0, tdev, tk, tc, tj);
           }
           free_t = fin;
           if (oaddr >= 0) ring[oaddr] = fin + tr.oc;
@@ -1019,7 +1020,7 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         if constexpr (TRACE) {
           const int tg = ak == 0 ? ga_tF[acx * 32 + lane] : (ak == 1 ? ga_tB[acx * 32 + lane] : -1);
           const int tdev = tg >= 0 ? (tg >> 3) - leader : -1;
-          trace_task(at, fin, (tdev >= 0 && tdev != d) ? rc.oc : (T)0, tdev == d ? -1 : tdev, ak, acx);
+          trace_task(at, fin, (tdev >= 0 && tdev != d) ? rc.oc : (T)0, tdev == d ? -1 : tdev, ak, acx, aj);
         }
         free_t = fin;
         dyn += DMEM(ak, acx);

@@ -55,7 +55,7 @@ ADAPTIS_LAYOUT_HD SeqLayout seq_layout(int S, int P2, bool search) {
   int r = 0;
   l.key = r; r += P2;
   l.fd = r; r += P2;
-  l.cnt = r; r += S;
+  l.cnt = r; r += S + 2;  // guard rows for stages -1 and S
   l.dur = r; r += 3 * S;
   l.lat = r; r += S;
   l.rf = r; r += kSeqK * S;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
   int64_t* __restrict__ rACT = w64 + lay.act * 32 + lane;
 #define KEY(d) rKEY[(d) * 32]
 #define FD(d) rFD[(d) * 32]
-#define CNT(s) rCNT[(s) * 32]
+#define CNT(s) rCNT[((s) + 1) * 32]
 #define DUR(k, s) rDUR[((k) * S + (s)) * 32]
 #define LAT(s) rLAT[(s) * 32]
 #define RF(k, s) rRF[((k) * S + (s)) * 32]
@@ -130,7 +130,12 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
   // next F of each own stage if it fits under Eq. 2, the head B whose F is
   // done, the head W whose B is done; at = max(free, earliest ready); among
   // the tasks ready by `at` the smallest (kind F < B < W, mb, stage) wins.
-  // Branch-free: every load is in bounds and selected afterwards.
+  // Branch-free: every load is in bounds and selected afterwards. The guard
+  // rows CNT(-1) (255 F items "produced" into stage 0) and CNT(S) (255 B items
+  // into stage S-1) make the input-less heads F(0, j) and B(S-1, j) (ready by
+  // the device's own free time) count as arrived: they take the current event
+  // time, which the compression argument above admits for any X with
+  // ready <= X <= the device's next action time.
   auto decide = [&](int d, uint32_t tnow) {
     const uint32_t free_t = FD(d) >> 4;
     const int64_t room = CAPD(d) - DYN(d);  // F of stage s fits iff act + stash <= room
@@ -139,14 +144,13 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
 #pragma unroll
     for (int c = 0; c < V; ++c) {
       const int s = sq_stage<PLC, P>(c, d);
-      const uint32_t cnt = CNT(s);
-      const uint32_t cp = CNT(s > 0 ? s - 1 : 0), cn = CNT(s < S - 1 ? s + 1 : S - 1);
+      const uint32_t cnt = CNT(s), cp = CNT(s - 1), cn = CNT(s + 1);
       const uint32_t gF = cnt & 255u, gB = (cnt >> 8) & 255u, gW = (cnt >> 16) & 255u;
-      const uint32_t prodF = s == 0 ? 255u : (cp & 255u);          // F items produced into s
-      const uint32_t prodB = s == S - 1 ? 255u : ((cn >> 8) & 255u);  // B items produced into s
+      const uint32_t prodF = cp & 255u;          // F items produced into s
+      const uint32_t prodB = (cn >> 8) & 255u;   // B items produced into s
       const uint32_t sF = RF(gF & (kSeqK - 1), s), sB = RB(gB & (kSeqK - 1), s);
-      const uint32_t aF = s == 0 ? 0u : (gF + kSeqK >= prodF ? sF : tnow);
-      const uint32_t aB = s == S - 1 ? 0u : (gB + kSeqK >= prodB ? sB : tnow);
+      const uint32_t aF = gF + kSeqK >= prodF ? sF : tnow;
+      const uint32_t aB = gB + kSeqK >= prodB ? sB : tnow;
       const bool okF = gF < (uint32_t)m && gF < prodF && AS(s) <= room;
       const bool okB = gB < gF && gB < prodB;
       rf[c] = okF ? aF : kSeqInf;
@@ -156,17 +160,16 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
       rmin = min(rmin, min(rf[c], min(rb[c], rw[c])));
     }
     const uint32_t at = max(free_t, rmin);
-    uint32_t kF = kSeqInf, kB = kSeqInf, kW = kSeqInf;
+    // the smallest (kind, mb, stage) among the tasks ready by `at`: kind << 10 | mb << 2 | chunk
+    uint32_t best = kSeqInf;
 #pragma unroll
     for (int c = 0; c < V; ++c) {
-      kF = rf[c] <= at ? min(kF, (gf[c] << 2) | (uint32_t)c) : kF;
-      kB = rb[c] <= at ? min(kB, (gb[c] << 2) | (uint32_t)c) : kB;
-      kW = rw[c] <= at ? min(kW, (gw[c] << 2) | (uint32_t)c) : kW;
+      best = min(best, rf[c] <= at ? ((gf[c] << 2) | (uint32_t)c) : kSeqInf);
+      best = min(best, rb[c] <= at ? ((1u << 10) | (gb[c] << 2) | (uint32_t)c) : kSeqInf);
+      best = min(best, rw[c] <= at ? ((2u << 10) | (gw[c] << 2) | (uint32_t)c) : kSeqInf);
     }
-    const uint32_t dec = kF != kSeqInf ? ((kF & 3u) << 2)
-                       : kB != kSeqInf ? (1u | ((kB & 3u) << 2)) : (2u | ((kW & 3u) << 2));
     KEY(d) = rmin == kSeqInf ? kSeqInf : ((at << 4) | (uint32_t)d);
-    FD(d) = (free_t << 4) | dec;
+    FD(d) = (free_t << 4) | ((best >> 10) & 3u) | ((best & 3u) << 2);
   };
 
   unsigned long long best_key = ~0ull >> 1, n_inv = 0, n_pr = 0, n_tasks = 0;
@@ -263,6 +266,8 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
         LAT(s) = lf | (lb << 16);
         CNT(s) = 0;
       }
+      CNT(-1) = 255u;       // guard: stage 0's F input is always there
+      CNT(S) = 255u << 8;   // guard: stage S-1's B input is always there
       // exact lower-bound prune (search): the bound of adaptis_seg.cuh, per
       // device d with lowest stage d: head = t_F[0, cuts[d]) + the d edge
       // latencies; split: max(head + busy_d, head + m (F + B)_d + t_B[0, cuts[d])

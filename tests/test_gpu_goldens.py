@@ -116,8 +116,10 @@ def test_whole_shard_fallback_counts_once(ctx, monkeypatch):
 
 def test_uniform_sample_parity_cfg3_ring2(ctx, monkeypatch):
     """Seeded-uniform cfg3 indices through adaptis_eval_indices with the
-    fallback forced (list-mode re-run of explicit index positions)."""
-    monkeypatch.setenv("ADAPTIS_RING_K", "2")
+    fallback forced (list-mode re-run of explicit index positions): one ring
+    slot per edge, so a producer waits for every consumer and most slots of a
+    multi-device candidate block together."""
+    monkeypatch.setenv("ADAPTIS_RING_K", "1")
     monkeypatch.setenv("ADAPTIS_NO_SEQ", "1")  # the lane-per-device kernels and their rings
     pr, sp = W.config(3)
     N = O.space_size(pr, sp)

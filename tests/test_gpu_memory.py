@@ -104,3 +104,33 @@ def test_memory_timeline_explicit_lists(ctx):
             assert want == O.memory_timeline(pr, 2, W.INTERLEAVED, po, cuts)
             n += 1
     assert n > 10
+
+
+def test_realized_lists_equal_the_event_loop_order(ctx):
+    """adaptis_realize_lists: the policy's realised per-device order equals the
+    oracle event loop's trace order, and evaluating it as an explicit schedule
+    (R30, LIST / LIST_FUSED) reproduces the plan's result."""
+    srng = W.SplitMix64(123)
+    rng = random.Random(123)
+    n = 0
+    for t in range(6):
+        p = [2, 3, 4][t % 3]
+        pr = W.random_problem(srng, 2 * p + 3, p, 2 * p, tmax=9, cmax=5, bytes_max=9,
+                              cap=W.INT64_MAX if t % 2 else 45)
+        prep = ctx.prepare(pr, W.Space([W.Group(1, W.FULL, combo_mask=0xF)]))
+        for plan in _plans(pr, rng, 10):
+            cuts = plan["cuts"][1:-1]
+            r = O.simulate(pr, plan["v"], plan["placement"], plan["policy"], cuts, trace=True)
+            if r["status"] not in (0, 2):
+                continue
+            fused = plan["policy"] in (W.GPIPE, W.ONEF1B)
+            want = [[(k, s, j) for (k, s, j, _t) in lst if not (fused and k == 2)] for lst in r["trace"]]
+            got = prep.realize_lists(plan)
+            assert got == want, plan
+            lp = dict(plan, policy=5 if fused else 4)
+            ev = prep.eval_lists([lp], [got])
+            assert int(ev["status"][0]) == r["status"]
+            if r["status"] == 0:
+                assert int(ev["makespan"][0]) == r["makespan"]
+            n += 1
+    assert n > 20
