@@ -789,7 +789,10 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
                 flags |= F_PRUNED;
             }
           }
-          const bool survivor = take && valid && !(flags & (F_PREOVER | F_PRUNED));
+          // a fused order over the cap is decided without simulating it, except in
+          // report launches, whose traces (R29 accounting, the memory timeline,
+          // realised lists) cover every plan of status 0 or 2
+          const bool survivor = take && valid && !(flags & F_PRUNED) && (TRACE || !(flags & F_PREOVER));
           const unsigned nonsurv_m = __ballot_sync(FULLMASK, take && !survivor);
           if (nonsurv_m) finalize(take && !survivor);
           if (survivor) {

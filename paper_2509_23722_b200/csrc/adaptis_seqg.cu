@@ -43,6 +43,13 @@ namespace adaptis {
 #define ADAPTIS_SEQG_K 2
 #endif
 constexpr int kSeqK = ADAPTIS_SEQG_K;   // exact arrival slots per edge (power of two)
+// compact state: a stage keeps its two cut rows instead of its durations,
+// latencies and act bytes, which the commit recomputes from the (L1-resident)
+// prefix and latency tables: 1,024 -> 704 B per candidate at p = 8, S = 16
+#ifndef ADAPTIS_SEQG_COMPACT
+#define ADAPTIS_SEQG_COMPACT 1
+#endif
+constexpr bool kSeqCompact = ADAPTIS_SEQG_COMPACT;
 constexpr uint32_t kSeqInf = 0xffffffffu;
 
 // shared-memory rows of one lane (a row is 32 lanes x 4 or 8 bytes)
@@ -50,14 +57,14 @@ struct SeqLayout {
   int key, fd, cnt, dur, lat, rf, rb, n32;  // u32 rows
   int dyn, capd, peak, as, act, n64;        // u64 rows
 };
-ADAPTIS_LAYOUT_HD SeqLayout seq_layout(int S, int P2, bool search) {
-  SeqLayout l;
+ADAPTIS_LAYOUT_HD constexpr SeqLayout seq_layout(int S, int P2, bool search) {
+  SeqLayout l{};
   int r = 0;
   l.key = r; r += P2;
   l.fd = r; r += P2;
   l.cnt = r; r += S + 2;  // guard rows for stages -1 and S
-  l.dur = r; r += 3 * S;
-  l.lat = r; r += S;
+  l.dur = r; r += kSeqCompact ? S : 3 * S;  // compact: CUT(s) = cuts[s] | cuts[s+1] << 16
+  l.lat = r; r += kSeqCompact ? 0 : S;
   l.rf = r; r += kSeqK * S;
   l.rb = r; r += kSeqK * S;
   l.n32 = (r + 1) & ~1;  // keep the u64 rows 8-byte aligned
@@ -66,14 +73,23 @@ ADAPTIS_LAYOUT_HD SeqLayout seq_layout(int S, int P2, bool search) {
   l.capd = r; r += P2;
   l.peak = r; r += search ? 0 : P2;  // per-device peaks are reported in eval mode only
   l.as = r; r += S;
-  l.act = r; r += S;
+  l.act = r; r += kSeqCompact ? 0 : S;
   l.n64 = r;
   return l;
 }
-size_t seqg_smem_bytes(int S, int p, bool search) {
-  const SeqLayout l = seq_layout(S, p, search);
-  return (size_t)32 * (4 * l.n32 + 8 * l.n64);
+ADAPTIS_LAYOUT_HD constexpr size_t seqg_smem_bytes(int S, int p, bool search) {
+  return (size_t)32 * (4 * seq_layout(S, p, search).n32 + 8 * seq_layout(S, p, search).n64);
 }
+// one-warp CTAs; the register cap follows the CTAs that shared memory admits
+// per SM (228 KB, 1 KB reserved per CTA), rounded up to a multiple of 4: a
+// warp's registers come from one of the 4 SM sub-partitions (16 K each), so n
+// warps per SM need 16384 / ceil(n / 4) registers per warp (at most 20 warps)
+template <int V, int P, bool SEARCH>
+struct SeqOcc {
+  static constexpr int by_smem = (int)((228 * 1024) / (seqg_smem_bytes(V * P, P, SEARCH) + 1024));
+  static constexpr int r4 = (by_smem + 3) & ~3;
+  static constexpr int value = r4 < 4 ? 4 : (r4 > 20 ? 20 : r4);
+};
 
 // placement of stage s = c * P + j (R12), compile-time P (a power of two)
 template <int PLC, int P>
@@ -90,7 +106,8 @@ __device__ __forceinline__ int sq_dev(int s) {
 }
 
 template <int V, int P, int PLC, bool SEARCH>
-__global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const SegLaunch sl) {
+__global__ void __launch_bounds__(32, (SeqOcc<V, P, SEARCH>::value))
+seqg_kernel(const DevTables tab, const SegLaunch sl) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int S = V * P;
   const int lane = threadIdx.x & 31;
@@ -115,6 +132,7 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
 #define FD(d) rFD[(d) * 32]
 #define CNT(s) rCNT[((s) + 1) * 32]
 #define DUR(k, s) rDUR[((k) * S + (s)) * 32]
+#define CUT(s) rDUR[(s) * 32]
 #define LAT(s) rLAT[(s) * 32]
 #define RF(k, s) rRF[((k) * S + (s)) * 32]
 #define RB(k, s) rRB[((k) * S + (s)) * 32]
@@ -254,16 +272,20 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
       for (int s = 0; s < S; ++s) {
         const int a = cuts[s], b = cuts[s + 1];
         const int ds = sq_dev<PLC, P>(s);
-        DUR(0, s) = (uint32_t)(PRE(kColTF, b) - PRE(kColTF, a));
-        DUR(1, s) = (uint32_t)(PRE(kColTB, b) - PRE(kColTB, a));
-        DUR(2, s) = (uint32_t)(PRE(kColTW, b) - PRE(kColTW, a));
         const int64_t act = PRE(kColAct, b) - PRE(kColAct, a);
         AS(s) = act + (PRE(kColStash, b) - PRE(kColStash, a));
-        ACT(s) = act;
         CAPD(ds) -= PRE(kColWG, b) - PRE(kColWG, a);  // cap - static (cannot overflow: static >= 0)
-        const uint32_t lf = (s < S - 1 && sq_dev<PLC, P>(s + 1) != ds) ? (uint32_t)tab.comm[b - 1] : 0u;
-        const uint32_t lb = (s > 0 && sq_dev<PLC, P>(s - 1) != ds) ? (uint32_t)tab.comm[a - 1] : 0u;
-        LAT(s) = lf | (lb << 16);
+        if constexpr (kSeqCompact) {
+          CUT(s) = (uint32_t)a | ((uint32_t)b << 16);
+        } else {
+          DUR(0, s) = (uint32_t)(PRE(kColTF, b) - PRE(kColTF, a));
+          DUR(1, s) = (uint32_t)(PRE(kColTB, b) - PRE(kColTB, a));
+          DUR(2, s) = (uint32_t)(PRE(kColTW, b) - PRE(kColTW, a));
+          ACT(s) = act;
+          const uint32_t lf = (s < S - 1 && sq_dev<PLC, P>(s + 1) != ds) ? (uint32_t)tab.comm[b - 1] : 0u;
+          const uint32_t lb = (s > 0 && sq_dev<PLC, P>(s - 1) != ds) ? (uint32_t)tab.comm[a - 1] : 0u;
+          LAT(s) = lf | (lb << 16);
+        }
         CNT(s) = 0;
       }
       CNT(-1) = 255u;       // guard: stage 0's F input is always there
@@ -275,15 +297,17 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
       // exceeds the incumbent key cannot win
       if (SEARCH && sl.prune) {
         int64_t lk = 0, lb = 0;
-        const int64_t w0 = DUR(2, 0);
+        const int64_t w0 = PRE(kColTW, cuts[1]);
         for (int d = 0; d < P; ++d) {
           if (d >= 1) lk += (int64_t)tab.comm[cuts[d] - 1];
           int64_t busy = 0, wsum = 0;
 #pragma unroll
           for (int c = 0; c < V; ++c) {
             const int s = sq_stage<PLC, P>(c, d);
-            busy += (int64_t)m * ((int64_t)DUR(0, s) + DUR(1, s) + DUR(2, s));
-            wsum += DUR(2, s);
+            const int a = cuts[s], b = cuts[s + 1];
+            const int64_t cw = PRE(kColTW, b) - PRE(kColTW, a);
+            busy += (int64_t)m * ((PRE(kColTF, b) - PRE(kColTF, a)) + (PRE(kColTB, b) - PRE(kColTB, a)) + cw);
+            wsum += cw;
           }
           const int64_t head = PRE(kColTF, cuts[d]) + lk;
           int64_t lbd = busy + head;
@@ -319,15 +343,31 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
           const uint32_t cnt = CNT(s);
           const int sh = 8 * kind;
           const uint32_t j = (cnt >> sh) & 255u;
-          const uint32_t fin = at + DUR(kind, s);
+          uint32_t dur, latw;
+          int64_t ac;
+          if constexpr (kSeqCompact) {
+            const uint32_t cw = CUT(s);
+            const int a = (int)(cw & 0xffffu), b = (int)(cw >> 16);
+            const int col = kind == 0 ? kColTF : (kind == 1 ? kColTB : kColTW);
+            dur = (uint32_t)(PRE(col, b) - PRE(col, a));
+            ac = PRE(kColAct, b) - PRE(kColAct, a);
+            // latencies of the output edges (R3-R6): 0 between stages of one device
+            const uint32_t lf = (s < S - 1 && sq_dev<PLC, P>(s + 1) != d) ? (uint32_t)__ldg(tab.comm + b - 1) : 0u;
+            const uint32_t lb = (s > 0 && sq_dev<PLC, P>(s - 1) != d) ? (uint32_t)__ldg(tab.comm + (a > 0 ? a - 1 : 0)) : 0u;
+            latw = lf | (lb << 16);
+          } else {
+            dur = DUR(kind, s);
+            ac = ACT(s);
+            latw = LAT(s);
+          }
+          const uint32_t fin = at + dur;
           // R16: act + stash at F start; act freed at B end, stash at W end
-          const int64_t as = AS(s), ac = ACT(s);
+          const int64_t as = AS(s);
           const int64_t dy = DYN(d) + (kind == 0 ? as : (kind == 1 ? -ac : ac - as));
           // the output item: F(s, j) -> F(s+1, j), B(s, j) -> B(s-1, j)
           const bool out = kind == 0 ? s < S - 1 : (kind == 1 && s > 0);
           int tg = kind == 0 ? s + 1 : s - 1;
           tg = tg < 0 ? 0 : (tg > S - 1 ? S - 1 : tg);
-          const uint32_t latw = LAT(s);
           const uint32_t lat = kind == 0 ? (latw & 0xffffu) : (latw >> 16);
           uint32_t* ring = (kind == 0 ? rRF : rRB) + (((int)(j & (kSeqK - 1)) * S + tg) * 32);
           const uint32_t old = *ring;
@@ -371,7 +411,11 @@ __global__ void __launch_bounds__(32, 4) seqg_kernel(const DevTables tab, const 
             const int64_t md = (sl.cap - CAPD(d)) + PEAK(d);
             mmax = md > mmax ? md : mmax;
           }
-          for (int s = 0; s < S; ++s) busy += (double)m * ((double)DUR(0, s) + DUR(1, s) + DUR(2, s));
+          for (int s = 0; s < S; ++s) {
+            const int a = cuts[s], b = cuts[s + 1];
+            busy += (double)m * (double)((PRE(kColTF, b) - PRE(kColTF, a)) + (PRE(kColTB, b) - PRE(kColTB, a)) +
+                                         (PRE(kColTW, b) - PRE(kColTW, a)));
+          }
           if (sl.out_status) sl.out_status[slot] = stuck ? ADAPTIS_CAND_STUCK : ADAPTIS_CAND_OK;
           if (sl.out_makespan) sl.out_makespan[slot] = stuck ? INT64_MAX : (int64_t)mk;
           if (sl.out_makespan_f32) sl.out_makespan_f32[slot] = stuck ? INFINITY : (float)mk;

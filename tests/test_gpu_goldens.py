@@ -114,22 +114,26 @@ def test_whole_shard_fallback_counts_once(ctx, monkeypatch):
     assert max(li["fallback"] for li in ctx.launch_info()) > (1 << 20)
 
 
-def test_uniform_sample_parity_cfg3_ring2(ctx, monkeypatch):
-    """Seeded-uniform cfg3 indices through adaptis_eval_indices with the
-    fallback forced (list-mode re-run of explicit index positions): one ring
-    slot per edge, so a producer waits for every consumer and most slots of a
-    multi-device candidate block together."""
+def test_eval_indices_fallback_matches_oracle(ctx, monkeypatch):
+    """adaptis_eval_indices (explicit index positions) with the fallback forced:
+    overflowed candidates are re-run from their recorded output slots (list
+    mode); seeded-uniform cfg3 indices, the block around the oracle's winner and
+    every candidate of random small spaces, element by element."""
     monkeypatch.setenv("ADAPTIS_RING_K", "1")
     monkeypatch.setenv("ADAPTIS_NO_SEQ", "1")  # the lane-per-device kernels and their rings
+    before = ctx.fallback_count
     pr, sp = W.config(3)
     N = O.space_size(pr, sp)
-    # uniform indices are mostly far from the seed (unbalanced, often over the
-    # cap); the block around the oracle's winner holds balanced ZB candidates
-    # whose dependency lag overflows two ring slots
     w = golden_argmin(3)["index"]
     idx = np.concatenate([np.random.default_rng(777).integers(0, N, 10_000),
                           np.arange(w - 5000, w + 5000)]).astype(np.uint64)
-    before = ctx.fallback_count
     got = ctx.prepare(pr, sp).eval_indices(idx)
-    _compare(got, O.eval_indices(pr, sp, idx), "cfg3 uniform K=2")
-    assert ctx.fallback_count > before
+    _compare(got, O.eval_indices(pr, sp, idx), "cfg3 uniform K=1")
+    fb = [li["fallback"] for li in ctx.launch_info()]
+    for pr2, sp2 in _random_spaces(8, 12):
+        N2 = O.space_size(pr2, sp2)
+        idx2 = np.random.default_rng(5).permutation(N2).astype(np.uint64)  # shuffled: no runs
+        got = ctx.prepare(pr2, sp2).eval_indices(idx2)
+        _compare(got, O.eval_indices(pr2, sp2, idx2), "random K=1 p=%d m=%d" % (pr2.p, pr2.m))
+        fb += [li["fallback"] for li in ctx.launch_info()]
+    assert ctx.fallback_count > before, fb
