@@ -43,11 +43,13 @@ namespace adaptis {
 #define ADAPTIS_SEQG_K 2
 #endif
 constexpr int kSeqK = ADAPTIS_SEQG_K;   // exact arrival slots per edge (power of two)
-// compact state: a stage keeps its two cut rows instead of its durations,
+// compact state (off): a stage keeps its two cut rows instead of its durations,
 // latencies and act bytes, which the commit recomputes from the (L1-resident)
-// prefix and latency tables: 1,024 -> 704 B per candidate at p = 8, S = 16
+// prefix and latency tables: 1,024 -> 704 B per candidate at p = 8, S = 16 and
+// 9 instead of 6 warps per SM, but the extra load level on every step's
+// critical path costs more (measured on cfg3: 2066 against 1958 ms)
 #ifndef ADAPTIS_SEQG_COMPACT
-#define ADAPTIS_SEQG_COMPACT 1
+#define ADAPTIS_SEQG_COMPACT 0
 #endif
 constexpr bool kSeqCompact = ADAPTIS_SEQG_COMPACT;
 constexpr uint32_t kSeqInf = 0xffffffffu;
