@@ -62,7 +62,12 @@ def spawn_ranks(args):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            "--nproc-per-node=%d" % args.gpus, "--master-addr", "127.0.0.1",
            "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
-    return subprocess.call(cmd)
+    # exactly one line on stdout: rank 0's JSON; anything else the ranks print goes to stderr
+    proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, text=True)
+    for line in proc.stdout:
+        (sys.stdout if line.startswith("{") else sys.stderr).write(line)
+        sys.stdout.flush()
+    return proc.wait()
 
 
 # ------------------------------------------------------------------ clocks
@@ -217,6 +222,9 @@ def main():
 
     torch.cuda.set_device(local)
     group = None
+    # NCCL's own messages (e.g. the NCCL_DEBUG=VERSION banner) go to stderr, so that
+    # rank 0's stdout carries exactly the one JSON line of the contract
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD

@@ -299,9 +299,9 @@ ADAPTIS_API adaptis_status adaptis_eval_indices(adaptis_ctx* ctx, adaptis_prepar
  * device d executes tasks[offsets[i*(p+1)+d] .. offsets[i*(p+1)+d+1]) in order:
  * every (F, B[, W]) x own stage x micro-batch exactly once, with F(s,j) before
  * B(s,j) before W(s,j) on the device (else EINVAL naming plan, device and
- * task). The offsets array (n*(p+1) entries) must be non-decreasing over its
- * whole length, plan after plan (else EINVAL): tasks[0 .. offsets[n*(p+1)-1])
- * is read. Cross-device waits follow the DAG; a cyclic wait gives status
+ * task). Each plan's offsets are non-decreasing (else EINVAL); plans may share
+ * or reorder task ranges: tasks[0 .. max_i offsets[i*(p+1)+p]) is read.
+ * Cross-device waits follow the DAG; a cyclic wait gives status
  * STUCK, a peak above the cap OVER_CAP (split precedence, R26). Outputs as
  * adaptis_eval_plans (report [n][7][p] optional). Not in FP32 cost mode. */
 ADAPTIS_API adaptis_status adaptis_eval_lists(adaptis_ctx* ctx, adaptis_prepared* prep,

@@ -750,11 +750,6 @@ adaptis_status validate_lists(adaptis_ctx* ctx, const adaptis_prepared* P, const
     const int nk = fused ? 2 : 3, S = pl.S;
     std::vector<int64_t> pos((size_t)nk * S * m, -1);
     const uint64_t* off = offsets + i * (uint64_t)(p + 1);
-    // the whole offsets array is non-decreasing (plan after plan), so its last
-    // entry bounds every task range: the device copy is sized by it
-    if (i > 0 && off[0] < off[-1])
-      return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: offsets start before the end of plans[%llu]",
-                  (unsigned long long)i, (unsigned long long)(i - 1));
     for (int d = 0; d < p; ++d) {
       if (off[d + 1] < off[d])
         return fail(ctx, ADAPTIS_EINVAL, "plans[%llu]: offsets of device %d decrease", (unsigned long long)i, d);
@@ -887,7 +882,9 @@ adaptis_status run_plans(adaptis_ctx* ctx, adaptis_prepared* P, const adaptis_pl
     CUP(cudaMemsetAsync(tb.trace_n, 0, (size_t)n * P->p * sizeof(int), ctx->stream));
   }
   if (tasks) {
-    const uint64_t ntask = offsets[n * (uint64_t)(P->p + 1) - 1];
+    // plans may share or reorder task ranges: the device copy covers the largest end
+    uint64_t ntask = 0;
+    for (uint64_t i = 0; i < n; ++i) ntask = std::max(ntask, offsets[i * (uint64_t)(P->p + 1) + P->p]);
     CUP(cudaMalloc(&d_tasks, std::max<uint64_t>(ntask, 1) * sizeof(adaptis_task)));
     CUP(cudaMalloc(&d_toff, n * (P->p + 1) * 8));
     CUP(cudaMemcpyAsync(d_tasks, tasks, ntask * sizeof(adaptis_task), cudaMemcpyHostToDevice, ctx->stream));
@@ -1788,7 +1785,8 @@ adaptis_status adaptis_eval_lists_contended(adaptis_ctx* ctx, adaptis_prepared* 
                 (unsigned long long)n, (long double)n * stride * 8);
   if (n == 0) return ADAPTIS_OK;
   CU(ctx, cudaSetDevice(ctx->device));
-  const uint64_t ntask = offsets[n * (uint64_t)(p + 1) - 1];
+  uint64_t ntask = 0;  // plans may share or reorder task ranges: copy up to the largest end
+  for (uint64_t i = 0; i < n; ++i) ntask = std::max(ntask, offsets[i * (uint64_t)(p + 1) + p]);
   adaptis_plan* d_plans = nullptr; adaptis_task* d_tasks = nullptr; uint64_t* d_off = nullptr;
   int64_t *d_scr = nullptr, *d_mk = nullptr, *d_pk = nullptr, *d_rep = nullptr;
   float* d_bub = nullptr; uint8_t* d_st = nullptr; unsigned long long* d_nt = nullptr;

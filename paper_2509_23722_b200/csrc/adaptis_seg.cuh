@@ -56,6 +56,9 @@ constexpr int kRun = ADAPTIS_KRUN;  // consecutive positions a slot claims (incr
 #ifndef ADAPTIS_GREEDY_ALWAYS_DECIDE
 #define ADAPTIS_GREEDY_ALWAYS_DECIDE 2  // from this V up, decide() always recomputes
 #endif
+#ifndef ADAPTIS_ZB_WFILL_ONE
+#define ADAPTIS_ZB_WFILL_ONE 0
+#endif
 #ifndef ADAPTIS_GREEDY_COMMITS
 #define ADAPTIS_GREEDY_COMMITS 1
 #endif
@@ -869,8 +872,10 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
         if (tk == 3) done = true;
       } else if (live) {  // phase B: execute
         if constexpr (ZB) {
-          // R13: (i) memory-forced W before an F that does not fit, (ii) W fill while free < r
-          for (;;) {
+          // R13: (i) memory-forced W before an F that does not fit, (ii) W fill while free < r.
+          // ADAPTIS_ZB_WFILL_ONE: one W per lane and round (the rest in later rounds),
+          // so that lanes with long W runs do not hold the warp in this loop
+          for (int wi = 0; !ADAPTIS_ZB_WFILL_ONE || wi < 1; ++wi) {
             if (nW >= nB) break;
             bool runW;
             if (tk == 2) runW = true;
@@ -886,7 +891,11 @@ seg_kernel(const DevTables tab, const SegLaunch sl) {
           }
         }
         bool xgo = tk < 2 && r >= 0;
-        if constexpr (ZB) xgo = xgo && (nW >= nB || free_t >= r);
+        if constexpr (ZB) {
+          xgo = xgo && (nW >= nB || free_t >= r);
+          // an F that does not fit waits while Ws remain to be drained (R13 (i))
+          if (tk == 0 && nW < nB && stat + dyn + DMEM(0, tc) > sl.cap) xgo = false;
+        }
         if (xgo && !ofree) { blocked = true; xgo = false; }
         if (xgo) {
           const T fin = (free_t > r ? free_t : r) + tr.dur;

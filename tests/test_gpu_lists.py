@@ -324,3 +324,30 @@ def test_int64_kernels_for_lists_plans_and_reports(ctx, monkeypatch):
     r = prep.repair_oom({"v": 1, "placement": 0, "policy": LIST_FUSED, "S": 1, "cuts": [0, 2]},
                         [[(0, 0, j) for j in range(4)] + [(1, 0, j) for j in range(4)]])
     assert r["moves"] == 2 and r["status"] == 0 and r["makespan"] == 24
+
+
+def test_eval_lists_shared_and_reordered_task_ranges(ctx):
+    """Plans may share one task range or list their ranges out of order (ADVICE
+    r1: the device copy is sized by the largest range end, not by the last
+    plan's): results equal each plan evaluated alone."""
+    from paper_2509_23722_b200 import adaptis as A
+    import ctypes as C
+    pr, sp = W.config(1)
+    prep = ctx.prepare(pr, sp)
+    L, p = len(pr.t_f), pr.p
+    plans = [{"v": 1, "placement": 0, "policy": 4, "S": 2, "cuts": [0, c, L]} for c in (2, 4, 6)]
+    fused, lists = realised(pr, 1, 0, 2, [4])
+    tasks, one = A.Prepared._task_arrays([lists], p)
+    n = len(plans)
+    for offs in (np.tile(one, n),                                   # one shared range
+                 np.concatenate([one + len(tasks), one, one])):      # first plan points past the others
+        big = np.concatenate([tasks, tasks]) if offs[0] > 0 else tasks
+        out = A._host_results(n)
+        soa = A._soa_from_numpy(out)
+        A._check(A.lib().adaptis_eval_lists(ctx.ptr, prep.ptr, A.make_plans(plans), big.ctypes.data,
+                                            offs.astype(np.uint64).ctypes.data_as(C.POINTER(C.c_uint64)),
+                                            n, C.byref(soa), None), ctx.ptr)
+        for i, pl in enumerate(plans):
+            alone = prep.eval_lists([pl], [lists])
+            assert int(out["status"][i]) == int(alone["status"][0])
+            assert int(out["makespan"][i]) == int(alone["makespan"][0])
