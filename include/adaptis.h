@@ -382,6 +382,22 @@ ADAPTIS_API adaptis_status adaptis_eval_plans(adaptis_ctx* ctx, adaptis_prepared
                                               const adaptis_plan* plans, uint64_t n,
                                               const adaptis_results_soa* out, int64_t* report);
 
+/* Contention on realised orders (Alg. 1 Step 3 with SPEC S:206 (a)/(c) and
+ * S:232; reading R36 in DESIGN.md): every candidate's policy decides its
+ * per-device order with pure-latency communication (R3-R6); that order is
+ * then executed as an explicit schedule (R30) under send/receive-engine
+ * contention (R34), on the GPU in batches (the policy kernels with traces, a
+ * conversion kernel and the contention kernel). adaptis_eval_contended writes
+ * per-candidate results for [first, first + count) to host arrays `out`
+ * (candidates without a complete order keep their policy status 1 or 3);
+ * adaptis_search_contended is the argmin of Eq. 1-2 over the contended
+ * makespans (lowest index among ties, R18) on this context's GPU, with the
+ * winner's T_d / busy_d / M_d. EOVERFLOW if the serial bound reaches 2^40
+ * ticks; not in FP32 cost mode. */
+ADAPTIS_API adaptis_status adaptis_eval_contended(adaptis_ctx* ctx, adaptis_prepared* prep, uint64_t first,
+                                                  uint64_t count, const adaptis_results_soa* out);
+ADAPTIS_API adaptis_status adaptis_search_contended(adaptis_ctx* ctx, adaptis_prepared* prep, adaptis_best* out);
+
 /* Realised workload scheduling results of one policy plan ("workload
  * scheduling results"; the Executor's compute-instruction lists): the
  * order in which each device executes its tasks under the plan's policy, as

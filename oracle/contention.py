@@ -193,3 +193,18 @@ def simulate_lists_contended(pr, v, placement, fused, cuts, lists, trace=False):
         res["tasks"] = task_iv
         res["transfers"] = xfer_iv
     return res
+
+
+def simulate_realised_contended(pr, v, placement, policy, cuts):
+    """Reading R36 (contention on realised orders): the policy decides each
+    device's order with pure-latency communication (the event loop, R9-R14);
+    that order is then executed as an explicit schedule (R30) under the R34
+    send/receive engines. Candidates without a complete order (invalid cuts,
+    stuck GREEDY) keep the event loop's status."""
+    from . import oracle as O
+    r = O.simulate(pr, v, placement, policy, cuts, trace=True)
+    if r["status"] not in (0, 2):
+        return {"status": r["status"], "makespan": O.INT64_MAX, "peak_mem": 0}
+    fused = policy in (0, 1)
+    lists = [[(k, s, j) for (k, s, j, _t) in lst if not (fused and k == 2)] for lst in r["trace"]]
+    return simulate_lists_contended(pr, v, placement, fused, cuts, lists)

@@ -191,6 +191,11 @@ def lib():
                                                C.POINTER(C.c_uint64), C.c_int32, C.c_void_p,
                                                C.POINTER(_Result), C.POINTER(C.c_int32),
                                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+            L.adaptis_eval_contended.restype = st
+            L.adaptis_eval_contended.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                                 C.POINTER(_ResultsSoa)]
+            L.adaptis_search_contended.restype = st
+            L.adaptis_search_contended.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Best)]
             L.adaptis_realize_lists.restype = st
             L.adaptis_realize_lists.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Plan), C.c_void_p,
                                                 C.c_uint64, C.POINTER(C.c_uint64)]
@@ -569,6 +574,22 @@ class Prepared:
                for d in range(p)]
         return {"lists": rep, "moves": int(nm.value), "status": int(res.status),
                 "makespan": int(res.makespan), "peak_mem": int(res.peak_mem_bytes)}
+
+    def eval_contended(self, first: int, count: int) -> dict:
+        """adaptis_eval_contended (R36): results of [first, first + count) when each
+        candidate's realised order runs under send/receive-engine contention."""
+        out = _host_results(count)
+        soa = _soa_from_numpy(out)
+        _check(lib().adaptis_eval_contended(self.ctx.ptr, self.ptr, first, count, C.byref(soa)), self.ctx.ptr)
+        return out
+
+    def search_contended(self) -> dict:
+        """adaptis_search_contended (R36): the argmin of the contended makespans."""
+        b = _Best()
+        st = lib().adaptis_search_contended(self.ctx.ptr, self.ptr, C.byref(b))
+        if st not in (OK, EINFEASIBLE):
+            raise AdaptisError(st, _err(self.ctx.ptr))
+        return _best_dict(b, st, self.ctx.ptr)
 
     def realize_lists(self, plan) -> list:
         """adaptis_realize_lists: the plan's realised per-device orders (R30 lists

@@ -32,6 +32,7 @@
 // the producer's finish otherwise.
 #include <cstdint>
 
+#include "adaptis_decode.cuh"
 #include "adaptis_internal.h"
 
 namespace adaptis {
@@ -386,6 +387,90 @@ int launch_contend(const int64_t* cols, const int64_t* comm, int L, int p, int m
     if (e != cudaSuccess) return (int)e;
   }
   contend_kernel<<<grid, kCWarps * 32, smem, (cudaStream_t)stream>>>(A, p2, Sm);
+  return (int)cudaGetLastError();
+}
+
+// ---- contention on realised orders (reading R36): candidates of one segment
+// whose policy run (pure latency, R3-R6) was traced become explicit schedules
+// (R30) for the contention kernel. One warp per candidate: the candidate's
+// cuts are decoded (R19), its traced per-device orders are copied to a
+// contiguous list, and kept candidates are compacted through an atomic slot.
+__global__ void realised_lists_kernel(const TraceEntry* __restrict__ trace, const int* __restrict__ trace_n,
+                                      int cap_t, int p, uint64_t n, uint64_t first,
+                                      const uint8_t* __restrict__ status, RealisedSeg seg,
+                                      adaptis_plan* __restrict__ plans, adaptis_task* __restrict__ tasks,
+                                      uint64_t* __restrict__ offsets, uint64_t* __restrict__ slot_idx,
+                                      unsigned int* __restrict__ n_kept) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t o = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (o >= n) return;
+  const uint8_t st = status[o];
+  if (st != ADAPTIS_CAND_OK && st != ADAPTIS_CAND_OVER_CAP) return;  // invalid / stuck: no full order
+  unsigned int k = 0;
+  if (lane == 0) k = atomicAdd(n_kept, 1u);
+  k = __shfl_sync(0xffffffffu, k, 0);
+  const uint64_t tb = (uint64_t)k * p * cap_t;  // this candidate's task range
+  if (lane == 0) {
+    adaptis_plan pl;
+    pl.v = seg.v; pl.placement = seg.placement; pl.S = seg.S;
+    pl.policy = seg.fused ? ADAPTIS_LIST_FUSED : ADAPTIS_LIST;
+    decode_cuts(seg.binom, seg.ball, seg.seeds, seg.group, seg.part_mode, seg.radius, seg.S, seg.L,
+                first + o - seg.base, pl.cuts);
+    plans[k] = pl;
+    slot_idx[k] = o;
+    uint64_t off = tb;
+    for (int d = 0; d < p; ++d) {
+      offsets[(uint64_t)k * (p + 1) + d] = off;
+      off += (uint64_t)min(trace_n[o * p + d], cap_t);
+    }
+    offsets[(uint64_t)k * (p + 1) + p] = off;
+  }
+  __syncwarp();
+  uint64_t off = tb;
+  for (int d = 0; d < p; ++d) {
+    const int nt = min(trace_n[o * p + d], cap_t);
+    const TraceEntry* e = trace + (o * p + d) * (uint64_t)cap_t;
+    for (int i = lane; i < nt; i += 32) {
+      adaptis_task t;
+      t.kind = e[i].kind; t.stage = e[i].stage; t.mb = e[i].mb;
+      tasks[off + i] = t;
+    }
+    off += (uint64_t)nt;
+  }
+}
+
+// packed argmin key of the contended results (R18: lowest index among equal
+// makespans), folded into *key with one atomicMin per warp
+__global__ void contended_key_kernel(const int64_t* __restrict__ makespan, const uint8_t* __restrict__ status,
+                                     const uint64_t* __restrict__ slot_idx, uint64_t n, uint64_t first,
+                                     int key_bits, unsigned long long* key) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long v = ~0ull >> 1;
+  if (k < n && status[k] == ADAPTIS_CAND_OK)
+    v = ((unsigned long long)makespan[k] << key_bits) | (first + slot_idx[k]);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = x < v ? x : v;
+  }
+  if ((threadIdx.x & 31) == 0 && v != (~0ull >> 1)) atomicMin(key, v);
+}
+
+int launch_realised_lists(const TraceEntry* trace, const int* trace_n, int trace_cap, int p, uint64_t n,
+                          uint64_t first, const uint8_t* status, const RealisedSeg& seg, adaptis_plan* plans,
+                          adaptis_task* tasks, uint64_t* offsets, uint64_t* slot_idx, unsigned int* n_kept,
+                          void* stream) {
+  if (n == 0) return 0;
+  const uint64_t threads = n * 32;
+  realised_lists_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      trace, trace_n, trace_cap, p, n, first, status, seg, plans, tasks, offsets, slot_idx, n_kept);
+  return (int)cudaGetLastError();
+}
+
+int launch_contended_key(const int64_t* makespan, const uint8_t* status, const uint64_t* slot_idx, uint64_t n,
+                         uint64_t first, int key_bits, unsigned long long* key, void* stream) {
+  if (n == 0) return 0;
+  contended_key_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(makespan, status, slot_idx,
+                                                                                     n, first, key_bits, key);
   return (int)cudaGetLastError();
 }
 

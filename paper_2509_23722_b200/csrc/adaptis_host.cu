@@ -1158,6 +1158,211 @@ adaptis_status adaptis_eval_batch(adaptis_ctx* ctx, const adaptis_problem* probl
   return st;
 }
 
+// ---- contention on realised orders (reading R36): every candidate's policy
+// order is realised by its policy kernel with pure-latency communication
+// (R3-R6, a traced report launch) and then executed as an explicit schedule
+// (R30) under send/receive-engine contention (R34), in batches per segment.
+// search: the packed argmin key of the contended makespans lands in *d_key;
+// eval: host results at [idx - lo] (status 1 / 3 from the policy run for
+// candidates without a complete order).
+static adaptis_status run_contended(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t lo, uint64_t hi, bool search,
+                                    const adaptis_results_soa* hout, unsigned long long* d_key, float* kernel_ms,
+                                    uint64_t* n_tasks, int64_t* report_one) {
+  if (P->tick == kTickF32) return fail(ctx, ADAPTIS_EINVAL, "FP32 cost mode is not supported under contention");
+  const int p = P->p, m = P->m, L = P->L;
+  {
+    long double bound = 0;  // the contention kernel's transfer keys hold eligibility times < 2^40
+    for (int l = 0; l < L; ++l)
+      bound += (long double)m * (P->h_cols[(size_t)kColTF * L + l] + P->h_cols[(size_t)kColTB * L + l] +
+                                 P->h_cols[(size_t)kColTW * L + l]) + 2.0L * m * P->h_comm[l];
+    if (bound >= (long double)(1ull << 40))
+      return fail(ctx, ADAPTIS_EOVERFLOW, "serial bound %.0Lf ticks >= 2^40 (contention keys)", bound);
+  }
+  CU(ctx, cudaSetDevice(ctx->device));
+  float ms_total = 0;
+  uint64_t tasks_total = 0;
+  for (const Seg& sg : P->segs) {
+    const uint64_t a0 = std::max(lo, sg.base), b0 = std::min(hi, sg.base + sg.count);
+    if (a0 >= b0) continue;
+    const bool fused = sg.policy == ADAPTIS_GPIPE || sg.policy == ADAPTIS_ONEF1B;
+    const int cap_t = 3 * m * sg.v;
+    const uint64_t stride = (uint64_t)5 * sg.S * m;
+    const uint64_t per = (uint64_t)p * cap_t * (sizeof(TraceEntry) + sizeof(adaptis_task)) + stride * 8 +
+                         (uint64_t)p * 48 + 64;
+    const uint64_t B = std::max<uint64_t>(256, std::min<uint64_t>(65536, ((uint64_t)3 << 29) / per));
+    RealisedSeg rs{P->d_binom, P->d_ball, P->d_seeds, sg.group, sg.part_mode, sg.radius, sg.S, L,
+                   sg.v, sg.placement, fused ? 1 : 0, sg.base};
+    for (uint64_t a = a0; a < b0; a += B) {
+      const uint64_t n = std::min(B, b0 - a);
+      TraceEntry* d_tr = nullptr; int* d_trn = nullptr; uint8_t* d_pst = nullptr; int64_t* d_rep = nullptr;
+      adaptis_plan* d_plans = nullptr; adaptis_task* d_tasks = nullptr; uint64_t *d_off = nullptr, *d_slot = nullptr;
+      unsigned int* d_nk = nullptr; int64_t *d_scr = nullptr, *d_mk = nullptr, *d_pk = nullptr, *d_crep = nullptr;
+      float* d_bub = nullptr; uint8_t* d_st = nullptr; unsigned long long* d_nt = nullptr;
+      auto cleanup = [&]() {
+        cudaFree(d_tr); cudaFree(d_trn); cudaFree(d_pst); cudaFree(d_rep); cudaFree(d_plans); cudaFree(d_tasks);
+        cudaFree(d_off); cudaFree(d_slot); cudaFree(d_nk); cudaFree(d_scr); cudaFree(d_mk); cudaFree(d_pk);
+        cudaFree(d_crep); cudaFree(d_bub); cudaFree(d_st); cudaFree(d_nt);
+      };
+#define CUR(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { cleanup(); \
+    return fail(ctx, ADAPTIS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
+      CUR(cudaMalloc(&d_tr, n * p * cap_t * sizeof(TraceEntry)));
+      CUR(cudaMalloc(&d_trn, n * p * sizeof(int)));
+      CUR(cudaMalloc(&d_pst, n));
+      CUR(cudaMalloc(&d_rep, n * 5 * p * 8));
+      CUR(cudaMalloc(&d_plans, n * sizeof(adaptis_plan)));
+      CUR(cudaMalloc(&d_tasks, n * p * cap_t * sizeof(adaptis_task)));
+      CUR(cudaMalloc(&d_off, n * (p + 1) * 8));
+      CUR(cudaMalloc(&d_slot, n * 8));
+      CUR(cudaMalloc(&d_nk, 4));
+      CUR(cudaMalloc(&d_scr, n * stride * 8));
+      CUR(cudaMalloc(&d_mk, n * 8));
+      CUR(cudaMalloc(&d_pk, n * 8));
+      CUR(cudaMalloc(&d_bub, n * 4));
+      CUR(cudaMalloc(&d_st, n));
+      CUR(cudaMalloc(&d_nt, 8));
+      if (report_one) CUR(cudaMalloc(&d_crep, n * 5 * p * 8));
+      CUR(cudaMemsetAsync(d_trn, 0, n * p * sizeof(int), ctx->stream));
+      CUR(cudaMemsetAsync(d_rep, 0, n * 5 * p * 8, ctx->stream));
+      CUR(cudaMemsetAsync(d_nk, 0, 4, ctx->stream));
+      CUR(cudaMemsetAsync(d_nt, 0, 8, ctx->stream));
+      // (1) the policy run with traces (pure latency): the realised orders
+      TraceBuf tb;
+      tb.trace = d_tr; tb.trace_n = d_trn; tb.cap = cap_t;
+      adaptis_results_soa pso{nullptr, nullptr, nullptr, d_pst, nullptr};
+      float t1 = 0;
+      adaptis_status st = run_range(ctx, P, a, a + n, false, 0, 1, &pso, a, d_rep, &t1, false, &tb);
+      if (st != ADAPTIS_OK) { cleanup(); return st; }
+      tasks_total += ctx->last_tasks;
+      CUR(cudaEventRecord(ctx->ev0, ctx->stream));
+      // (2) the orders as explicit schedules, compacted
+      int e = launch_realised_lists(d_tr, d_trn, cap_t, p, n, a, d_pst, rs, d_plans, d_tasks, d_off, d_slot,
+                                    d_nk, ctx->stream);
+      if (e) { cleanup(); return fail(ctx, ADAPTIS_ECUDA, "realised lists: %s", cudaGetErrorString((cudaError_t)e)); }
+      unsigned int nk = 0;
+      CUR(cudaMemcpyAsync(&nk, d_nk, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CUR(cudaStreamSynchronize(ctx->stream));
+      // (3) contention (R34) on them, (4) the argmin key or the results
+      e = launch_contend(P->d_cols, P->d_comm, L, p, m, P->cap, nk, d_plans, d_tasks, d_off, d_scr, stride, d_mk,
+                         d_pk, d_bub, d_st, d_crep, d_nt, sg.S, ctx->stream);
+      if (e) { cleanup(); return fail(ctx, ADAPTIS_ECUDA, "contention kernel: %s", cudaGetErrorString((cudaError_t)e)); }
+      if (search) {
+        e = launch_contended_key(d_mk, d_st, d_slot, nk, a, P->key_bits, d_key, ctx->stream);
+        if (e) { cleanup(); return fail(ctx, ADAPTIS_ECUDA, "contended key: %s", cudaGetErrorString((cudaError_t)e)); }
+      }
+      CUR(cudaEventRecord(ctx->ev1, ctx->stream));
+      ctx->launches += 3;
+      unsigned long long nt = 0;
+      CUR(cudaMemcpyAsync(&nt, d_nt, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      if (!search && hout) {
+        std::vector<uint8_t> pst(n), cst(nk);
+        std::vector<int64_t> mk(nk), pk(nk);
+        std::vector<float> bub(nk);
+        std::vector<uint64_t> slot(nk);
+        CUR(cudaMemcpyAsync(pst.data(), d_pst, n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (nk) {
+          CUR(cudaMemcpyAsync(cst.data(), d_st, nk, cudaMemcpyDeviceToHost, ctx->stream));
+          CUR(cudaMemcpyAsync(mk.data(), d_mk, nk * 8, cudaMemcpyDeviceToHost, ctx->stream));
+          CUR(cudaMemcpyAsync(pk.data(), d_pk, nk * 8, cudaMemcpyDeviceToHost, ctx->stream));
+          CUR(cudaMemcpyAsync(bub.data(), d_bub, nk * 4, cudaMemcpyDeviceToHost, ctx->stream));
+          CUR(cudaMemcpyAsync(slot.data(), d_slot, nk * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        if (report_one && nk) CUR(cudaMemcpyAsync(report_one, d_crep, 5 * p * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CUR(cudaStreamSynchronize(ctx->stream));
+        for (uint64_t i = 0; i < n; ++i) {  // no complete order: the policy run's status
+          const uint64_t o = a + i - lo;
+          if (hout->status) hout->status[o] = pst[i];
+          if (hout->makespan) hout->makespan[o] = INT64_MAX;
+          if (hout->peak_mem_bytes) hout->peak_mem_bytes[o] = 0;
+          if (hout->bubble_ratio) hout->bubble_ratio[o] = 0.0f;
+          if (hout->makespan_f32) hout->makespan_f32[o] = INFINITY;
+        }
+        for (unsigned int k = 0; k < nk; ++k) {
+          const uint64_t o = a + slot[k] - lo;
+          if (hout->status) hout->status[o] = cst[k];
+          if (hout->makespan) hout->makespan[o] = mk[k];
+          if (hout->peak_mem_bytes) hout->peak_mem_bytes[o] = pk[k];
+          if (hout->bubble_ratio) hout->bubble_ratio[o] = bub[k];
+          if (hout->makespan_f32) hout->makespan_f32[o] = cst[k] == 0 ? (float)mk[k] : INFINITY;
+        }
+      } else {
+        CUR(cudaStreamSynchronize(ctx->stream));
+      }
+      float t2 = 0;
+      cudaEventElapsedTime(&t2, ctx->ev0, ctx->ev1);
+      ms_total += t1 + t2;
+      tasks_total += nt;
+#undef CUR
+      cleanup();
+    }
+  }
+  if (kernel_ms) *kernel_ms = ms_total;
+  if (n_tasks) *n_tasks = tasks_total;
+  return ADAPTIS_OK;
+}
+
+adaptis_status adaptis_eval_contended(adaptis_ctx* ctx, adaptis_prepared* P, uint64_t first, uint64_t count,
+                                      const adaptis_results_soa* out) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");
+  if (first > P->N || count > P->N - first)
+    return fail(ctx, ADAPTIS_EINVAL, "range [%llu, +%llu) exceeds |space| = %llu", (unsigned long long)first,
+                (unsigned long long)count, (unsigned long long)P->N);
+  if (count == 0) return ADAPTIS_OK;
+  float ms = 0; uint64_t nt = 0;
+  adaptis_status st = run_contended(ctx, P, first, first + count, false, out, nullptr, &ms, &nt, nullptr);
+  ctx->last_tasks = nt;
+  return st;
+}
+
+adaptis_status adaptis_search_contended(adaptis_ctx* ctx, adaptis_prepared* P, adaptis_best* out) {
+  if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
+  if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");
+  CU(ctx, cudaSetDevice(ctx->device));
+  memset(out, 0, sizeof(*out));
+  adaptis_status st = ensure_scratch(ctx, kHdr + kSegWords, kOverflowPerSeg);
+  if (st != ADAPTIS_OK) return st;
+  const unsigned long long inf = ~0ull >> 1;
+  CU(ctx, cudaMemcpyAsync(ctx->d_scratch, &inf, 8, cudaMemcpyHostToDevice, ctx->stream));
+  float ms = 0; uint64_t nt = 0;
+  st = run_contended(ctx, P, 0, P->N, true, nullptr, ctx->d_scratch, &ms, &nt, nullptr);
+  if (st != ADAPTIS_OK) return st;
+  unsigned long long key = 0;
+  CU(ctx, cudaMemcpyAsync(&key, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  out->kernel_ms = ms;
+  out->n_tasks = nt;
+  out->n_candidates = P->N;
+  out->p = P->p;
+  if (key == inf) {
+    out->index = UINT64_MAX;
+    out->result.makespan = INT64_MAX;
+    return fail(ctx, ADAPTIS_EINFEASIBLE, "no candidate satisfies the memory constraint (Eq. 2)");
+  }
+  const uint64_t idx = key & ((1ull << P->key_bits) - 1);
+  out->index = idx;
+  fill_plan(*P, idx, &out->plan, nullptr);
+  // the winner's contended result and per-device report
+  int64_t mk = 0, pk = 0; float bub = 0, mkf = 0; uint8_t stt = 0;
+  std::vector<int64_t> rep(5 * P->p, 0);
+  adaptis_results_soa ho{&mk, &pk, &bub, &stt, &mkf};
+  st = run_contended(ctx, P, idx, idx + 1, false, &ho, nullptr, nullptr, nullptr, rep.data());
+  if (st != ADAPTIS_OK) return st;
+  out->result.makespan = mk;
+  out->result.peak_mem_bytes = pk;
+  out->result.bubble_ratio = bub;
+  out->result.status = stt;
+  out->result.makespan_f32 = (float)mk;
+  out->result.throughput = (mk > 0 && P->tick_seconds > 0)
+      ? (double)P->m * (double)P->tokens_per_mb / ((double)mk * P->tick_seconds) : 0.0;
+  for (int d = 0; d < P->p; ++d) {
+    out->T_d[d] = rep[d]; out->busy_d[d] = rep[P->p + d]; out->M_d[d] = rep[2 * P->p + d];
+  }
+  if (stt != ADAPTIS_CAND_OK || mk != (int64_t)(key >> P->key_bits))
+    return fail(ctx, ADAPTIS_ECUDA, "contended winner re-evaluation disagrees (index %llu: %llu vs %lld)",
+                (unsigned long long)idx, (unsigned long long)(key >> P->key_bits), (long long)mk);
+  return ADAPTIS_OK;
+}
+
 adaptis_status adaptis_search_prepared(adaptis_ctx* ctx, adaptis_prepared* P, adaptis_best* out) {
   if (!ctx || !P) return fail(ctx, ADAPTIS_EINVAL, "ctx or prepared is NULL");
   if (!out) return fail(ctx, ADAPTIS_EINVAL, "out is NULL");

@@ -157,6 +157,20 @@ int launch_contend(const int64_t* cols, const int64_t* comm, int L, int p, int m
                    const adaptis_plan* plans, const adaptis_task* tasks, const uint64_t* offsets,
                    int64_t* scratch, uint64_t stride, int64_t* makespan, int64_t* peak, float* bubble,
                    uint8_t* status, int64_t* report, unsigned long long* n_tasks, int Sm, void* stream);
+// R36 (contention on realised orders): a segment's decode tables and shape
+struct RealisedSeg {
+  const uint64_t* binom;
+  const uint64_t* ball;
+  const int16_t* seeds;
+  int group, part_mode, radius, S, L, v, placement, fused;
+  uint64_t base;  // global index of the segment's first candidate
+};
+int launch_realised_lists(const TraceEntry* trace, const int* trace_n, int trace_cap, int p, uint64_t n,
+                          uint64_t first, const uint8_t* status, const RealisedSeg& seg, adaptis_plan* plans,
+                          adaptis_task* tasks, uint64_t* offsets, uint64_t* slot_idx, unsigned int* n_kept,
+                          void* stream);
+int launch_contended_key(const int64_t* makespan, const uint8_t* status, const uint64_t* slot_idx, uint64_t n,
+                         uint64_t first, int key_bits, unsigned long long* key, void* stream);
 int occupancy_ctas_per_sm(const SegLaunch& s, bool fallback);
 // sequential GREEDY kernel (adaptis_seqg.cu): one thread per candidate
 bool seqg_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int min_warps);
