@@ -424,6 +424,27 @@ def main():
             (best["index"], best["makespan"]) == (g["index"], g["makespan"])
         line["cfg5"] = cfg5
         line["generator"] = gen
+        # §8(f) f1 / R36: the whole cfg2 space searched with every candidate's realised
+        # order executed under send/receive-engine contention (one GPU)
+        if world == 1:
+            try:
+                pr2, sp2 = W.config(2)
+                prep2 = ctx.prepare(pr2, sp2)
+                prep2.search_contended()  # warm
+                t = time.perf_counter()
+                bc = prep2.search_contended()
+                wall = 1000 * (time.perf_counter() - t)
+                bl = prep2.search()
+                line["contended_search"] = {
+                    "workload": CONFIG_NAMES[2], "candidates": prep2.N, "wall_ms": wall,
+                    "kernel_ms": bc["kernel_ms"], "tasks": bc["n_tasks"],
+                    "winner": {"index": bc["index"], "makespan_ticks": bc["makespan"], "plan": bc["plan"]},
+                    "latency_only_winner": {"index": bl["index"], "makespan_ticks": bl["makespan"]},
+                    "note": "R36: policy order realised with pure latency, then executed under FIFO "
+                            "send/receive engines (R34); single GPU"}
+                prep2.close()
+            except Exception as e:  # reported, never silently replaced
+                line["contended_search"] = {"error": repr(e)}
         # §8(f) f1 / R34: explicit cfg3-shaped schedules under send/receive-engine
         # contention (adaptis_eval_lists_contended), latencies x100 so transfers queue
         try:

@@ -106,7 +106,7 @@ struct adaptis_ctx {
 // winner report block behind the five report rows: makespan, peak, fp32
 // makespan, bubble, status (one allocation and one D2H per search)
 constexpr size_t kReportBytes = 5 * ADAPTIS_MAX_P * 8;
-constexpr size_t kWinBytes = 32;
+constexpr size_t kWinBytes = 40;  // + the contended search's key word at +32
 
 namespace {
 
@@ -432,6 +432,17 @@ void shard(uint64_t lo, uint64_t hi, int rank, int world, SegLaunch* s) {
 }
 
 constexpr size_t kOverflowPerSeg = 1u << 20;
+// overflow list capacity of one job: the fixed orders' 8-slot shared rings can
+// overflow on a large share of a segment (cfg5's v = 2 ZB: 38 %), so their lists
+// hold up to 2^26 positions (512 MB) and only the overflowed candidates are
+// re-run; beyond that (and for the other policies beyond 2^20) the whole shard
+// is re-run in fallback mode
+size_t overflow_cap_of(const SegLaunch& s) {
+  if (const char* e = getenv("ADAPTIS_OVERFLOW_CAP"))  // test hook: exercise the whole-shard re-run
+    return (size_t)std::min<uint64_t>(s.n_pos, (uint64_t)std::max(1, atoi(e)));
+  const bool ringed = s.policy == ADAPTIS_ZB || s.policy == ADAPTIS_ONEF1B;
+  return (size_t)std::min<uint64_t>(s.n_pos, ringed ? (1ull << 26) : kOverflowPerSeg);
+}
 
 // fast-path ring slots per stage and direction: GREEDY's F-first rule lets a
 // producer run further ahead than the fixed orders do (DESIGN.md §"Rings")
@@ -528,7 +539,9 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
                         const TraceBuf* tb = nullptr) {
   const size_t nseg = jobs.size();
   const size_t nwords = kHdr + kSegWords * std::max<size_t>(nseg, 1);
-  adaptis_status st = ensure_scratch(ctx, nwords, kOverflowPerSeg * std::max<size_t>(nseg, 1));
+  std::vector<size_t> ov_off(nseg + 1, 0);
+  for (size_t i = 0; i < nseg; ++i) ov_off[i + 1] = ov_off[i] + overflow_cap_of(jobs[i].s);
+  adaptis_status st = ensure_scratch(ctx, nwords, std::max<size_t>(ov_off[nseg], 1));
   if (st != ADAPTIS_OK) return st;
   while (ctx->seg_events.size() < 2 * nseg) {
     cudaEvent_t e;
@@ -559,8 +572,8 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
     if (tb && P->tick != kTickF32) { s.trace = tb->trace; s.trace_n = tb->trace_n; s.trace_cap = tb->cap; }
     s.cursor = sw + 0;
     s.overflow_count = reinterpret_cast<unsigned int*>(sw + 1);
-    s.overflow_idx = ctx->d_overflow + kOverflowPerSeg * i;
-    s.overflow_cap = (unsigned)kOverflowPerSeg;
+    s.overflow_idx = ctx->d_overflow + ov_off[i];
+    s.overflow_cap = (unsigned)(ov_off[i + 1] - ov_off[i]);
     s.n_invalid = sw + 5;
     s.n_tasks = sw + 2;
     s.n_rounds = W + 3;
@@ -617,7 +630,7 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
     int K = 1;
     while (K < P->m) K <<= 1;
     s.ring_k = K;
-    if (cnt <= kOverflowPerSeg) {
+    if (cnt <= jobs[i].s.overflow_cap) {
       if (s.list_slot) s.list_slot = s.overflow_idx;  // explicit-index mode records slots
       else s.list_idx = s.overflow_idx;
       s.n_pos = cnt;
@@ -655,7 +668,7 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
     const unsigned long long* jw = words.data() + kHdr + kSegWords * i;
     // a whole-shard fallback re-counted every candidate of the job: its counts
     // replace the first pass's; a list fallback only saw the overflowed ones
-    const bool whole = active[i] == 2 && (jw[1] & 0xffffffffu) > kOverflowPerSeg;
+    const bool whole = active[i] == 2 && (jw[1] & 0xffffffffu) > jobs[i].s.overflow_cap;
     const uint64_t jt = whole ? jw[9] : jw[2] + jw[9];
     invalid += whole ? jw[7] : jw[5] + jw[7];
     pruned += whole ? jw[8] : jw[6] + jw[8];
@@ -1189,22 +1202,22 @@ static adaptis_status run_contended(adaptis_ctx* ctx, adaptis_prepared* P, uint6
     const uint64_t stride = (uint64_t)5 * sg.S * m;
     const uint64_t per = (uint64_t)p * cap_t * (sizeof(TraceEntry) + sizeof(adaptis_task)) + stride * 8 +
                          (uint64_t)p * 48 + 64;
-    const uint64_t B = std::max<uint64_t>(256, std::min<uint64_t>(65536, ((uint64_t)3 << 29) / per));
+    const uint64_t B = std::max<uint64_t>(256, std::min<uint64_t>(65536, ((uint64_t)1 << 32) / per));
     RealisedSeg rs{P->d_binom, P->d_ball, P->d_seeds, sg.group, sg.part_mode, sg.radius, sg.S, L,
                    sg.v, sg.placement, fused ? 1 : 0, sg.base};
-    for (uint64_t a = a0; a < b0; a += B) {
-      const uint64_t n = std::min(B, b0 - a);
-      TraceEntry* d_tr = nullptr; int* d_trn = nullptr; uint8_t* d_pst = nullptr; int64_t* d_rep = nullptr;
-      adaptis_plan* d_plans = nullptr; adaptis_task* d_tasks = nullptr; uint64_t *d_off = nullptr, *d_slot = nullptr;
-      unsigned int* d_nk = nullptr; int64_t *d_scr = nullptr, *d_mk = nullptr, *d_pk = nullptr, *d_crep = nullptr;
-      float* d_bub = nullptr; uint8_t* d_st = nullptr; unsigned long long* d_nt = nullptr;
-      auto cleanup = [&]() {
-        cudaFree(d_tr); cudaFree(d_trn); cudaFree(d_pst); cudaFree(d_rep); cudaFree(d_plans); cudaFree(d_tasks);
-        cudaFree(d_off); cudaFree(d_slot); cudaFree(d_nk); cudaFree(d_scr); cudaFree(d_mk); cudaFree(d_pk);
-        cudaFree(d_crep); cudaFree(d_bub); cudaFree(d_st); cudaFree(d_nt);
-      };
+    const uint64_t n = std::min(B, b0 - a0);  // buffers for the segment's largest batch, reused
+    TraceEntry* d_tr = nullptr; int* d_trn = nullptr; uint8_t* d_pst = nullptr; int64_t* d_rep = nullptr;
+    adaptis_plan* d_plans = nullptr; adaptis_task* d_tasks = nullptr; uint64_t *d_off = nullptr, *d_slot = nullptr;
+    unsigned int* d_nk = nullptr; int64_t *d_scr = nullptr, *d_mk = nullptr, *d_pk = nullptr, *d_crep = nullptr;
+    float* d_bub = nullptr; uint8_t* d_st = nullptr; unsigned long long* d_nt = nullptr;
+    auto cleanup = [&]() {
+      cudaFree(d_tr); cudaFree(d_trn); cudaFree(d_pst); cudaFree(d_rep); cudaFree(d_plans); cudaFree(d_tasks);
+      cudaFree(d_off); cudaFree(d_slot); cudaFree(d_nk); cudaFree(d_scr); cudaFree(d_mk); cudaFree(d_pk);
+      cudaFree(d_crep); cudaFree(d_bub); cudaFree(d_st); cudaFree(d_nt);
+    };
 #define CUR(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { cleanup(); \
     return fail(ctx, ADAPTIS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
+    {
       CUR(cudaMalloc(&d_tr, n * p * cap_t * sizeof(TraceEntry)));
       CUR(cudaMalloc(&d_trn, n * p * sizeof(int)));
       CUR(cudaMalloc(&d_pst, n));
@@ -1221,6 +1234,9 @@ static adaptis_status run_contended(adaptis_ctx* ctx, adaptis_prepared* P, uint6
       CUR(cudaMalloc(&d_st, n));
       CUR(cudaMalloc(&d_nt, 8));
       if (report_one) CUR(cudaMalloc(&d_crep, n * 5 * p * 8));
+    }
+    for (uint64_t a = a0; a < b0; a += B) {
+      const uint64_t n = std::min(B, b0 - a);
       CUR(cudaMemsetAsync(d_trn, 0, n * p * sizeof(int), ctx->stream));
       CUR(cudaMemsetAsync(d_rep, 0, n * 5 * p * 8, ctx->stream));
       CUR(cudaMemsetAsync(d_nk, 0, 4, ctx->stream));
@@ -1291,9 +1307,9 @@ static adaptis_status run_contended(adaptis_ctx* ctx, adaptis_prepared* P, uint6
       cudaEventElapsedTime(&t2, ctx->ev0, ctx->ev1);
       ms_total += t1 + t2;
       tasks_total += nt;
-#undef CUR
-      cleanup();
     }
+#undef CUR
+    cleanup();
   }
   if (kernel_ms) *kernel_ms = ms_total;
   if (n_tasks) *n_tasks = tasks_total;
@@ -1321,13 +1337,16 @@ adaptis_status adaptis_search_contended(adaptis_ctx* ctx, adaptis_prepared* P, a
   memset(out, 0, sizeof(*out));
   adaptis_status st = ensure_scratch(ctx, kHdr + kSegWords, kOverflowPerSeg);
   if (st != ADAPTIS_OK) return st;
+  // the key lives apart from the scratch words, which every policy run resets
+  unsigned long long* d_key = reinterpret_cast<unsigned long long*>(
+      reinterpret_cast<unsigned char*>(ctx->d_report) + kReportBytes + 32);
   const unsigned long long inf = ~0ull >> 1;
-  CU(ctx, cudaMemcpyAsync(ctx->d_scratch, &inf, 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(d_key, &inf, 8, cudaMemcpyHostToDevice, ctx->stream));
   float ms = 0; uint64_t nt = 0;
-  st = run_contended(ctx, P, 0, P->N, true, nullptr, ctx->d_scratch, &ms, &nt, nullptr);
+  st = run_contended(ctx, P, 0, P->N, true, nullptr, d_key, &ms, &nt, nullptr);
   if (st != ADAPTIS_OK) return st;
   unsigned long long key = 0;
-  CU(ctx, cudaMemcpyAsync(&key, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(&key, d_key, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   out->kernel_ms = ms;
   out->n_tasks = nt;

@@ -100,18 +100,20 @@ def test_forced_fallback_matches_oracle(ctx, monkeypatch):
 
 
 def test_whole_shard_fallback_counts_once(ctx, monkeypatch):
-    """More than 2^20 overflowed candidates in one segment re-run the whole
-    segment shard in fallback mode. The winner still equals the oracle's, and
-    the invalid count is the oracle's exactly: the re-run's counts replace the
-    first pass's for that segment instead of adding to them."""
+    """More overflowed candidates than a segment's overflow list holds re-run the
+    whole segment shard in fallback mode (the list capacity is forced down to
+    4096 here). The winner still equals the oracle's, and the invalid count is
+    the oracle's exactly: the re-run's counts replace the first pass's for that
+    segment instead of adding to them."""
     monkeypatch.setenv("ADAPTIS_RING_K", "2")
+    monkeypatch.setenv("ADAPTIS_OVERFLOW_CAP", "4096")
     monkeypatch.setenv("ADAPTIS_NO_SEQ", "1")  # the lane-per-device kernels and their rings
     g = golden_argmin(3)
     pr, sp = W.config(3)
     b = ctx.search(pr, sp)
     assert (b["index"], b["makespan"]) == (g["index"], g["makespan"])
     assert b["n_invalid"] == g["n_invalid"]
-    assert max(li["fallback"] for li in ctx.launch_info()) > (1 << 20)
+    assert max(li["fallback"] for li in ctx.launch_info()) > 4096
 
 
 def test_eval_indices_fallback_matches_oracle(ctx, monkeypatch):
