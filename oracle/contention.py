@@ -200,7 +200,8 @@ def simulate_realised_contended(pr, v, placement, policy, cuts):
     device's order with pure-latency communication (the event loop, R9-R14);
     that order is then executed as an explicit schedule (R30) under the R34
     send/receive engines. Candidates without a complete order (invalid cuts,
-    stuck GREEDY) keep the event loop's status."""
+    stuck GREEDY) keep the event loop's status. `cuts` is the full list
+    [0, c_1, ..., L] (unambiguous also for invalid decodes)."""
     from . import oracle as O
     r = O.simulate(pr, v, placement, policy, cuts, trace=True)
     if r["status"] not in (0, 2):
