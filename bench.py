@@ -525,6 +525,7 @@ def roofline(seg_ms, seg_tasks, seg_n, config_id=None):
     tot_ms, tot_tasks = sum(seg_ms.values()), sum(seg_tasks.values())
     allk = ALG_INSTR_PER_TASK * tot_tasks / (tot_ms / 1e3) / 1e12
     name = "seqg_kernel<v=%d, %s>" % (k[0], PLACEMENT[k[1]]) if k[3] == 1 else \
+        "fixed_kernel<%s, v=%d> (%s placement)" % (POLICY[k[2]], k[0], PLACEMENT[k[1]]) if k[3] == 2 else \
         "seg_kernel<%s, v=%d> (%s placement)" % (POLICY[k[2]], k[0], PLACEMENT[k[1]])
     out.update(achieved=ach, frac=ach / peak, kernel=name,
                kernel_share_of_step=seg_ms[k] / tot_ms, tasks_per_launch=tasks,

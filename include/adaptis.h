@@ -228,7 +228,8 @@ typedef struct {
   uint64_t candidates;       /* candidates this launch evaluated                    */
   uint64_t tasks;            /* F/B/W tasks it simulated                             */
   float ms;                  /* device time of the launch (+ its fallback), CUDA events */
-  int32_t kernel;            /* 0 lane-per-device segment kernel, 1 sequential GREEDY */
+  int32_t kernel;            /* 0 lane-per-device segment kernel, 1 sequential GREEDY,
+                                 2 static-order kernel (GPIPE / ONEF1B / ZB)            */
 } adaptis_launch_info;
 /* Copies up to `max` records of the last evaluation into `out`; returns how
  * many there are. The winner re-evaluation of a search is not included. */

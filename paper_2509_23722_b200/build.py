@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libadaptis.so")
 # one translation unit per policy for the segment kernels, compiled in parallel
-SOURCES = ["adaptis_seqg.cu", "adaptis_inst_greedy.cu", "adaptis_inst_zb.cu", "adaptis_inst_onef1b.cu", "adaptis_inst_list.cu",
+SOURCES = ["adaptis_seqg.cu", "adaptis_fixed.cu", "adaptis_inst_greedy.cu", "adaptis_inst_zb.cu", "adaptis_inst_onef1b.cu", "adaptis_inst_list.cu",
            "adaptis_inst_gpipe.cu", "adaptis_host.cu", "adaptis_kernels.cu", "adaptis_executor.cu",
            "adaptis_contend.cu"]
 HEADERS = ["adaptis_internal.h", "adaptis_decode.cuh", "adaptis_seg.cuh"]
@@ -25,7 +25,7 @@ def _inputs():
 
 FLAG_VARS = ("ADAPTIS_GREEDY_MINB", "ADAPTIS_GREEDY_V4_MINB", "ADAPTIS_FIXED_V4_MINB", "ADAPTIS_GREEDY_COMMITS",
              "ADAPTIS_DEBUG", "ADAPTIS_KRUN", "ADAPTIS_GREEDY_ALWAYS_DECIDE", "ADAPTIS_TSTAR_REDUX",
-             "ADAPTIS_SEQG_K", "ADAPTIS_SEQG_COMPACT",
+             "ADAPTIS_SEQG_K",
              "ADAPTIS_ZB_WFILL_ONE")
 STAMP = LIB + ".flags"  # the -D flags the library was built with
 

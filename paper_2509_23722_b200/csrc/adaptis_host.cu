@@ -57,6 +57,9 @@ struct adaptis_prepared {
   int key_bits = 1;
   int tick = kTickI32;
   bool seq_ok = false;  // sequential kernels admitted: U < 2^28, latencies < 2^16
+  // static orders of the fixed-order segments (adaptis_fixed.cu), built on first use
+  struct FxOrder { int policy, placement, v; bool ok; int n, slots; uint32_t* d_ent; };
+  std::vector<FxOrder> fx_orders;
   std::vector<uint64_t> h_binom, h_ball;
   std::vector<int16_t> h_seeds;
   std::vector<int64_t> h_cols, h_comm;  // host copies of the layer columns (kNumCols x L) and comm
@@ -468,6 +471,38 @@ int seq_min_warps() {
   const char* e = getenv("ADAPTIS_SEQ_MINW");
   return e ? atoi(e) : 5;
 }
+// the static order of a GPIPE / ONEF1B / ZB segment for the static-order
+// kernel, built and uploaded once per prepared problem; false when that kernel
+// cannot take the segment (ADAPTIS_NO_FIXED=1 keeps the lane kernels)
+bool fixed_order(adaptis_ctx* ctx, adaptis_prepared* P, SegLaunch& s) {
+  if (s.policy != ADAPTIS_GPIPE && s.policy != ADAPTIS_ONEF1B && s.policy != ADAPTIS_ZB) return false;
+  if (getenv("ADAPTIS_NO_FIXED") || !P->seq_ok) return false;
+  const adaptis_prepared::FxOrder* fo = nullptr;
+  for (const auto& o : P->fx_orders)
+    if (o.policy == s.policy && o.placement == s.placement && o.v == s.v) fo = &o;
+  if (!fo) {
+    adaptis_prepared::FxOrder o{s.policy, s.placement, s.v, false, 0, 0, nullptr};
+    std::vector<uint32_t> ent;
+    if (fx_build_order(s.policy, s.placement, s.p, s.v, s.m, ent, o.slots) && !ent.empty() &&
+        cudaMalloc(&o.d_ent, ent.size() * 4) == cudaSuccess) {
+      if (cudaMemcpy(o.d_ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess) {
+        o.ok = true;
+        o.n = (int)ent.size();
+      } else {
+        cudaFree(o.d_ent);
+        o.d_ent = nullptr;
+      }
+    }
+    (void)ctx;
+    P->fx_orders.push_back(o);
+    fo = &P->fx_orders.back();
+  }
+  if (!fo->ok || !fixed_eligible(s, P->seq_ok, ctx->max_smem, fo->slots)) return false;
+  s.fx_ent = fo->d_ent;
+  s.fx_n = fo->n;
+  s.fx_slots = fo->slots;
+  return true;
+}
 constexpr uint64_t kSeedPass = 4096;  // indices per segment in the pruned search's seed pass
 constexpr size_t kHdr = 8;  // [0] key [1] invalid [2] tasks [3] rounds [4] live lane-rounds [5] pruned
 constexpr size_t kGreedySmemRing = 0;  // per warp: GREEDY rings live in global memory (L2)
@@ -600,6 +635,10 @@ adaptis_status run_jobs(adaptis_ctx* ctx, adaptis_prepared* P, std::vector<Job>&
       // overflows go to the global-ring fallback below like the fast path's
       jobs[i].info.kernel = 1;
       e = launch_seqg(P->tabs, s, ctx->num_sms, ctx->stream);
+    } else if (fixed_order(ctx, P, s)) {
+      // GPIPE / ONEF1B / ZB as one static task order, a thread per candidate
+      jobs[i].info.kernel = 2;
+      e = launch_fixed(P->tabs, s, ctx->num_sms, ctx->stream);
     } else if (direct_global) {
       unsigned grid_limit = 0;
       st = ensure_gring(ctx, P, s, &grid_limit);
@@ -1125,6 +1164,7 @@ void adaptis_prepared_free(adaptis_prepared* P) {
   if (!P) return;
   cudaFree(P->d_cols); cudaFree(P->d_pre); cudaFree(P->d_comm); cudaFree(P->d_colsf); cudaFree(P->d_commf); cudaFree(P->d_binom); cudaFree(P->d_ball);
   cudaFree(P->d_seeds);
+  for (auto& o : P->fx_orders) cudaFree(o.d_ent);
   delete P;
 }
 

@@ -3,6 +3,7 @@
 // (oracle/) shares none of it.
 #pragma once
 #include <cstdint>
+#include <vector>
 
 #include "../../include/adaptis.h"
 
@@ -88,6 +89,10 @@ struct SegLaunch {
   int ring_k;                   // ring slots (fast path: kRingK; fallback: >= m)
   int64_t* gring;               // fallback: global ring scratch
   int tick;                     // kTickI32 (host-proved bound), kTickI64, kTickF32 (fp32 variant)
+  // static-order kernel (adaptis_fixed.cu): the segment's F/B entries and arrival slots
+  const uint32_t* fx_ent;
+  int fx_n;
+  int fx_slots;
 };
 
 // one committed task in report mode (R29): its compute interval and, when its
@@ -175,6 +180,10 @@ int occupancy_ctas_per_sm(const SegLaunch& s, bool fallback);
 // sequential GREEDY kernel (adaptis_seqg.cu): one thread per candidate
 bool seqg_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int min_warps);
 int launch_seqg(const DevTables& t, const SegLaunch& s, int num_sms, void* stream);
+// static-order kernel for GPIPE / ONEF1B / ZB (adaptis_fixed.cu): one thread per candidate
+bool fx_build_order(int policy, int placement, int p, int v, int m, std::vector<uint32_t>& ent, int& slots);
+bool fixed_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int slots);
+int launch_fixed(const DevTables& t, const SegLaunch& s, int num_sms, void* stream);
 size_t smem_bytes(const SegLaunch& s, bool fallback);
 
 }  // namespace adaptis

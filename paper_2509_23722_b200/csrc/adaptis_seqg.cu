@@ -32,9 +32,11 @@
 //
 // Layout. All per-candidate state lives in shared memory as [field][lane]
 // words (conflict-free for any per-lane index): per device the cached key
-// (at << 4 | d), free << 4 | decision, dyn, cap - static, peak; per stage the
-// counters gF | gB << 8 | gW << 16, durations, latencies, act + stash and act
-// bytes, and the K-slot arrival rings of its F and B inputs.
+// (at << 4 | d), free << 4 | decision, room = cap - static - dynamic bytes
+// (and its minimum, for M_d); per stage the counters gF | gB << 8 | gW << 16,
+// the durations (t_F | t_B << 16 and t_W; a stage with t_F or t_B >= 2^16
+// goes to the fallback), latencies, act + stash and act bytes, and the K-slot
+// arrival rings of its F and B inputs.
 #include "adaptis_seg.cuh"
 
 namespace adaptis {
@@ -43,21 +45,12 @@ namespace adaptis {
 #define ADAPTIS_SEQG_K 2
 #endif
 constexpr int kSeqK = ADAPTIS_SEQG_K;   // exact arrival slots per edge (power of two)
-// compact state (off): a stage keeps its two cut rows instead of its durations,
-// latencies and act bytes, which the commit recomputes from the (L1-resident)
-// prefix and latency tables: 1,024 -> 704 B per candidate at p = 8, S = 16 and
-// 9 instead of 6 warps per SM, but the extra load level on every step's
-// critical path costs more (measured on cfg3: 2066 against 1958 ms)
-#ifndef ADAPTIS_SEQG_COMPACT
-#define ADAPTIS_SEQG_COMPACT 0
-#endif
-constexpr bool kSeqCompact = ADAPTIS_SEQG_COMPACT;
 constexpr uint32_t kSeqInf = 0xffffffffu;
 
 // shared-memory rows of one lane (a row is 32 lanes x 4 or 8 bytes)
 struct SeqLayout {
   int key, fd, cnt, dur, lat, rf, rb, n32;  // u32 rows
-  int dyn, capd, peak, as, act, n64;        // u64 rows
+  int room, minroom, as, act, n64;          // u64 rows
 };
 ADAPTIS_LAYOUT_HD constexpr SeqLayout seq_layout(int S, int P2, bool search) {
   SeqLayout l{};
@@ -65,17 +58,16 @@ ADAPTIS_LAYOUT_HD constexpr SeqLayout seq_layout(int S, int P2, bool search) {
   l.key = r; r += P2;
   l.fd = r; r += P2;
   l.cnt = r; r += S + 2;  // guard rows for stages -1 and S
-  l.dur = r; r += kSeqCompact ? S : 3 * S;  // compact: CUT(s) = cuts[s] | cuts[s+1] << 16
-  l.lat = r; r += kSeqCompact ? 0 : S;
+  l.dur = r; r += 2 * S;  // t_F | t_B << 16, t_W (16-bit durations, else the fallback)
+  l.lat = r; r += S;
   l.rf = r; r += kSeqK * S;
   l.rb = r; r += kSeqK * S;
   l.n32 = (r + 1) & ~1;  // keep the u64 rows 8-byte aligned
   r = 0;
-  l.dyn = r; r += P2;
-  l.capd = r; r += P2;
-  l.peak = r; r += search ? 0 : P2;  // per-device peaks are reported in eval mode only
+  l.room = r; r += P2;      // cap - static - dynamic bytes
+  l.minroom = r; r += search ? 0 : P2;  // its minimum (eval mode: M_d = cap - minroom)
   l.as = r; r += S;
-  l.act = r; r += kSeqCompact ? 0 : S;
+  l.act = r; r += S;
   l.n64 = r;
   return l;
 }
@@ -125,22 +117,20 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
   uint32_t* __restrict__ rLAT = w32 + lay.lat * 32 + lane;
   uint32_t* __restrict__ rRF = w32 + lay.rf * 32 + lane;
   uint32_t* __restrict__ rRB = w32 + lay.rb * 32 + lane;
-  int64_t* __restrict__ rDYN = w64 + lay.dyn * 32 + lane;
-  int64_t* __restrict__ rCAPD = w64 + lay.capd * 32 + lane;
-  int64_t* __restrict__ rPEAK = w64 + lay.peak * 32 + lane;
+  int64_t* __restrict__ rROOM = w64 + lay.room * 32 + lane;
+  int64_t* __restrict__ rMINROOM = w64 + lay.minroom * 32 + lane;
   int64_t* __restrict__ rAS = w64 + lay.as * 32 + lane;
   int64_t* __restrict__ rACT = w64 + lay.act * 32 + lane;
 #define KEY(d) rKEY[(d) * 32]
 #define FD(d) rFD[(d) * 32]
 #define CNT(s) rCNT[((s) + 1) * 32]
-#define DUR(k, s) rDUR[((k) * S + (s)) * 32]
-#define CUT(s) rDUR[(s) * 32]
+#define DURFB(s) rDUR[(s) * 32]
+#define DURW(s) rDUR[(S + (s)) * 32]
 #define LAT(s) rLAT[(s) * 32]
 #define RF(k, s) rRF[((k) * S + (s)) * 32]
 #define RB(k, s) rRB[((k) * S + (s)) * 32]
-#define DYN(d) rDYN[(d) * 32]
-#define CAPD(d) rCAPD[(d) * 32]
-#define PEAK(d) rPEAK[(d) * 32]
+#define ROOM(d) rROOM[(d) * 32]
+#define MINROOM(d) rMINROOM[(d) * 32]
 #define AS(s) rAS[(s) * 32]
 #define ACT(s) rACT[(s) * 32]
   const int64_t* pre = tab.pre;  // [kNumCols][L + 1] prefix sums (global, read-only)
@@ -158,7 +148,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
   // ready <= X <= the device's next action time.
   auto decide = [&](int d, uint32_t tnow) {
     const uint32_t free_t = FD(d) >> 4;
-    const int64_t room = CAPD(d) - DYN(d);  // F of stage s fits iff act + stash <= room
+    const int64_t room = ROOM(d);  // F of stage s fits iff act + stash <= room
     uint32_t rf[V], rb[V], rw[V], gf[V], gb[V], gw[V];
     uint32_t rmin = kSeqInf;
 #pragma unroll
@@ -203,7 +193,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
   for (;;) {
     // ---- setup: every lane looks for its next candidate to simulate (a1-a4);
     // invalid decodes and pruned candidates are finalised here
-    bool have = false;
+    bool have = false, wide = false;
     uint64_t idx = 0, slot = 0;
     for (;;) {
       const bool need = !have && !(exhausted && rpos >= rend);
@@ -267,28 +257,29 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
       }
       // a2/a3: stage sums by prefix differences, device statics
 #pragma unroll
-      for (int d = 0; d < P; ++d) {
-        CAPD(d) = sl.cap; DYN(d) = 0; FD(d) = 0;
-        if (!SEARCH) PEAK(d) = 0;
-      }
+      for (int d = 0; d < P; ++d) { ROOM(d) = sl.cap; FD(d) = 0; }
+      wide = false;
       for (int s = 0; s < S; ++s) {
         const int a = cuts[s], b = cuts[s + 1];
         const int ds = sq_dev<PLC, P>(s);
         const int64_t act = PRE(kColAct, b) - PRE(kColAct, a);
         AS(s) = act + (PRE(kColStash, b) - PRE(kColStash, a));
-        CAPD(ds) -= PRE(kColWG, b) - PRE(kColWG, a);  // cap - static (cannot overflow: static >= 0)
-        if constexpr (kSeqCompact) {
-          CUT(s) = (uint32_t)a | ((uint32_t)b << 16);
-        } else {
-          DUR(0, s) = (uint32_t)(PRE(kColTF, b) - PRE(kColTF, a));
-          DUR(1, s) = (uint32_t)(PRE(kColTB, b) - PRE(kColTB, a));
-          DUR(2, s) = (uint32_t)(PRE(kColTW, b) - PRE(kColTW, a));
-          ACT(s) = act;
-          const uint32_t lf = (s < S - 1 && sq_dev<PLC, P>(s + 1) != ds) ? (uint32_t)tab.comm[b - 1] : 0u;
-          const uint32_t lb = (s > 0 && sq_dev<PLC, P>(s - 1) != ds) ? (uint32_t)tab.comm[a - 1] : 0u;
-          LAT(s) = lf | (lb << 16);
-        }
+        ROOM(ds) -= PRE(kColWG, b) - PRE(kColWG, a);  // cap - static (cannot overflow: static >= 0)
+        const int64_t tf = PRE(kColTF, b) - PRE(kColTF, a), tb = PRE(kColTB, b) - PRE(kColTB, a);
+        const int64_t tw = PRE(kColTW, b) - PRE(kColTW, a);
+        // 16-bit durations; a wider stage sends the candidate to the fallback
+        wide = wide || tf >= 65536 || tb >= 65536;
+        DURFB(s) = (uint32_t)tf | ((uint32_t)tb << 16);
+        DURW(s) = (uint32_t)tw;
+        ACT(s) = act;
+        const uint32_t lf = (s < S - 1 && sq_dev<PLC, P>(s + 1) != ds) ? (uint32_t)tab.comm[b - 1] : 0u;
+        const uint32_t lb = (s > 0 && sq_dev<PLC, P>(s - 1) != ds) ? (uint32_t)tab.comm[a - 1] : 0u;
+        LAT(s) = lf | (lb << 16);
         CNT(s) = 0;
+      }
+      if (!SEARCH) {
+#pragma unroll
+        for (int d = 0; d < P; ++d) MINROOM(d) = ROOM(d);  // M_d = static + peak dynamic = cap - min room
       }
       CNT(-1) = 255u;       // guard: stage 0's F input is always there
       CNT(S) = 255u << 8;   // guard: stage S-1's B input is always there
@@ -327,7 +318,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
     if (!__any_sync(FULLMASK, have)) break;
 
     // ---- a5: the event loop, one committed task per step (all lanes in lockstep)
-    bool alive = have, stuck = false, overflow = false;
+    bool alive = have && !wide, stuck = false, overflow = have && wide;
     for (int t = 0; t < T; ++t) {
       if (alive) {
         uint32_t kmin = KEY(0);
@@ -345,27 +336,14 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
           const uint32_t cnt = CNT(s);
           const int sh = 8 * kind;
           const uint32_t j = (cnt >> sh) & 255u;
-          uint32_t dur, latw;
-          int64_t ac;
-          if constexpr (kSeqCompact) {
-            const uint32_t cw = CUT(s);
-            const int a = (int)(cw & 0xffffu), b = (int)(cw >> 16);
-            const int col = kind == 0 ? kColTF : (kind == 1 ? kColTB : kColTW);
-            dur = (uint32_t)(PRE(col, b) - PRE(col, a));
-            ac = PRE(kColAct, b) - PRE(kColAct, a);
-            // latencies of the output edges (R3-R6): 0 between stages of one device
-            const uint32_t lf = (s < S - 1 && sq_dev<PLC, P>(s + 1) != d) ? (uint32_t)__ldg(tab.comm + b - 1) : 0u;
-            const uint32_t lb = (s > 0 && sq_dev<PLC, P>(s - 1) != d) ? (uint32_t)__ldg(tab.comm + (a > 0 ? a - 1 : 0)) : 0u;
-            latw = lf | (lb << 16);
-          } else {
-            dur = DUR(kind, s);
-            ac = ACT(s);
-            latw = LAT(s);
-          }
+          const uint32_t fb = DURFB(s);
+          const uint32_t dur = kind == 0 ? (fb & 0xffffu) : (kind == 1 ? (fb >> 16) : DURW(s));
+          const int64_t ac = ACT(s);
+          const uint32_t latw = LAT(s);
           const uint32_t fin = at + dur;
           // R16: act + stash at F start; act freed at B end, stash at W end
           const int64_t as = AS(s);
-          const int64_t dy = DYN(d) + (kind == 0 ? as : (kind == 1 ? -ac : ac - as));
+          const int64_t room = ROOM(d) - (kind == 0 ? as : (kind == 1 ? -ac : ac - as));
           // the output item: F(s, j) -> F(s+1, j), B(s, j) -> B(s-1, j)
           const bool out = kind == 0 ? s < S - 1 : (kind == 1 && s > 0);
           int tg = kind == 0 ? s + 1 : s - 1;
@@ -378,8 +356,8 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
           const bool ovf = out && j >= (uint32_t)kSeqK && consumed + kSeqK <= j && old > at;
           FD(d) = fin << 4;
           CNT(s) = cnt + (1u << sh);
-          DYN(d) = dy;
-          if (!SEARCH && kind == 0 && dy > PEAK(d)) PEAK(d) = dy;
+          ROOM(d) = room;
+          if (!SEARCH && kind == 0 && room < MINROOM(d)) MINROOM(d) = room;
           if (out) *ring = fin + lat;
           const int d2 = out ? sq_dev<PLC, P>(tg) : d;
           if (ovf) { overflow = true; alive = false; }
@@ -410,7 +388,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
           int64_t mmax = 0;
           double busy = 0;
           for (int d = 0; d < P; ++d) {
-            const int64_t md = (sl.cap - CAPD(d)) + PEAK(d);
+            const int64_t md = sl.cap - MINROOM(d);
             mmax = md > mmax ? md : mmax;
           }
           for (int s = 0; s < S; ++s) {
@@ -431,13 +409,13 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
 #undef KEY
 #undef FD
 #undef CNT
-#undef DUR
+#undef DURFB
+#undef DURW
 #undef LAT
 #undef RF
 #undef RB
-#undef DYN
-#undef CAPD
-#undef PEAK
+#undef ROOM
+#undef MINROOM
 #undef AS
 #undef ACT
   // warp reductions of the key and the counters
