@@ -146,22 +146,42 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
   // the device's own free time) count as arrived: they take the current event
   // time, which the compression argument above admits for any X with
   // ready <= X <= the device's next action time.
-  auto decide = [&](int d, uint32_t tnow) {
-    const uint32_t free_t = FD(d) >> 4;
-    const int64_t room = ROOM(d);  // F of stage s fits iff act + stash <= room
+  // The decision is split into its loads and its arithmetic so that the two
+  // decisions of a step (the committing device and the consumer) issue their
+  // shared-memory loads back to back and overlap their latencies; the free
+  // time comes in a register (the committer's is its finish time).
+  struct DecIn {
+    uint32_t free_t, cnt[V], cp[V], cn[V], sF[V], sB[V];
+    int64_t room, as[V];
+  };
+  auto dec_load = [&](int d, uint32_t free_t, DecIn& in) {
+    in.free_t = free_t;
+    in.room = ROOM(d);  // F of stage s fits iff act + stash <= room
+#pragma unroll
+    for (int c = 0; c < V; ++c) {
+      const int s = sq_stage<PLC, P>(c, d);
+      in.cnt[c] = CNT(s); in.cp[c] = CNT(s - 1); in.cn[c] = CNT(s + 1);
+      in.as[c] = AS(s);
+    }
+#pragma unroll
+    for (int c = 0; c < V; ++c) {
+      const int s = sq_stage<PLC, P>(c, d);
+      in.sF[c] = RF(in.cnt[c] & (kSeqK - 1), s);
+      in.sB[c] = RB((in.cnt[c] >> 8) & (kSeqK - 1), s);
+    }
+  };
+  auto dec_compute = [&](int d, const DecIn& in, uint32_t tnow) {
     uint32_t rf[V], rb[V], rw[V], gf[V], gb[V], gw[V];
     uint32_t rmin = kSeqInf;
 #pragma unroll
     for (int c = 0; c < V; ++c) {
-      const int s = sq_stage<PLC, P>(c, d);
-      const uint32_t cnt = CNT(s), cp = CNT(s - 1), cn = CNT(s + 1);
+      const uint32_t cnt = in.cnt[c];
       const uint32_t gF = cnt & 255u, gB = (cnt >> 8) & 255u, gW = (cnt >> 16) & 255u;
-      const uint32_t prodF = cp & 255u;          // F items produced into s
-      const uint32_t prodB = (cn >> 8) & 255u;   // B items produced into s
-      const uint32_t sF = RF(gF & (kSeqK - 1), s), sB = RB(gB & (kSeqK - 1), s);
-      const uint32_t aF = gF + kSeqK >= prodF ? sF : tnow;
-      const uint32_t aB = gB + kSeqK >= prodB ? sB : tnow;
-      const bool okF = gF < (uint32_t)m && gF < prodF && AS(s) <= room;
+      const uint32_t prodF = in.cp[c] & 255u;          // F items produced into s
+      const uint32_t prodB = (in.cn[c] >> 8) & 255u;   // B items produced into s
+      const uint32_t aF = gF + kSeqK >= prodF ? in.sF[c] : tnow;
+      const uint32_t aB = gB + kSeqK >= prodB ? in.sB[c] : tnow;
+      const bool okF = gF < (uint32_t)m && gF < prodF && in.as[c] <= in.room;
       const bool okB = gB < gF && gB < prodB;
       rf[c] = okF ? aF : kSeqInf;
       rb[c] = okB ? aB : kSeqInf;
@@ -169,7 +189,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
       gf[c] = gF; gb[c] = gB; gw[c] = gW;
       rmin = min(rmin, min(rf[c], min(rb[c], rw[c])));
     }
-    const uint32_t at = max(free_t, rmin);
+    const uint32_t at = max(in.free_t, rmin);
     // the smallest (kind, mb, stage) among the tasks ready by `at`: kind << 10 | mb << 2 | chunk
     uint32_t best = kSeqInf;
 #pragma unroll
@@ -179,7 +199,12 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
       best = min(best, rw[c] <= at ? ((2u << 10) | (gw[c] << 2) | (uint32_t)c) : kSeqInf);
     }
     KEY(d) = rmin == kSeqInf ? kSeqInf : ((at << 4) | (uint32_t)d);
-    FD(d) = (free_t << 4) | ((best >> 10) & 3u) | ((best & 3u) << 2);
+    FD(d) = (in.free_t << 4) | ((best >> 10) & 3u) | ((best & 3u) << 2);
+  };
+  auto decide = [&](int d, uint32_t free_t, uint32_t tnow) {
+    DecIn in;
+    dec_load(d, free_t, in);
+    dec_compute(d, in, tnow);
   };
 
   unsigned long long best_key = ~0ull >> 1, n_inv = 0, n_pr = 0, n_tasks = 0;
@@ -259,14 +284,24 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
 #pragma unroll
       for (int d = 0; d < P; ++d) { ROOM(d) = sl.cap; FD(d) = 0; }
       wide = false;
+      // prefix differences with the running prefix carried (one gather per column and stage)
+      int64_t pv[kNumCols];
+#pragma unroll
+      for (int col = 0; col < kNumCols; ++col) pv[col] = PRE(col, cuts[0]);
       for (int s = 0; s < S; ++s) {
         const int a = cuts[s], b = cuts[s + 1];
         const int ds = sq_dev<PLC, P>(s);
-        const int64_t act = PRE(kColAct, b) - PRE(kColAct, a);
-        AS(s) = act + (PRE(kColStash, b) - PRE(kColStash, a));
-        ROOM(ds) -= PRE(kColWG, b) - PRE(kColWG, a);  // cap - static (cannot overflow: static >= 0)
-        const int64_t tf = PRE(kColTF, b) - PRE(kColTF, a), tb = PRE(kColTB, b) - PRE(kColTB, a);
-        const int64_t tw = PRE(kColTW, b) - PRE(kColTW, a);
+        int64_t dv[kNumCols];
+#pragma unroll
+        for (int col = 0; col < kNumCols; ++col) {
+          const int64_t x = PRE(col, b);
+          dv[col] = x - pv[col];
+          pv[col] = x;
+        }
+        const int64_t act = dv[kColAct];
+        AS(s) = act + dv[kColStash];
+        ROOM(ds) -= dv[kColWG];  // cap - static (cannot overflow: static >= 0)
+        const int64_t tf = dv[kColTF], tb = dv[kColTB], tw = dv[kColTW];
         // 16-bit durations; a wider stage sends the candidate to the fallback
         wide = wide || tf >= 65536 || tb >= 65536;
         DURFB(s) = (uint32_t)tf | ((uint32_t)tb << 16);
@@ -312,7 +347,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
         if ((((unsigned long long)lb << sl.key_bits) | idx) > inc) { ++n_pr; continue; }
       }
 #pragma unroll
-      for (int d = 0; d < P; ++d) decide(d, 0u);
+      for (int d = 0; d < P; ++d) decide(d, 0u, 0u);
       have = true;
     }
     if (!__any_sync(FULLMASK, have)) break;
@@ -354,15 +389,22 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
           const uint32_t consumed = (CNT(tg) >> sh) & 255u;
           // the slot's previous item j-K must be consumed or already arrived
           const bool ovf = out && j >= (uint32_t)kSeqK && consumed + kSeqK <= j && old > at;
-          FD(d) = fin << 4;
+          const int d2 = out ? sq_dev<PLC, P>(tg) : d;
+          // the consumer's free time (read before this step's stores; the
+          // committer's is its finish time, written with its next decision)
+          const uint32_t free2 = d2 == d ? fin : (FD(d2) >> 4);
           CNT(s) = cnt + (1u << sh);
           ROOM(d) = room;
           if (!SEARCH && kind == 0 && room < MINROOM(d)) MINROOM(d) = room;
           if (out) *ring = fin + lat;
-          const int d2 = out ? sq_dev<PLC, P>(tg) : d;
           if (ovf) { overflow = true; alive = false; }
-          decide(d, at);
-          decide(d2, at);  // the consumer (the device itself again when no output)
+          // re-decide the committer and the consumer (the committer itself
+          // again when there is no output: same inputs, same result)
+          DecIn A, B;
+          dec_load(d, fin, A);
+          dec_load(d2, free2, B);
+          dec_compute(d, A, at);
+          dec_compute(d2, B, at);
         }
       }
     }
