@@ -34,9 +34,9 @@
 // words (conflict-free for any per-lane index): per device the cached key
 // (at << 4 | d), free << 4 | decision, room = cap - static - dynamic bytes
 // (and its minimum, for M_d); per stage the counters gF | gB << 8 | gW << 16,
-// the durations (t_F | t_B << 16 and t_W; a stage with t_F or t_B >= 2^16
-// goes to the fallback), latencies, act + stash and act bytes, and the K-slot
-// arrival rings of its F and B inputs.
+// the durations and the latency of its output edge (t_F | t_B << 16 and
+// t_W | latency << 16; a stage with a duration >= 2^16 goes to the fallback),
+// act + stash and act bytes, and the K-slot arrival rings of its F and B inputs.
 #include "adaptis_seg.cuh"
 
 namespace adaptis {
@@ -49,7 +49,7 @@ constexpr uint32_t kSeqInf = 0xffffffffu;
 
 // shared-memory rows of one lane (a row is 32 lanes x 4 or 8 bytes)
 struct SeqLayout {
-  int key, fd, cnt, dur, lat, rf, rb, n32;  // u32 rows
+  int key, fd, cnt, dur, rf, rb, n32;  // u32 rows
   int room, minroom, as, act, n64;          // u64 rows
 };
 ADAPTIS_LAYOUT_HD constexpr SeqLayout seq_layout(int S, int P2, bool search) {
@@ -58,8 +58,7 @@ ADAPTIS_LAYOUT_HD constexpr SeqLayout seq_layout(int S, int P2, bool search) {
   l.key = r; r += P2;
   l.fd = r; r += P2;
   l.cnt = r; r += S + 2;  // guard rows for stages -1 and S
-  l.dur = r; r += 2 * S;  // t_F | t_B << 16, t_W (16-bit durations, else the fallback)
-  l.lat = r; r += S;
+  l.dur = r; r += 2 * S;  // t_F | t_B << 16, t_W | latency of edge (s, s+1) << 16
   l.rf = r; r += kSeqK * S;
   l.rb = r; r += kSeqK * S;
   l.n32 = (r + 1) & ~1;  // keep the u64 rows 8-byte aligned
@@ -114,7 +113,6 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
   uint32_t* __restrict__ rFD = w32 + lay.fd * 32 + lane;
   uint32_t* __restrict__ rCNT = w32 + lay.cnt * 32 + lane;
   uint32_t* __restrict__ rDUR = w32 + lay.dur * 32 + lane;
-  uint32_t* __restrict__ rLAT = w32 + lay.lat * 32 + lane;
   uint32_t* __restrict__ rRF = w32 + lay.rf * 32 + lane;
   uint32_t* __restrict__ rRB = w32 + lay.rb * 32 + lane;
   int64_t* __restrict__ rROOM = w64 + lay.room * 32 + lane;
@@ -125,8 +123,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
 #define FD(d) rFD[(d) * 32]
 #define CNT(s) rCNT[((s) + 1) * 32]
 #define DURFB(s) rDUR[(s) * 32]
-#define DURW(s) rDUR[(S + (s)) * 32]
-#define LAT(s) rLAT[(s) * 32]
+#define DURWL(s) rDUR[(S + (s)) * 32]
 #define RF(k, s) rRF[((k) * S + (s)) * 32]
 #define RB(k, s) rRB[((k) * S + (s)) * 32]
 #define ROOM(d) rROOM[(d) * 32]
@@ -303,13 +300,13 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
         ROOM(ds) -= dv[kColWG];  // cap - static (cannot overflow: static >= 0)
         const int64_t tf = dv[kColTF], tb = dv[kColTB], tw = dv[kColTW];
         // 16-bit durations; a wider stage sends the candidate to the fallback
-        wide = wide || tf >= 65536 || tb >= 65536;
-        DURFB(s) = (uint32_t)tf | ((uint32_t)tb << 16);
-        DURW(s) = (uint32_t)tw;
-        ACT(s) = act;
+        wide = wide || tf >= 65536 || tb >= 65536 || tw >= 65536;
+        // the latency of edge (s, s+1) (R3-R6: 0 between stages of one device)
+        // serves F(s) -> F(s+1) and B(s+1) -> B(s)
         const uint32_t lf = (s < S - 1 && sq_dev<PLC, P>(s + 1) != ds) ? (uint32_t)tab.comm[b - 1] : 0u;
-        const uint32_t lb = (s > 0 && sq_dev<PLC, P>(s - 1) != ds) ? (uint32_t)tab.comm[a - 1] : 0u;
-        LAT(s) = lf | (lb << 16);
+        DURFB(s) = (uint32_t)tf | ((uint32_t)tb << 16);
+        DURWL(s) = (uint32_t)tw | (lf << 16);
+        ACT(s) = act;
         CNT(s) = 0;
       }
       if (!SEARCH) {
@@ -372,9 +369,9 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
           const int sh = 8 * kind;
           const uint32_t j = (cnt >> sh) & 255u;
           const uint32_t fb = DURFB(s);
-          const uint32_t dur = kind == 0 ? (fb & 0xffffu) : (kind == 1 ? (fb >> 16) : DURW(s));
+          const uint32_t wl = DURWL(s);
+          const uint32_t dur = kind == 0 ? (fb & 0xffffu) : (kind == 1 ? (fb >> 16) : (wl & 0xffffu));
           const int64_t ac = ACT(s);
-          const uint32_t latw = LAT(s);
           const uint32_t fin = at + dur;
           // R16: act + stash at F start; act freed at B end, stash at W end
           const int64_t as = AS(s);
@@ -383,7 +380,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
           const bool out = kind == 0 ? s < S - 1 : (kind == 1 && s > 0);
           int tg = kind == 0 ? s + 1 : s - 1;
           tg = tg < 0 ? 0 : (tg > S - 1 ? S - 1 : tg);
-          const uint32_t lat = kind == 0 ? (latw & 0xffffu) : (latw >> 16);
+          const uint32_t lat = (kind == 0 ? wl : DURWL(tg)) >> 16;  // edge (s, s+1) or (s-1, s)
           uint32_t* ring = (kind == 0 ? rRF : rRB) + (((int)(j & (kSeqK - 1)) * S + tg) * 32);
           const uint32_t old = *ring;
           const uint32_t consumed = (CNT(tg) >> sh) & 255u;
@@ -400,11 +397,20 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
           if (ovf) { overflow = true; alive = false; }
           // re-decide the committer and the consumer (the committer itself
           // again when there is no output: same inputs, same result)
-          DecIn A, B;
-          dec_load(d, fin, A);
-          dec_load(d2, free2, B);
-          dec_compute(d, A, at);
-          dec_compute(d2, B, at);
+          // (WAVE placement: one after the other, measured faster there)
+#ifndef ADAPTIS_SEQG_WAVE_OVERLAP
+#define ADAPTIS_SEQG_WAVE_OVERLAP 0
+#endif
+          if constexpr (PLC != ADAPTIS_WAVE || ADAPTIS_SEQG_WAVE_OVERLAP) {
+            DecIn A, B;
+            dec_load(d, fin, A);
+            dec_load(d2, free2, B);
+            dec_compute(d, A, at);
+            dec_compute(d2, B, at);
+          } else {
+            decide(d, fin, at);
+            decide(d2, free2, at);
+          }
         }
       }
     }
@@ -452,8 +458,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
 #undef FD
 #undef CNT
 #undef DURFB
-#undef DURW
-#undef LAT
+#undef DURWL
 #undef RF
 #undef RB
 #undef ROOM
@@ -526,6 +531,8 @@ int launch_seqg(const DevTables& t, const SegLaunch& s, int num_sms, void* strea
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 32, sm);
   if (e != cudaSuccess) return (int)e;
   if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
+  static const int max_cta = getenv("ADAPTIS_SEQ_MAXCTA") ? atoi(getenv("ADAPTIS_SEQ_MAXCTA")) : 0;  // A/B hook
+  if (max_cta > 0 && per_sm > max_cta) per_sm = max_cta;
   unsigned grid = (unsigned)num_sms * (unsigned)per_sm;
   const uint64_t warps_needed = (s.n_pos + 31) / 32;
   if (warps_needed < grid) grid = (unsigned)(warps_needed ? warps_needed : 1);
