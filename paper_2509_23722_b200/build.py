@@ -25,7 +25,7 @@ def _inputs():
 
 FLAG_VARS = ("ADAPTIS_GREEDY_MINB", "ADAPTIS_GREEDY_V4_MINB", "ADAPTIS_FIXED_V4_MINB", "ADAPTIS_GREEDY_COMMITS",
              "ADAPTIS_DEBUG", "ADAPTIS_KRUN", "ADAPTIS_GREEDY_ALWAYS_DECIDE", "ADAPTIS_TSTAR_REDUX",
-             "ADAPTIS_SEQG_K", "ADAPTIS_SEQG_WAVE_OVERLAP",
+             "ADAPTIS_SEQG_K",
              "ADAPTIS_ZB_WFILL_ONE")
 STAMP = LIB + ".flags"  # the -D flags the library was built with
 

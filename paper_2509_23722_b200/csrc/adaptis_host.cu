@@ -469,7 +469,7 @@ int ring_slots(int policy, int m) {
 // on B200); ADAPTIS_SEQ_MINW overrides, ADAPTIS_NO_SEQ disables
 int seq_min_warps() {
   const char* e = getenv("ADAPTIS_SEQ_MINW");
-  return e ? atoi(e) : 5;
+  return e ? atoi(e) : 0;  // 0: the kernel's per-placement default
 }
 // the static order of a GPIPE / ONEF1B / ZB segment for the static-order
 // kernel, built and uploaded once per prepared problem; false when that kernel

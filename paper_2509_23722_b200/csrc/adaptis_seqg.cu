@@ -397,20 +397,11 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
           if (ovf) { overflow = true; alive = false; }
           // re-decide the committer and the consumer (the committer itself
           // again when there is no output: same inputs, same result)
-          // (WAVE placement: one after the other, measured faster there)
-#ifndef ADAPTIS_SEQG_WAVE_OVERLAP
-#define ADAPTIS_SEQG_WAVE_OVERLAP 0
-#endif
-          if constexpr (PLC != ADAPTIS_WAVE || ADAPTIS_SEQG_WAVE_OVERLAP) {
-            DecIn A, B;
-            dec_load(d, fin, A);
-            dec_load(d2, free2, B);
-            dec_compute(d, A, at);
-            dec_compute(d2, B, at);
-          } else {
-            decide(d, fin, at);
-            decide(d2, free2, at);
-          }
+          DecIn A, B;
+          dec_load(d, fin, A);
+          dec_load(d2, free2, B);
+          dec_compute(d, A, at);
+          dec_compute(d2, B, at);
         }
       }
     }
@@ -512,8 +503,11 @@ static SeqFn pick_v(int v, int p, int plc) {
 // m <= 255 (8-bit counters), latencies < 2^16, p in {2, 4, 8, 16} (compile-time
 // placement arithmetic), and a plain position range (no explicit plans,
 // lists or traces; the fallback re-run keeps the global-ring kernel), with
-// `min_warps` warps of state per SM
+// `min_warps` warps of state per SM (0: 4, and 5 for the WAVE placement,
+// measured on cfg5's p = 16 v = 2 segments against the lane kernel: INT 26.6 s
+// against 29.3 s at 4 warps, WAVE 31.0 s against 25.6 s)
 bool seqg_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int min_warps) {
+  if (min_warps <= 0) min_warps = s.placement == ADAPTIS_WAVE ? 5 : 4;
   if (!seq_ok || s.policy != ADAPTIS_GREEDY || s.tick != kTickI32 || s.trace || s.list_cuts ||
       s.list_tasks || s.out_report || s.m > 255 || s.v < 1 || s.v > 4 ||
       (s.p != 2 && s.p != 4 && s.p != 8 && s.p != 16))

@@ -16,15 +16,23 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 
 
-def raw(rep):
+def raw(rep, row=0):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    h, u, v = rows[0], rows[1], rows[2]
+    h, u, v = rows[0], rows[1], rows[2 + row]
     return {h[i]: (v[i], u[i]) for i in range(len(h))}
 
 
-def main(rep):
-    m = raw(rep)
+def n_kernels(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    return max(0, len(list(csv.reader(out.splitlines()))) - 2)
+
+
+def main(rep, row=0):
+    m = raw(rep, row)
+    for k in ("Kernel Name", "Block Size", "Grid Size"):
+        if k in m:
+            print("%-60s %s" % (k, m[k][0]))
     for k in KEYS:
         if k in m:
             print("%-60s %s %s" % (k, m[k][0], m[k][1]))
@@ -55,6 +63,8 @@ def main(rep):
 
 
 if __name__ == "__main__":
+    # one summary per captured kernel (the opcode mix is the report's, all kernels)
     for r in sys.argv[1:]:
-        print("==", r)
-        main(r)
+        for k in range(max(1, n_kernels(r))):
+            print("==", r, "kernel", k)
+            main(r, k)

@@ -11,5 +11,5 @@ timeout 1500 python bench.py --steps 5 --warmup 3 > $D/bench_cfg3.json 2> $D/ben
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $D/bench_cfg3_reference.json 2>&1; echo "ref rc=$?"
 for c in 2 3 4; do timeout 600 python tools/search_breakdown.py $c > $D/breakdown_cfg$c.txt 2>&1; done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $D/launches_cfg3.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --cfg5-steps 0 > $D/ncu_launch.log 2>&1; echo "ncu list rc=$?"
-timeout 1500 ncu --set full --import-source on --clock-control none -k regex:seqg_kernel --launch-skip 1 -c 1 -o $D/dominant -f python tools/search_breakdown.py 3 > $D/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 1500 ncu --set full --import-source on --clock-control none -k regex:seqg_kernel --launch-skip 1 -c 2 -o $D/dominant -f python tools/search_breakdown.py 3 > $D/ncu_full.log 2>&1; echo "ncu full rc=$?"
 timeout 1500 ncu --set full --import-source on --clock-control none -k regex:fixed_kernel --launch-skip 5 -c 1 -o $D/fixed_zb -f python tools/search_breakdown.py 3 > $D/ncu_fixed.log 2>&1; echo "ncu fixed rc=$?"
