@@ -66,12 +66,21 @@ ADAPTIS_LAYOUT_HD size_t fx_smem_bytes(int S, int p, int R, bool zb, bool search
   return (size_t)32 * (4 * l.n32 + 8 * l.n64);
 }
 
-template <int V, bool ZB, bool SEARCH>
+// P: the device count when it is a power of two <= 16 (compile-time W-queue
+// arithmetic), 0 for any other p
+template <int V, int P, bool ZB, bool SEARCH>
 __global__ void __launch_bounds__(32, 16)
 fixed_kernel(const DevTables tab, const SegLaunch sl) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
-  const int L = sl.L, m = sl.m, p = sl.p, S = sl.S, plc = sl.placement;
+  const int L = sl.L, m = sl.m, p = P > 0 ? P : sl.p, S = sl.S, plc = sl.placement;
+  // ZB's k-th pending W of device d is the W of its k-th B: chunk v-1 - (k / p) mod v
+  // (R10 backward order); ZB is enumerated on SEQ (v = 1) and INT placements only (R12)
+  auto w_stage = [&](unsigned k, int d) -> int {
+    if constexpr (V == 1) return d;
+    else if constexpr (P > 0) return (V - 1 - (int)((k / (unsigned)P) % V)) * P + d;
+    else return (V - 1 - (int)((k / (unsigned)p) % V)) * p + d;
+  };
   const FxLayout lay = fx_layout(S, p, sl.fx_slots, ZB, SEARCH);
   uint32_t* __restrict__ w32 = reinterpret_cast<uint32_t*>(smem);
   int64_t* __restrict__ w64 = reinterpret_cast<int64_t*>(smem + (size_t)128 * lay.n32);
@@ -316,8 +325,7 @@ fixed_kernel(const DevTables tab, const SegLaunch sl) {
           int64_t room = ROOM(d);
           const int64_t need = kind == 0 ? AS(s) : INT64_MIN;
           while ((nbwd & 0xffffu) > (nbwd >> 16) && (fr < r || room < need)) {
-            const int k = (int)(nbwd >> 16);
-            const int ws = stage_of(plc, p, V - 1 - ((k / p) % V), d);  // the k-th B of d (R10 order)
+            const int ws = w_stage(nbwd >> 16, d);  // the W of d's oldest pending B
             fr += DW(ws);
             room += AS(ws) - ACT(ws);  // R16: stash freed at W end
             nbwd += 1u << 16;
@@ -346,7 +354,7 @@ fixed_kernel(const DevTables tab, const SegLaunch sl) {
         if constexpr (ZB) {  // the Ws still pending after the last F/B run back to back
           const uint32_t nbwd = NBWD(d);
           for (int k = (int)(nbwd >> 16); k < (int)(nbwd & 0xffffu); ++k)
-            fr += DW(stage_of(plc, p, V - 1 - ((k / p) % V), d));
+            fr += DW(w_stage((unsigned)k, d));
         }
         mk = max(mk, fr);
       }
@@ -501,13 +509,24 @@ bool fx_build_order(int policy, int placement, int p, int v, int m, std::vector<
 }
 
 using FxFn = void (*)(const DevTables, const SegLaunch);
+template <int V, bool ZB, bool SEARCH>
+static FxFn fx_pick_p(int p) {
+  switch (p) {
+    case 1: return fixed_kernel<V, 1, ZB, SEARCH>;
+    case 2: return fixed_kernel<V, 2, ZB, SEARCH>;
+    case 4: return fixed_kernel<V, 4, ZB, SEARCH>;
+    case 8: return fixed_kernel<V, 8, ZB, SEARCH>;
+    case 16: return fixed_kernel<V, 16, ZB, SEARCH>;
+    default: return fixed_kernel<V, 0, ZB, SEARCH>;
+  }
+}
 template <bool ZB, bool SEARCH>
-static FxFn fx_pick_v(int v) {
+static FxFn fx_pick_v(int v, int p) {
   switch (v) {
-    case 1: return fixed_kernel<1, ZB, SEARCH>;
-    case 2: return fixed_kernel<2, ZB, SEARCH>;
-    case 3: return fixed_kernel<3, ZB, SEARCH>;
-    default: return fixed_kernel<4, ZB, SEARCH>;
+    case 1: return fx_pick_p<1, ZB, SEARCH>(p);
+    case 2: return fx_pick_p<2, ZB, SEARCH>(p);
+    case 3: return fx_pick_p<3, ZB, SEARCH>(p);
+    default: return fx_pick_p<4, ZB, SEARCH>(p);
   }
 }
 
@@ -523,6 +542,7 @@ bool fixed_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int slots) {
   const int minw = minw_env > 0 ? minw_env : (s.policy == ADAPTIS_ONEF1B ? 8 : s.policy == ADAPTIS_ZB ? 4 : 2);
   if (!seq_ok || (s.policy != ADAPTIS_GPIPE && s.policy != ADAPTIS_ONEF1B && s.policy != ADAPTIS_ZB) ||
       s.tick != kTickI32 || s.trace || s.list_cuts || s.list_tasks || s.out_report || s.p > 16 ||
+      (s.policy == ADAPTIS_ZB && s.placement == ADAPTIS_WAVE) ||
       s.m > 65535 || s.v < 1 || s.v > 4 || s.S > 64)
     return false;
   const size_t per_warp = fx_smem_bytes(s.S, s.p, slots, s.policy == ADAPTIS_ZB, s.key != nullptr);
@@ -531,8 +551,8 @@ bool fixed_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int slots) {
 
 int launch_fixed(const DevTables& t, const SegLaunch& s, int num_sms, void* stream) {
   const bool zb = s.policy == ADAPTIS_ZB;
-  FxFn f = zb ? (s.key ? fx_pick_v<true, true>(s.v) : fx_pick_v<true, false>(s.v))
-              : (s.key ? fx_pick_v<false, true>(s.v) : fx_pick_v<false, false>(s.v));
+  FxFn f = zb ? (s.key ? fx_pick_v<true, true>(s.v, s.p) : fx_pick_v<true, false>(s.v, s.p))
+              : (s.key ? fx_pick_v<false, true>(s.v, s.p) : fx_pick_v<false, false>(s.v, s.p));
   const size_t sm = fx_smem_bytes(s.S, s.p, s.fx_slots, zb, s.key != nullptr);
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return (int)e;

@@ -36,7 +36,8 @@
 // (and its minimum, for M_d); per stage the counters gF | gB << 8 | gW << 16,
 // the durations and the latency of its output edge (t_F | t_B << 16 and
 // t_W | latency << 16; a stage with a duration >= 2^16 goes to the fallback),
-// act + stash and act bytes, and the K-slot arrival rings of its F and B inputs.
+// act + stash bytes, act bytes (40 bits: the low word and a byte beside the
+// counters), and the K-slot arrival rings of its F and B inputs.
 #include "adaptis_seg.cuh"
 
 namespace adaptis {
@@ -49,16 +50,17 @@ constexpr uint32_t kSeqInf = 0xffffffffu;
 
 // shared-memory rows of one lane (a row is 32 lanes x 4 or 8 bytes)
 struct SeqLayout {
-  int key, fd, cnt, dur, rf, rb, n32;  // u32 rows
-  int room, minroom, as, act, n64;          // u64 rows
+  int key, fd, cnt, dur, actlo, rf, rb, n32;  // u32 rows
+  int room, minroom, as, n64;                 // u64 rows
 };
 ADAPTIS_LAYOUT_HD constexpr SeqLayout seq_layout(int S, int P2, bool search) {
   SeqLayout l{};
   int r = 0;
   l.key = r; r += P2;
   l.fd = r; r += P2;
-  l.cnt = r; r += S + 2;  // guard rows for stages -1 and S
+  l.cnt = r; r += S + 2;  // guard rows for stages -1 and S; bits 24-31: act bytes >> 32
   l.dur = r; r += 2 * S;  // t_F | t_B << 16, t_W | latency of edge (s, s+1) << 16
+  l.actlo = r; r += S;    // act bytes, low 32 bits
   l.rf = r; r += kSeqK * S;
   l.rb = r; r += kSeqK * S;
   l.n32 = (r + 1) & ~1;  // keep the u64 rows 8-byte aligned
@@ -66,7 +68,6 @@ ADAPTIS_LAYOUT_HD constexpr SeqLayout seq_layout(int S, int P2, bool search) {
   l.room = r; r += P2;      // cap - static - dynamic bytes
   l.minroom = r; r += search ? 0 : P2;  // its minimum (eval mode: M_d = cap - minroom)
   l.as = r; r += S;
-  l.act = r; r += S;
   l.n64 = r;
   return l;
 }
@@ -118,7 +119,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
   int64_t* __restrict__ rROOM = w64 + lay.room * 32 + lane;
   int64_t* __restrict__ rMINROOM = w64 + lay.minroom * 32 + lane;
   int64_t* __restrict__ rAS = w64 + lay.as * 32 + lane;
-  int64_t* __restrict__ rACT = w64 + lay.act * 32 + lane;
+  uint32_t* __restrict__ rACTLO = w32 + lay.actlo * 32 + lane;
 #define KEY(d) rKEY[(d) * 32]
 #define FD(d) rFD[(d) * 32]
 #define CNT(s) rCNT[((s) + 1) * 32]
@@ -129,7 +130,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
 #define ROOM(d) rROOM[(d) * 32]
 #define MINROOM(d) rMINROOM[(d) * 32]
 #define AS(s) rAS[(s) * 32]
-#define ACT(s) rACT[(s) * 32]
+#define ACTLO(s) rACTLO[(s) * 32]
   const int64_t* pre = tab.pre;  // [kNumCols][L + 1] prefix sums (global, read-only)
   auto PRE = [&](int col, int row) -> int64_t { return __ldg(pre + (size_t)col * (L + 1) + row); };
 
@@ -299,15 +300,15 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
         AS(s) = act + dv[kColStash];
         ROOM(ds) -= dv[kColWG];  // cap - static (cannot overflow: static >= 0)
         const int64_t tf = dv[kColTF], tb = dv[kColTB], tw = dv[kColTW];
-        // 16-bit durations; a wider stage sends the candidate to the fallback
-        wide = wide || tf >= 65536 || tb >= 65536 || tw >= 65536;
+        // 16-bit durations and 40-bit act bytes; a wider stage sends the candidate to the fallback
+        wide = wide || tf >= 65536 || tb >= 65536 || tw >= 65536 || act >= (1ll << 40);
         // the latency of edge (s, s+1) (R3-R6: 0 between stages of one device)
         // serves F(s) -> F(s+1) and B(s+1) -> B(s)
         const uint32_t lf = (s < S - 1 && sq_dev<PLC, P>(s + 1) != ds) ? (uint32_t)tab.comm[b - 1] : 0u;
         DURFB(s) = (uint32_t)tf | ((uint32_t)tb << 16);
         DURWL(s) = (uint32_t)tw | (lf << 16);
-        ACT(s) = act;
-        CNT(s) = 0;
+        ACTLO(s) = (uint32_t)act;
+        CNT(s) = (uint32_t)((uint64_t)act >> 32) << 24;  // 40-bit act: its high byte above the counters
       }
       if (!SEARCH) {
 #pragma unroll
@@ -371,7 +372,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
           const uint32_t fb = DURFB(s);
           const uint32_t wl = DURWL(s);
           const uint32_t dur = kind == 0 ? (fb & 0xffffu) : (kind == 1 ? (fb >> 16) : (wl & 0xffffu));
-          const int64_t ac = ACT(s);
+          const int64_t ac = (int64_t)(((uint64_t)(cnt >> 24) << 32) | ACTLO(s));
           const uint32_t fin = at + dur;
           // R16: act + stash at F start; act freed at B end, stash at W end
           const int64_t as = AS(s);
@@ -455,7 +456,7 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
 #undef ROOM
 #undef MINROOM
 #undef AS
-#undef ACT
+#undef ACTLO
   // warp reductions of the key and the counters
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long x = __shfl_xor_sync(FULLMASK, best_key, o);
