@@ -353,8 +353,6 @@ seqg_kernel(const DevTables tab, const SegLaunch sl) {
     // ---- a5: the event loop, one committed task per step (all lanes in lockstep)
     bool alive = have && !wide, stuck = false, overflow = have && wide;
     for (int t = 0; t < T; ++t) {
-      // stuck and overflowed candidates stop early; stop when none is left
-      if ((t & 63) == 63 && !__any_sync(FULLMASK, alive)) break;
       if (alive) {
         uint32_t kmin = KEY(0);
 #pragma unroll
