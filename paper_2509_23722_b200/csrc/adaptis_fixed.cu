@@ -538,7 +538,8 @@ static FxFn fx_pick_v(int v, int p) {
 // candidates all run; 4 for ZB and 2 for GPIPE, which decide most candidates at
 // setup (the ZB warm-up check, a4); ADAPTIS_FIXED_MINW overrides all three
 bool fixed_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int slots) {
-  static const int minw_env = getenv("ADAPTIS_FIXED_MINW") ? atoi(getenv("ADAPTIS_FIXED_MINW")) : 0;
+  const char* me = getenv("ADAPTIS_FIXED_MINW");  // read per launch (tests set it)
+  const int minw_env = me ? atoi(me) : 0;
   const int minw = minw_env > 0 ? minw_env : (s.policy == ADAPTIS_ONEF1B ? 8 : s.policy == ADAPTIS_ZB ? 4 : 2);
   if (!seq_ok || (s.policy != ADAPTIS_GPIPE && s.policy != ADAPTIS_ONEF1B && s.policy != ADAPTIS_ZB) ||
       s.tick != kTickI32 || s.trace || s.list_cuts || s.list_tasks || s.out_report || s.p > 16 ||

@@ -105,3 +105,26 @@ def test_lane_kernels_still_exact_when_fixed_disabled(monkeypatch):
         assert all(li["kernel"] != 2 for li in c.launch_info())
     finally:
         c.close()
+
+
+def test_fixed_large_sv_instances_equal_oracle(monkeypatch):
+    """ADAPTIS_FIXED_MINW=1 puts cfg5's p = 16, v = 4 (S = 64) ZB and ONEF1B
+    segments on the static-order kernel (by default they stay on the lane
+    kernel for occupancy): blocks of both equal the oracle."""
+    from paper_2509_23722_b200 import adaptis as A
+    monkeypatch.setenv("ADAPTIS_FIXED_MINW", "1")
+    pr, sp = W.config(5)
+    c = A.Context(0)
+    try:
+        seen = 0
+        for first, n_s, v, cb in _segments(pr, sp):
+            if v != 4 or O.combo(v, cb)[1] not in (W.ZB, W.ONEF1B):
+                continue
+            n = min(48, n_s)
+            got = c.eval_batch(pr, sp, first, n)
+            assert all(li["kernel"] == 2 for li in c.launch_info() if li["candidates"])
+            _compare(got, O.eval_indices(pr, sp, range(first, first + n)), "cfg5 v=4 combo %d" % cb)
+            seen += 1
+        assert seen == 2
+    finally:
+        c.close()
