@@ -534,13 +534,12 @@ static FxFn fx_pick_v(int v, int p) {
 // (seq_ok: U < 2^28, latencies < 2^16), p <= 16, m <= 65535, a plain position
 // range (no explicit plans, lists, traces or reports: the lane kernels keep
 // those), and room for enough warps of state per SM (measured on cfg5's p = 16
-// segments, where the lane kernel is faster below them): 8 for ONEF1B, whose
-// candidates all run; 4 for ZB and 2 for GPIPE, which decide most candidates at
-// setup (the ZB warm-up check, a4); ADAPTIS_FIXED_MINW overrides all three
+// segments, where the lane kernel is faster below them): 4 for ONEF1B and ZB,
+// 2 for GPIPE, which a4 decides at setup; ADAPTIS_FIXED_MINW overrides all three
 bool fixed_eligible(const SegLaunch& s, bool seq_ok, int max_smem, int slots) {
   const char* me = getenv("ADAPTIS_FIXED_MINW");  // read per launch (tests set it)
   const int minw_env = me ? atoi(me) : 0;
-  const int minw = minw_env > 0 ? minw_env : (s.policy == ADAPTIS_ONEF1B ? 8 : s.policy == ADAPTIS_ZB ? 4 : 2);
+  const int minw = minw_env > 0 ? minw_env : (s.policy == ADAPTIS_GPIPE ? 2 : 4);
   if (!seq_ok || (s.policy != ADAPTIS_GPIPE && s.policy != ADAPTIS_ONEF1B && s.policy != ADAPTIS_ZB) ||
       s.tick != kTickI32 || s.trace || s.list_cuts || s.list_tasks || s.out_report || s.p > 16 ||
       (s.policy == ADAPTIS_ZB && s.placement == ADAPTIS_WAVE) ||
