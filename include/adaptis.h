@@ -239,6 +239,22 @@ ADAPTIS_API int            adaptis_ctx_launch_info(const adaptis_ctx* ctx, adapt
  * utilisation = out[0] / out[2]; tasks per warp-round = out[0] / out[1]). */
 ADAPTIS_API void           adaptis_ctx_counters(const adaptis_ctx* ctx, uint64_t out[3]);
 
+/* The static task order the static-order kernel evaluates for a GPIPE /
+ * ONEF1B / ZB segment (Alg. 1 Step 3, under the fixed lists of
+ * readings R9-R11): every device's F/B list merged into one
+ * topological order of the DAG plus list edges, shared by all candidates with
+ * these (policy, placement, p, v, m). Host only, no GPU needed.
+ * entries[i] = stage | kind << 6 (0 F, 1 B) | in_slot << 8 | out_slot << 16 |
+ * device << 24, where a slot (< 255; 255 = none) holds the arrival time of
+ * the item the entry consumes (its F or B input) or produces. *n_entries =
+ * 2 S m; *n_slots = the slots used. Caller owns `entries` (capacity `cap`).
+ * EINVAL: bad arguments, p > 16, S > 64, or the lists deadlock / need more
+ * than 254 slots (the lane kernels then evaluate the segment); EOVERFLOW:
+ * cap < 2 S m (n_entries still set). */
+ADAPTIS_API adaptis_status adaptis_static_order(int32_t policy, int32_t placement, int32_t p, int32_t v,
+                                                int32_t m, uint32_t* entries, uint64_t cap,
+                                                uint64_t* n_entries, int32_t* n_slots);
+
 /* |space| for this problem (the candidate space). EINVAL on an
  * invalid problem/space; EOVERFLOW if the count does not fit in 63 bits. */
 ADAPTIS_API adaptis_status adaptis_space_size(const adaptis_problem* problem, const adaptis_space* space,

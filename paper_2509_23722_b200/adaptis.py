@@ -152,6 +152,10 @@ def lib():
             L.adaptis_ctx_counters.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
             L.adaptis_ctx_launch_info.restype = C.c_int
             L.adaptis_ctx_launch_info.argtypes = [C.c_void_p, C.POINTER(_LaunchInfo), C.c_int]
+            L.adaptis_static_order.restype = st
+            L.adaptis_static_order.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                               C.POINTER(C.c_uint32), C.c_uint64, C.POINTER(C.c_uint64),
+                                               C.POINTER(C.c_int32)]
             L.adaptis_space_size.restype = st
             L.adaptis_space_size.argtypes = [C.POINTER(_Problem), C.POINTER(_Space), C.POINTER(C.c_uint64)]
             L.adaptis_decode.restype = st
@@ -302,6 +306,23 @@ def lower(p: int, plan: dict, lists, repair: bool = True, hoist: bool = True) ->
         raise AdaptisError(st, (lib().adaptis_lower_error() or b"").decode())
     prog = [[tuple(int(x) for x in out[i]) for i in range(int(ooff[d]), int(ooff[d + 1]))] for d in range(p)]
     return {"programs": prog, "repairs": int(nr.value), "hoists": int(nh.value)}
+
+
+def static_order(policy: int, placement: int, p: int, v: int, m: int):
+    """The static-order kernel's task order of a GPIPE / ONEF1B / ZB segment
+    (host-only entry point): a list of (stage, kind, in_slot, out_slot,
+    device) with slot None for no item, and the number of slots."""
+    n = C.c_uint64()
+    ns = C.c_int32()
+    cap = 2 * p * v * m  # 2 S m F/B entries
+    buf = (C.c_uint32 * max(cap, 1))()
+    _check(lib().adaptis_static_order(policy, placement, p, v, m, buf, cap, C.byref(n), C.byref(ns)))
+    out = []
+    for i in range(int(n.value)):
+        e = int(buf[i])
+        ins, outs = (e >> 8) & 255, (e >> 16) & 255
+        out.append((e & 63, (e >> 6) & 1, None if ins == 255 else ins, None if outs == 255 else outs, (e >> 24) & 15))
+    return out, int(ns.value)
 
 
 def space_size(pr: W.Problem, sp: W.Space) -> int:

@@ -1124,6 +1124,25 @@ void adaptis_ctx_counters(const adaptis_ctx* ctx, uint64_t out[3]) {
   for (int i = 0; i < 3; ++i) out[i] = ctx ? ctx->counters[i] : 0;
 }
 
+adaptis_status adaptis_static_order(int32_t policy, int32_t placement, int32_t p, int32_t v, int32_t m,
+                                    uint32_t* entries, uint64_t cap, uint64_t* n_entries, int32_t* n_slots) {
+  if (!n_entries || !n_slots || (!entries && cap)) return fail(nullptr, ADAPTIS_EINVAL, "a pointer argument is NULL");
+  if (policy != ADAPTIS_GPIPE && policy != ADAPTIS_ONEF1B && policy != ADAPTIS_ZB)
+    return fail(nullptr, ADAPTIS_EINVAL, "policy = %d is not GPIPE, ONEF1B or ZB", policy);
+  if (placement < ADAPTIS_SEQ || placement > ADAPTIS_WAVE || p < 1 || v < 1 || m < 1 ||
+      (placement == ADAPTIS_SEQ) != (v == 1) || (v > 1 && m % p != 0))
+    return fail(nullptr, ADAPTIS_EINVAL, "placement %d, p %d, v %d, m %d is not an R12 combination", placement, p, v, m);
+  std::vector<uint32_t> ent;
+  int slots = 0;
+  if (!fx_build_order(policy, placement, p, v, m, ent, slots))
+    return fail(nullptr, ADAPTIS_EINVAL, "no static order (p > 16, S > 64, deadlocking lists or > 254 slots)");
+  *n_entries = ent.size();
+  *n_slots = slots;
+  if (cap < ent.size()) return fail(nullptr, ADAPTIS_EOVERFLOW, "cap %llu < %zu entries", (unsigned long long)cap, ent.size());
+  std::copy(ent.begin(), ent.end(), entries);
+  return ADAPTIS_OK;
+}
+
 adaptis_status adaptis_space_size(const adaptis_problem* problem, const adaptis_space* space,
                                   uint64_t* n_out) {
   if (!n_out) return fail(nullptr, ADAPTIS_EINVAL, "n_out is NULL");
