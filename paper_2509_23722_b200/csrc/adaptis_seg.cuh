@@ -256,7 +256,7 @@ __device__ __forceinline__ uint64_t pos_to_index(const SegLaunch& sl, uint64_t p
 #define ADAPTIS_GREEDY_MINB 5
 #endif
 #ifndef ADAPTIS_GREEDY_V4_MINB
-#define ADAPTIS_GREEDY_V4_MINB 4
+#define ADAPTIS_GREEDY_V4_MINB 3  // cfg5 p = 16 v = 4: 3 CTAs 4.32 / 3.58 s, 4 CTAs 4.45 / 3.69 s, 2 CTAs 5.43 / 4.51 s
 #endif
 #ifndef ADAPTIS_FIXED_V4_MINB
 #define ADAPTIS_FIXED_V4_MINB 4
