@@ -253,8 +253,8 @@ __device__ __forceinline__ uint64_t pos_to_index(const SegLaunch& sl, uint64_t p
 // runs best at <= 102 registers (5 CTAs of 4 warps per SM); GREEDY with its
 // rings in global memory so that shared memory does not cap occupancy
 #ifndef ADAPTIS_GREEDY_MINB
-#define ADAPTIS_GREEDY_MINB 5
-#endif
+#define ADAPTIS_GREEDY_MINB 4  // round 2: the lane kernel's GREEDY v <= 2 now runs mainly cfg5's p = 16 WAVE
+#endif                         // segment: 4 CTAs 24.5 s, 5 CTAs 25.7 s, 3 CTAs 27.1 s
 #ifndef ADAPTIS_GREEDY_V4_MINB
 #define ADAPTIS_GREEDY_V4_MINB 3  // cfg5 p = 16 v = 4: 3 CTAs 4.32 / 3.58 s, 4 CTAs 4.45 / 3.69 s, 2 CTAs 5.43 / 4.51 s
 #endif
